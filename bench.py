@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the batched full-order PIC step (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One "step" = one fused gather-kick-drift-deposit pass over all Np x p particles
+plus the per-instance Poisson solve (picrom_pic_push + picrom_pic_solve), on
+device-resident state; the default workload is BASELINE.json configs[1] (C2:
+two-stream, p = 32 instances x 250,000 particles, Nx = 128, cubic splines).
+L2 is flushed (256 MiB write, outside the timed events) between timed steps.
+Multi-GPU (torchrun): every rank runs its own independent C2 batch (instance
+sharding, no collective on the data path; weak scaling); time = max over ranks.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+numpy oracle port in oracle/, all host cores via column threads like
+VlasovSystem(workers=...)) on the same config; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "particle-pushes/s (Np x p x steps) fp64 on 1 B200; % of HBM roofline"
+UNIT = "pushes/s"
+BYTES_PER_PUSH = 32          # x, v read + write, fp64
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.rows = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        threading.Thread(target=self._read, daemon=True).start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        time.sleep(0.05)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_oracle_rate(w, seconds=10.0, max_steps=20, warm=1):
+    """Reference algorithm on the host cores: oracle port, column threads."""
+    from oracle import fe_bspline as fe
+    from oracle import pic_loop
+    from paper_2201_05555_b200 import workloads as wl
+    cores = len(os.sched_getaffinity(0))
+    x, v = wl.generate(w)
+    n, p = x.shape
+    L = float(w.lengths[0])
+    sysm = pic_loop.System(fe.Mesh(L, w.num_cells, w.degree), fe.Charge(n, L), workers=cores)
+    st = pic_loop.Stepper(sysm)
+    t = 0.0
+    for _ in range(warm):
+        x, v, t = st.step(x, v, t, w.dt)
+    steps, t0 = 0, time.perf_counter()
+    while steps < max_steps:
+        x, v, t = st.step(x, v, t, w.dt)
+        steps += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    return n * p * steps / el, cores, steps, el
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    from oracle import fe_bspline as fe
+    from oracle import pic_loop
+    from paper_2201_05555_b200 import workloads as wl
+    cores = len(os.sched_getaffinity(0))
+    x, v = wl.generate(w)
+    n, p = x.shape
+    L = float(w.lengths[0])
+    sysm = pic_loop.System(fe.Mesh(L, w.num_cells, w.degree), fe.Charge(n, L), workers=cores)
+    st = pic_loop.Stepper(sysm)
+    t = 0.0
+    for _ in range(args.warmup):
+        x, v, t = st.step(x, v, t, w.dt)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x, v, t = st.step(x, v, t, w.dt)
+    el = time.perf_counter() - t0
+    val = n * p * args.steps / el
+    sample = (f"{w.name} full size ({p} x {n} particles), {args.steps} reference-order Verlet "
+              f"steps (fullorder.py:122-134) of the numpy oracle port, degree {w.degree}, "
+              f"{cores} column threads")
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": w.describe() | {"parallelism": "host threads"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, w, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2201_05555_b200 import _build, _lib
+    from paper_2201_05555_b200 import _device as dev
+    from paper_2201_05555_b200 import fem, fullorder
+    from paper_2201_05555_b200 import workloads as wl
+    _build.build()
+    _lib.load()
+
+    # weak scaling: each rank owns an independent batch (distinct seed)
+    if world > 1:
+        w = wl.config(w.name, seed=w.seed + rank)
+    xh, vh = wl.generate(w, layout="pn")                 # (p, N) host
+    p, n = xh.shape
+    L = float(w.lengths[0])
+    sysm = fullorder.VlasovSystem(fem.build_mesh(L, w.num_cells, w.degree), fem.ChargeConfig(n, L))
+    xd = torch.from_numpy(xh).cuda()
+    vd = torch.from_numpy(vh).cuda()
+    total_steps = args.warmup + args.steps + 1
+    run = fullorder.PicRun(sysm, xd, vd, w.dt, total_steps)
+    run.init_field()
+    run.advance(1)                      # the half-kick first step
+    s = dev.stream_handle()
+    gp = p * run.nx
+
+    def push():
+        _lib.call("picrom_pic_push", run.x.data_ptr(), run.v.data_ptr(), n, p, n,
+                  run.inst.data_ptr(), run.nx, run.degree, run.phi.data_ptr(), run.dt, run.dt,
+                  0.5 * run.dt, 0, run.counter.data_ptr(), run.ws.data_ptr(),
+                  run.status.data_ptr(), s)
+
+    def solve():
+        _lib.call("picrom_pic_solve", n, p, run.nx, run.degree, run.inst.data_ptr(),
+                  run.c.khat.data_ptr(), run.c.stencil.data_ptr(), run.phi.data_ptr(), 0,
+                  run.counter.data_ptr(), run.rho_hist.data_ptr() + 8 * gp,
+                  run.phi_hist.data_ptr() + 8 * gp, run.ee_hist.data_ptr() + 8 * p,
+                  run.kin_hist.data_ptr(), run.ws.data_ptr(), s)
+
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        flush.zero_()
+        push()
+        solve()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()                       # L2 flush outside the timed events
+        evs[k][0].record()
+        push()
+        evs[k][1].record()
+        solve()
+        evs[k][2].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        tdist.barrier()
+    push_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    step_ms = sum(e[0].elapsed_time(e[2]) for e in evs)
+    run.check()
+    t_local = torch.tensor([step_ms, push_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(t_local, op=tdist.ReduceOp.MAX)
+    step_ms, push_ms = float(t_local[0]), float(t_local[1])
+    launches = 2 * args.steps
+
+    # end-to-end: the public call with host (pinned) buffers, full configured run
+    e2e_steps = args.e2e_steps or w.num_steps
+    xn = torch.from_numpy(np.ascontiguousarray(xh.T)).pin_memory()
+    vn = torch.from_numpy(np.ascontiguousarray(vh.T)).pin_memory()
+    del run, xd, vd
+    torch.cuda.empty_cache()
+    ens = fullorder.ParticleEnsemble(xn, vn, 0.0)
+    rec_opts = fullorder.RecordOptions(energy_stride=1, record_snapshots=False)
+    fullorder.run_full_order(sysm, fullorder.ParticleEnsemble(xn[:1000].clone(), vn[:1000].clone(), 0.0),
+                             w.dt, 2 * w.dt, record=rec_opts)   # warm the graph path
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rec = fullorder.run_full_order(sysm, ens, w.dt, e2e_steps * w.dt, record=rec_opts)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    assert rec.final_state.x.device.type == "cpu"
+    e_local = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(e_local, op=tdist.ReduceOp.MAX)
+        e2e_s = float(e_local[0])
+    h2d = 2 * n * p * 8
+    d2h = 2 * n * p * 8 + rec.electric_history.nbytes * 2 + rec.potential_history.nbytes * 2
+
+    if rank != 0:
+        tdist.destroy_process_group()
+        return
+    pushes = n * p * args.steps * world
+    value = pushes / (step_ms / 1e3)
+    peak, peak_src = peaks()
+    push_avg_s = push_ms / 1e3 / args.steps
+    achieved = BYTES_PER_PUSH * n * p / push_avg_s / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(w.name, {}).get("traffic_bytes_per_launch")
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rate, cores, cs, el = cpu_oracle_rate(w)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{w.name} full size ({p} x {n}), {cs} Verlet steps in {el:.1f} s, numpy "
+                         f"oracle port (degree {w.degree}), {cores} column threads"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded two-stream loading, SURVEY.md §8(d))",
+        "config": w.describe() | {"parallelism": f"instances, {world} rank(s), no data-path collective",
+                                  "l2": "flushed between timed steps (256 MiB write outside events)",
+                                  "state_bytes": 2 * n * p * 8},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "step_kernel (fused gather-kick-drift-deposit)",
+                     "algorithmic_bytes_per_launch": BYTES_PER_PUSH * n * p,
+                     "avg_launch_ms": push_ms / args.steps, "peak_source": peak_src},
+        "kernel_share_of_step": push_ms / step_ms,
+        "e2e": {"value": n * p * e2e_steps * world / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": h2d / e2e_steps, "d2h_bytes_per_step": d2h / e2e_steps,
+                "call": f"fullorder.run_full_order({e2e_steps} steps) from pinned host (N,p) "
+                        "arrays, host record + final state back", "seconds": e2e_s},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    from paper_2201_05555_b200 import workloads as wl
+    w = wl.config(args.config)
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+    else:
+        run_ours(args, w, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

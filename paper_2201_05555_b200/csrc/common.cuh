@@ -1,0 +1,187 @@
+// Shared device helpers: locate, B-spline weights, cell polynomials, status.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/picrom_b200.h"
+
+namespace picrom {
+
+// per-instance parameter row (PICROM_INST_STRIDE doubles)
+enum InstField { I_H = 0, I_INVH = 1, I_QW = 2, I_BGH = 3, I_ECOEF = 4, I_GCOEF = 5,
+                 I_HALFINVMP = 6, I_LENGTH = 7 };
+
+constexpr int kThreads = 256;
+
+// Python-style (non-negative) c mod nx of an integer-valued double, matching
+// numpy's `cell.astype(np.int64) % nx` (fem.py:115) including the saturating
+// out-of-range cast (numpy yields INT64_MIN for NaN/inf/huge).
+__device__ __forceinline__ int cell_mod(double c, int nx, double inv_nx) {
+  if (fabs(c) < 2147483648.0) {
+    int ci = static_cast<int>(c);
+    int q = __double2int_rd(static_cast<double>(ci) * inv_nx);
+    int r = ci - q * nx;
+    if (r < 0) r += nx;
+    if (r >= nx) r -= nx;
+    return r;
+  }
+  long long ci;
+  if (fabs(c) < 9223372036854775808.0) ci = static_cast<long long>(c);
+  else ci = (long long)(-9223372036854775807LL - 1);
+  long long r = ci % nx;
+  if (r < 0) r += nx;
+  return static_cast<int>(r);
+}
+
+// fem._locate arithmetic (fem.py:112-115): s = x / h (IEEE division), cell =
+// floor(s), frac = s - cell (exact), i0 = cell mod nx.
+__device__ __forceinline__ void locate(double x, double h, int nx, double inv_nx,
+                                       int& i0, double& frac) {
+  double s = __ddiv_rn(x, h);
+  double c = floor(s);
+  frac = __dsub_rn(s, c);
+  i0 = cell_mod(c, nx, inv_nx);
+}
+
+template <int D> struct Spline;
+
+// P1 hat functions -- fem.py:179-200 exactly (weights 1-f, f; gradient -1/h, 1/h)
+template <> struct Spline<1> {
+  static constexpr int OFF = 0;     // first node = cell + OFF
+  __device__ static __forceinline__ void weights(double f, double* w) {
+    w[0] = __dsub_rn(1.0, f);
+    w[1] = f;
+  }
+  __device__ static __forceinline__ void dweights(double f, double g, double* w) {
+    w[0] = -g;
+    w[1] = g;
+  }
+};
+
+// quadratic: nodes c-1, c, c+1; weights N_2(f+2), N_2(f+1), N_2(f)
+template <> struct Spline<2> {
+  static constexpr int OFF = -1;
+  __device__ static __forceinline__ void weights(double f, double* w) {
+    double g = 1.0 - f;
+    double e = f - 0.5;
+    w[0] = 0.5 * g * g;
+    w[1] = 0.75 - e * e;
+    w[2] = 0.5 * f * f;
+  }
+  __device__ static __forceinline__ void dweights(double f, double g, double* w) {
+    w[0] = (f - 1.0) * g;
+    w[1] = (1.0 - 2.0 * f) * g;
+    w[2] = f * g;
+  }
+};
+
+// cubic: nodes c-1..c+2; weights N_3(f+3), N_3(f+2), N_3(f+1), N_3(f)
+template <> struct Spline<3> {
+  static constexpr int OFF = -1;
+  __device__ static __forceinline__ void weights(double f, double* w) {
+    const double s6 = 1.0 / 6.0;
+    double g = 1.0 - f;
+    double f2 = f * f;
+    w[0] = g * g * g * s6;
+    w[1] = (2.0 / 3.0) - f2 + 0.5 * f2 * f;
+    w[2] = s6 + 0.5 * (f + f2 - f2 * f);
+    w[3] = f2 * f * s6;
+  }
+  __device__ static __forceinline__ void dweights(double f, double g, double* w) {
+    const double e = 1.0 - f;
+    w[0] = (-0.5 * e * e) * g;
+    w[1] = (1.5 * f * f - 2.0 * f) * g;
+    w[2] = (-1.5 * f * f + f + 0.5) * g;
+    w[3] = (0.5 * f * f) * g;
+  }
+};
+
+__device__ __forceinline__ int wrap_node(int q, int nx) {
+  q %= nx;
+  return q < 0 ? q + nx : q;
+}
+
+// Per-cell polynomial coefficients of the gathered quantity in the in-cell
+// fraction f:  value  sum_m phi_m N_d(f+d-m)            (D+1 coefficients)
+//              deriv  coef * sum_m phi_m dN_d/dx(...)    (D coefficients)
+// phi_m = phi[(c + OFF + m) mod nx].  D = 1 deriv keeps the reference's
+// operation order coef * ((-g)*phi0 + g*phi1) (fem.py:146,188-190,256).
+template <int D>
+__device__ __forceinline__ void deriv_coeffs(const double* ph, double coef, double g, double* C) {
+  if constexpr (D == 1) {
+    C[0] = __dmul_rn(coef, __dadd_rn(__dmul_rn(-g, ph[0]), __dmul_rn(g, ph[1])));
+  } else if constexpr (D == 2) {
+    double s = coef * g;
+    C[0] = s * (ph[1] - ph[0]);
+    C[1] = s * (ph[0] - 2.0 * ph[1] + ph[2]);
+  } else {
+    double s = coef * g;
+    C[0] = s * 0.5 * (ph[2] - ph[0]);
+    C[1] = s * (ph[0] - 2.0 * ph[1] + ph[2]);
+    C[2] = s * (-0.5 * ph[0] + 1.5 * ph[1] - 1.5 * ph[2] + 0.5 * ph[3]);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void value_coeffs(const double* ph, double* C) {
+  if constexpr (D == 1) {
+    C[0] = ph[0];
+    C[1] = ph[1];       // evaluated directly as (1-f)*phi0 + f*phi1
+  } else if constexpr (D == 2) {
+    C[0] = 0.5 * (ph[0] + ph[1]);
+    C[1] = ph[1] - ph[0];
+    C[2] = 0.5 * ph[0] - ph[1] + 0.5 * ph[2];
+  } else {
+    const double s6 = 1.0 / 6.0;
+    C[0] = (ph[0] + 4.0 * ph[1] + ph[2]) * s6;
+    C[1] = 0.5 * (ph[2] - ph[0]);
+    C[2] = 0.5 * (ph[0] - 2.0 * ph[1] + ph[2]);
+    C[3] = (-ph[0] + 3.0 * ph[1] - 3.0 * ph[2] + ph[3]) * s6;
+  }
+}
+
+// Horner in f over NC coefficients (C[0] + f*C[1] + ...)
+template <int NC>
+__device__ __forceinline__ double horner(const double* C, double f) {
+  double r = C[NC - 1];
+#pragma unroll
+  for (int k = NC - 2; k >= 0; --k) r = fma(r, f, C[k]);
+  return r;
+}
+
+__device__ __forceinline__ void record_bad(unsigned long long* status, long long step,
+                                           long long row, int col, int p) {
+  if (status) {
+    unsigned long long lin = (unsigned long long)row * (unsigned long long)p + (unsigned long long)col;
+    atomicMin(status, ((unsigned long long)step << 40) | lin);
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// deterministic block reduction (fixed tree); all threads get the result
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  int nw = (blockDim.x + 31) >> 5;
+  if (w == 0) {
+    t = l < nw ? red[l] : 0.0;
+    t = warp_sum(t);
+    if (l == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+}  // namespace picrom
