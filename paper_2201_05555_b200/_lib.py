@@ -31,7 +31,7 @@ SIGNATURES = {
     "picrom_field_energy": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "picrom_gather": (_i, [_vp, _ll, _i, _ll, _vp, _i, _i, _vp, _i, _vp, _ll, _vp, _vp]),
     "picrom_pic_step": (_i, [_vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _vp, _vp,
-                             _d, _d, _d, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+                             _d, _d, _d, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "picrom_pic_push": (_i, [_vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _d, _d, _d, _ll, _vp,
                              _vp, _vp, _vp]),
     "picrom_pic_solve": (_i, [_ll, _i, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp,
@@ -49,8 +49,18 @@ _lib = None
 
 def header_symbols():
     """Function names declared in include/picrom_b200.h."""
-    text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(picrom_\w+)\s*\(", text, re.M)))
+    return sorted(header_arity())
+
+
+def header_arity():
+    """{name: number of parameters} parsed from the header's declarations."""
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    out = {}
+    for m in re.finditer(r"^\s*(?:int|size_t|const char\*)\s+(picrom_\w+)\s*\(([^)]*)\)\s*;",
+                         text, re.M):
+        params = m.group(2).strip()
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
 
 
 def load():

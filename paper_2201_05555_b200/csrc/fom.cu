@@ -278,9 +278,8 @@ step_kernel(StepArgs a) {
     const int seg = blockIdx.x + j;
     for (int nd = tid; nd < nx; nd += kThreads) {
       double s = 0.0;
-      // histogram row r holds node (r + OFF) mod nx
-      for (int r = nd - Spline<D>::OFF; r < nh; r += nx) {
-        if (r < 0) continue;
+      // histogram row r holds node (r + OFF) mod nx: rows r0, r0 + nx, ... < nh
+      for (int r = (nd - Spline<D>::OFF) % nx; r < nh; r += nx) {
         const double* row = hist + (size_t)r * H;
         for (int hh = 0; hh < H; ++hh) s += row[hh];
       }

@@ -14,6 +14,12 @@ def test_header_and_bindings_agree():
     assert declared == set(_lib.SIGNATURES), (declared ^ set(_lib.SIGNATURES))
 
 
+def test_binding_arity_matches_header():
+    arity = _lib.header_arity()
+    for name, (_, args) in _lib.SIGNATURES.items():
+        assert len(args) == arity[name], (name, len(args), arity[name])
+
+
 def test_library_exports_every_declared_symbol(lib_built):
     for name in _lib.header_symbols():
         assert hasattr(lib_built, name), name
