@@ -191,12 +191,14 @@ def run_ours(args, w, rank, world, local_rank):
                   0.5 * run.dt, 0, run.counter.data_ptr(), run.ws.data_ptr(),
                   run.status.data_ptr(), s)
 
-    def solve():
+    def solve(hist=True):
         _lib.call("picrom_pic_solve", n, p, run.nx, run.degree, run.inst.data_ptr(),
                   run.c.khat.data_ptr(), run.c.stencil.data_ptr(), run.phi.data_ptr(), 0,
-                  run.counter.data_ptr(), run.rho_hist.data_ptr() + 8 * gp,
-                  run.phi_hist.data_ptr() + 8 * gp, run.ee_hist.data_ptr() + 8 * p,
-                  run.kin_hist.data_ptr(), run.ws.data_ptr(), s)
+                  run.counter.data_ptr(),
+                  run.rho_hist.data_ptr() + 8 * gp if hist else None,
+                  run.phi_hist.data_ptr() + 8 * gp if hist else None,
+                  run.ee_hist.data_ptr() + 8 * p if hist else None,
+                  run.kin_hist.data_ptr() if hist else None, run.ws.data_ptr(), s)
 
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
     for _ in range(args.warmup):
@@ -211,6 +213,17 @@ def run_ours(args, w, rank, world, local_rank):
         tdist.barrier()
     torch.cuda.synchronize()
     clocks.start()
+    # soak (untimed) so the 200 ms nvidia-smi sampler sees the clocks under
+    # this exact load; the timed K steps follow immediately
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 1.0:
+        for _ in range(10):
+            flush.zero_()
+            push()
+            solve(hist=False)
+        torch.cuda.synchronize()
+    run.counter[0] = args.warmup + 1        # history rows of the timed steps
+    torch.cuda.synchronize()
     for k in range(args.steps):
         flush.zero_()                       # L2 flush outside the timed events
         evs[k][0].record()

@@ -177,6 +177,91 @@ int picrom_transpose(const double* in, long long rows, long long cols,
 int picrom_transpose_i64(const long long* in, long long rows, long long cols,
                          long long* out, void* stream);
 
+/* ---------------------------------------------------------------- ROM --- */
+/* Reduced basis U (2N x n) row-major: rows [0, N) = U_X, [N, 2N) = U_V;
+ * coefficients Z (n x p') row-major with leading dimension ldz; `cols`
+ * (nullable) maps each column of Z to its instance row in `inst` (per-instance
+ * meshes, BASELINE C3/C4). */
+
+/* Scratch for the reduced-basis calls at (N, p', n, nx). */
+size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx);
+
+/* Field half of driver.exact_gradients (driver.py:70-73): X_r = U_X Z is
+ * formed in registers, deposited, and each column solved:
+ * phi/rho (p', nx), energy (p') -- each may be NULL. */
+int picrom_rom_field(const double* ux, long long N, int n, const double* z, int ldz,
+                     int p, const int* cols, const double* inst, int nx, int degree,
+                     const double* khat, const double* stencil, double* phi,
+                     double* rho, double* energy, void* workspace,
+                     unsigned long long* status, void* stream);
+
+/* Gather half (driver.py:74-76, make_full_stage driver.py:83-85):
+ * E = coef * d/dx (phi . lambda)(U_X Z) with coef = qw/m_p (coef_kind 0) or 1
+ * (coef_kind 1); g_out (n x p', leading dim ldg) = U_X^T E (nullable);
+ * lam (N x p', row stride ldo) = (phi . lambda)(U_X Z) (DEIM harvest,
+ * nullable); eout (N x p', row stride ldo) = E (nullable). */
+int picrom_rom_gather(const double* ux, long long N, int n, const double* z, int ldz,
+                      int p, const int* cols, const double* inst, int nx, int degree,
+                      const double* phi, int coef_kind, double* g_out, int ldg,
+                      double* lam, double* eout, long long ldo, void* workspace,
+                      unsigned long long* status, void* stream);
+
+/* out (w x w) = W^T W, W = [B_0 | ... | B_{k-1}] the column concatenation of k
+ * tall blocks with N rows (block i: ptrs[i], row stride lds[i], widths[i]
+ * columns; jswap[i] = 1 uses J B_i, the block with its row halves swapped and
+ * the new lower half negated -- reduction.jmul, reduction.py:44-47), w <= 128,
+ * k <= 8; jswap may be NULL.  Every n x n product of reduction.py:143-182 (and
+ * the residuals :85-90) is a sub-block of one such Gram. */
+int picrom_paired_gram(int nblocks, const double* const* ptrs, const int* lds,
+                       const int* widths, const int* jswap, long long N, double* out,
+                       void* workspace, void* stream);
+
+/* out (wa x wb) = A^T B with A = blocks [0, na) and B = blocks [na, nblocks)
+ * (same block conventions as picrom_paired_gram; total width <= 256):
+ * the sliding DEIM-window Gram update and the Rayleigh-Ritz products of the
+ * windowed SVD (hyper.py:262). */
+int picrom_cross_gram(int nblocks, int na, const double* const* ptrs, const int* lds,
+                      const int* widths, const int* jswap, long long N, double* out,
+                      void* workspace, void* stream);
+
+/* DEIM greedy selection step (hyper.py:241-244): out_index = the first index
+ * of max |v[i*stride]| over i < n with the `banned` indices scored -1;
+ * out_value (nullable) = that maximum. */
+int picrom_argmax_abs(const double* v, long long n, long long stride,
+                      const long long* banned, int nbanned, long long* out_index,
+                      double* out_value, void* workspace, void* stream);
+
+/* out (N x c, row stride ldo) (+)= sum_t op_t(in_t) (N x widths[t]) @ M_t,
+ * op_t = J when jswap[t] (nullable), M_t (widths[t] x c) at mats + moffs[t]
+ * (device); c <= 32, at most 6 terms. */
+int picrom_combine(int nterms, const double* const* ins, const int* lds,
+                   const int* widths, const int* jswap, const int* moffs,
+                   const double* mats, int mats_len, long long N, double* out, int ldo,
+                   int c, int accumulate, void* stream);
+
+/* Batched DMD extrapolation of the potential (DMDModel.potential,
+ * hyper.py:76-91): re_out (p x nx) = Re(modes (nx x r) . (coords (r x p) * w)),
+ * w_m = exp(omega_m (t - t0)); complex arrays interleaved (re, im), row-major;
+ * im_out (nullable) = the imaginary part (the reference's imag-defect check). */
+int picrom_dmd_extrapolate(const double* modes, const double* coords, const double* w,
+                           int nx, int r, int p, double* re_out, double* im_out,
+                           void* stream);
+
+/* DEIM-sampled gather + projection of the hyper-reduced coefficient gradient
+ * (make_hyper_stage.g, hyper.py:320-328): for each column j,
+ * out[k][j] = inv_mp_j * sum_r uxd[r][k] * dphi_j(uxd[r] . z_j) * w[r] * wscale[j]
+ * with dphi_j the x-derivative of the potential phi (p x nx) on instance j's
+ * mesh; uxd (d x n) = U_X rows at the DEIM indices; wscale nullable (= 1). */
+int picrom_deim_gather(const double* uxd, const double* z, int ldz, const double* phi,
+                       const double* inst, const int* cols, const double* w,
+                       const double* wscale, int d, int n, int p, int nx, int degree,
+                       double* out, int ldo, unsigned long long* status, void* stream);
+
+/* out (d x w) = rows idx of src (row-major, leading dim ld): U_X[I] of
+ * make_hyper_stage (hyper.py:312). */
+int picrom_rows_gather(const double* src, int ld, const long long* idx, int d, int w,
+                       double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,19 @@ SIGNATURES = {
     "picrom_verlet_kick": (_i, [_vp, _vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _d, _vp, _vp, _vp]),
     "picrom_half_sumsq": (_i, [_vp, _ll, _i, _ll, _vp, _vp, _vp]),
     "picrom_transpose": (_i, [_vp, _ll, _ll, _vp, _vp]),
+    "picrom_rom_workspace_bytes": (_sz, [_ll, _i, _i, _i]),
+    "picrom_rom_field": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp,
+                              _vp, _vp, _vp, _vp]),
+    "picrom_rom_gather": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _i,
+                               _vp, _vp, _ll, _vp, _vp, _vp]),
+    "picrom_paired_gram": (_i, [_i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp]),
+    "picrom_cross_gram": (_i, [_i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp]),
+    "picrom_argmax_abs": (_i, [_vp, _ll, _ll, _vp, _i, _vp, _vp, _vp, _vp]),
+    "picrom_combine": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _i, _i, _i, _vp]),
+    "picrom_dmd_extrapolate": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
+    "picrom_deim_gather": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _i,
+                                _vp, _vp]),
+    "picrom_rows_gather": (_i, [_vp, _i, _vp, _i, _i, _vp, _vp]),
     "picrom_transpose_i64": (_i, [_vp, _ll, _ll, _vp, _vp]),
 }
 
@@ -72,7 +85,8 @@ def load():
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python -m paper_2201_05555_b200._build` "
             "(there is no CPU fallback for the hot path)")
-    lib = C.CDLL(str(LIB_PATH))
+    import os
+    lib = C.CDLL(os.environ.get("PICROM_LIB", str(LIB_PATH)))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

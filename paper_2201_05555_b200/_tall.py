@@ -1,0 +1,92 @@
+"""Tall-skinny primitives over device matrices (the two kernels every manifold
+operation of the reduced basis is built from).
+
+* ``gram(blocks)``    -> W^T W on the host (numpy), W = column concatenation of
+                         tall device blocks, optionally J-applied (picrom_paired_gram)
+* ``combine(terms)``  -> sum_t op_t(B_t) @ M_t on the device (picrom_combine)
+
+Tall blocks are row-major float64 CUDA tensors with a common row count; the
+small matrices live on the host and are shipped per call.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _lib
+from .errors import ConfigurationError
+
+_WS = {}
+
+
+def _ws(rows, width):
+    need = int(_lib.query("picrom_rom_workspace_bytes", int(rows), 1, 1, 1))
+    key = torch.cuda.current_device()
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < need:
+        buf = _WS[key] = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device="cuda")
+    return buf
+
+
+def _arr(ctype, vals):
+    return (ctype * len(vals))(*vals)
+
+
+def gram(blocks):
+    """blocks: list of (tensor (M x w_i), jswap) -> numpy (W x W) Gram."""
+    if not blocks:
+        raise ConfigurationError("gram needs at least one block")
+    rows = blocks[0][0].shape[0]
+    for t, _ in blocks:
+        if t.shape[0] != rows or t.dtype != torch.float64 or not t.is_cuda:
+            raise ConfigurationError("gram blocks must be float64 CUDA tensors with equal rows")
+    if len(blocks) > 8:
+        # split into two Grams is not needed by any caller; keep the limit explicit
+        raise ConfigurationError("at most 8 Gram blocks")
+    blocks = [(t if t.is_contiguous() else t.contiguous(), j) for t, j in blocks]
+    widths = [int(t.shape[1]) for t, _ in blocks]
+    W = sum(widths)
+    out = torch.empty((W, W), dtype=torch.float64, device="cuda")
+    _lib.call("picrom_paired_gram", len(blocks),
+              _arr(C.c_void_p, [t.data_ptr() for t, _ in blocks]),
+              _arr(C.c_int, [int(t.stride(0)) for t, _ in blocks]),
+              _arr(C.c_int, widths), _arr(C.c_int, [int(bool(j)) for _, j in blocks]),
+              rows, out.data_ptr(), _ws(rows, W).data_ptr(), dev.stream_handle())
+    return out.cpu().numpy()
+
+
+def combine(terms, out=None, accumulate=False):
+    """terms: list of (tensor (M x a_t), M_t numpy (a_t x c), jswap) -> tensor (M x c)."""
+    rows = terms[0][0].shape[0]
+    c = terms[0][1].shape[1]
+    mats, offs = [], []
+    off = 0
+    for t, m, _ in terms:
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        if m.shape != (t.shape[1], c):
+            raise ConfigurationError(f"combine: matrix {m.shape} does not match block {tuple(t.shape)}")
+        mats.append(m.ravel())
+        offs.append(off)
+        off += m.size
+    buf = torch.from_numpy(np.concatenate(mats)).to("cuda")
+    if out is None:
+        out = torch.empty((rows, c), dtype=torch.float64, device="cuda")
+        accumulate = False
+    ts = [(t if t.is_contiguous() else t.contiguous()) for t, _, _ in terms]
+    _lib.call("picrom_combine", len(terms), _arr(C.c_void_p, [t.data_ptr() for t in ts]),
+              _arr(C.c_int, [int(t.stride(0)) for t in ts]), _arr(C.c_int, [int(t.shape[1]) for t in ts]),
+              _arr(C.c_int, [int(bool(j)) for _, _, j in terms]), _arr(C.c_int, offs),
+              buf.data_ptr(), int(off), rows, out.data_ptr(), int(out.stride(0)), int(c),
+              int(bool(accumulate)), dev.stream_handle())
+    return out
+
+
+def split(G, widths):
+    """Blocks of a Gram: split(G, [a, b])[i][j] is block_i^T block_j."""
+    edges = np.concatenate([[0], np.cumsum(widths)])
+    return [[G[edges[i]:edges[i + 1], edges[j]:edges[j + 1]] for j in range(len(widths))]
+            for i in range(len(widths))]

@@ -16,10 +16,12 @@ constexpr int kThreads = 256;
 
 // Python-style (non-negative) c mod nx of an integer-valued double, matching
 // numpy's `cell.astype(np.int64) % nx` (fem.py:115) including the saturating
-// out-of-range cast (numpy yields INT64_MIN for NaN/inf/huge).
+// out-of-range cast (numpy yields INT64_MIN for NaN/inf/huge).  Power-of-two
+// nx (all BASELINE configs) is a mask of the two's-complement index.
 __device__ __forceinline__ int cell_mod(double c, int nx, double inv_nx) {
   if (fabs(c) < 2147483648.0) {
-    int ci = static_cast<int>(c);
+    const int ci = static_cast<int>(c);
+    if ((nx & (nx - 1)) == 0) return ci & (nx - 1);
     int q = __double2int_rd(static_cast<double>(ci) * inv_nx);
     int r = ci - q * nx;
     if (r < 0) r += nx;
@@ -34,14 +36,50 @@ __device__ __forceinline__ int cell_mod(double c, int nx, double inv_nx) {
   return static_cast<int>(r);
 }
 
+// Correctly rounded x / h from the correctly rounded reciprocal inv_h =
+// RN(1/h) (host-computed): q0 = RN(x*inv_h) is within 1 ulp of x/h, the FMA
+// residual r = x - h*q0 is exact, and RN(q0 + r*inv_h) = RN(x/h) (Markstein's
+// theorem); tiny/huge/non-finite quotients take IEEE division.  Verified against IEEE division in tests/test_fem_gpu.py.
+__device__ __forceinline__ double div_rn(double x, double h, double inv_h) {
+  const double q0 = __dmul_rn(x, inv_h);
+  // outside the range where the residual is exact: plain IEEE division
+  if (!(fabs(q0) > 1e-280 && fabs(q0) < 1e280)) return __ddiv_rn(x, h);
+  const double r = fma(-h, q0, x);
+  return fma(r, inv_h, q0);
+}
+
 // fem._locate arithmetic (fem.py:112-115): s = x / h (IEEE division), cell =
 // floor(s), frac = s - cell (exact), i0 = cell mod nx.
-__device__ __forceinline__ void locate(double x, double h, int nx, double inv_nx,
+__device__ __forceinline__ void locate(double x, double h, double inv_h, int nx, double inv_nx,
                                        int& i0, double& frac) {
-  double s = __ddiv_rn(x, h);
-  double c = floor(s);
+  const double s = div_rn(x, h, inv_h);
+  const double c = floor(s);
   frac = __dsub_rn(s, c);
   i0 = cell_mod(c, nx, inv_nx);
+}
+
+// Branch-free common path of locate(): valid when |x/h| is in (1e-280, 2^31)
+// (then cvt is exact and the Markstein residual exact); `rare` flags the
+// other inputs (tiny/huge/non-finite), which callers re-run through locate()
+// in a warp-uniform fix-up pass.  mask = nx-1 for power-of-two nx, else -1.
+__device__ __forceinline__ void locate_fast(double x, double h, double inv_h, int nx, int mask,
+                                            double inv_nx, int& i0, double& frac, bool& rare) {
+  const double q0 = __dmul_rn(x, inv_h);
+  const double r = fma(-h, q0, x);
+  const double s = fma(r, inv_h, q0);
+  const double c = floor(s);
+  frac = __dsub_rn(s, c);
+  rare = !(fabs(q0) > 1e-280 && fabs(c) < 2147483647.0);
+  const int ci = __double2int_rz(c);
+  if (mask >= 0) {
+    i0 = ci & mask;
+  } else {
+    const int q = __double2int_rd(static_cast<double>(ci) * inv_nx);
+    int rr = ci - q * nx;
+    rr += (rr < 0) ? nx : 0;
+    rr -= (rr >= nx) ? nx : 0;
+    i0 = rr;
+  }
 }
 
 template <int D> struct Spline;

@@ -35,6 +35,10 @@ static int check_launch(const char* what) {
 }
 
 extern "C" const char* picrom_last_error(void) { return g_err; }
+
+// internal (C++ linkage) helpers shared with rom.cu
+int picrom_set_error(int code, const char* msg) { return set_err(code, msg); }
+int picrom_check_launch(const char* what) { return check_launch(what); }
 extern "C" int picrom_version(void) { return 1; }
 
 extern "C" int picrom_device_info(int* num_sms, int* cc_major, int* cc_minor) {
@@ -48,6 +52,9 @@ extern "C" int picrom_device_info(int* num_sms, int* cc_major, int* cc_minor) {
   if (cc_minor) *cc_minor = prop.minor;
   return PICROM_OK;
 }
+
+static int num_sms();
+int picrom_num_sms() { return num_sms(); }
 
 static int num_sms() {
   static int sms = 0;
@@ -69,6 +76,7 @@ static int num_sms() {
 // rows of the CTAs covering [j*N, (j+1)*N) in CTA order -> deterministic.
 
 struct Plan {
+  bool tma;     // leapfrog pass uses the TMA-fed kernel
   int G;        // CTAs
   int K;        // lanes sharing one smem histogram
   int H;        // histograms per CTA
@@ -84,37 +92,56 @@ static int hist_budget_bytes() {
   return b;
 }
 
+static int step_nt() {
+  static int nt = 0;
+  if (!nt) {
+    const char* s = getenv("PICROM_STEP_NT");
+    nt = (s && atoi(s) == 128) ? 128 : 256;
+  }
+  return nt;
+}
+
 static int choose_k(int nx, int degree) {
   int budget = hist_budget_bytes();
   for (int k = 1; k <= 32; k <<= 1) {
-    size_t bytes = (size_t)(nx + degree) * (kThreads / k) * sizeof(double);
+    size_t bytes = (size_t)(nx + degree) * (step_nt() / k) * sizeof(double);
     if ((int)bytes <= budget) return k;
   }
   return 32;
 }
 
 static size_t step_smem(int nx, int degree, int K, bool with_coef) {
-  size_t h = (size_t)(nx + degree) * (kThreads / K) * sizeof(double);
+  size_t h = (size_t)(nx + degree) * (step_nt() / K) * sizeof(double);
   size_t c = with_coef ? (size_t)nx * degree * sizeof(double) : 0;
   return h + c + 64 * sizeof(double);
 }
 
-static int grid_for(long long total, size_t smem) {
-  // one resident wave: SMs x CTAs-per-SM by shared memory, at most 8
-  size_t per_sm = 227 * 1024;
-  int occ = (int)std::min<size_t>(8, std::max<size_t>(1, per_sm / (smem + 1024)));
+static int grid_for(long long total, int occ) {
+  // exactly one resident wave: SMs x CTAs-per-SM (queried for the kernel)
   long long want = (total + 2047) / 2048;     // >= 2048 particles per CTA
-  long long g = std::min<long long>((long long)num_sms() * occ, std::max<long long>(1, want));
+  long long g = std::min<long long>((long long)num_sms() * std::max(occ, 1), std::max<long long>(1, want));
   return (int)g;
 }
+
+static int step_occupancy(int degree, int K, size_t smem);
+
+struct TmaCfg {
+  int ncw, k, stages;
+  size_t smem;
+};
+static bool tma_config(int nx, int degree, TmaCfg* cfg);
 
 static Plan make_plan(long long n, int p, int nx, int degree, bool with_coef) {
   Plan pl;
   pl.K = choose_k(nx, degree);
-  pl.H = kThreads / pl.K;
+  pl.H = step_nt() / pl.K;
   pl.smem = step_smem(nx, degree, pl.K, with_coef);
-  // grid independent of with_coef so workspace sizes agree across calls
-  pl.G = grid_for((long long)n * p, step_smem(nx, degree, pl.K, true));
+  // grid independent of the mode so workspace sizes agree across calls: the
+  // occupancy of the leapfrog kernel (largest smem + registers) sizes it
+  pl.G = grid_for((long long)n * p, step_occupancy(degree, pl.K, step_smem(nx, degree, pl.K, true)));
+  TmaCfg tc;
+  pl.tma = tma_config(nx, degree, &tc) && (long long)n * p >= 4096LL * num_sms();
+  if (pl.tma) pl.G = num_sms();     // one warp-specialised CTA per SM
   return pl;
 }
 
@@ -164,17 +191,41 @@ struct StepArgs {
   const long long* counter;  // optional device step counter (graph replay)
 };
 
-template <int D, int K, int MODE>
-__global__ void __launch_bounds__(kThreads)
+#ifndef PICROM_STEP_U
+#define PICROM_STEP_U 2
+#endif
+
+// exact locate for the rare inputs of locate_fast (kept out of line so the
+// common path stays a straight-line instruction stream)
+struct CellFrac {
+  double f;
+  int c;
+};
+__device__ __noinline__ CellFrac locate_rare(double x, double h, double inv_h, int nx,
+                                             double inv_nx) {
+  CellFrac r;
+  locate(x, h, inv_h, nx, inv_nx, r.c, r.f);
+  return r;
+}
+
+// Fused particle pass.  NT threads; K consecutive lanes share one private
+// smem histogram [row][H] (H = NT/K; bank = histogram id mod 16 for any row,
+// so every access is conflict-free) and take turns (K phases); each lane
+// handles U particles per iteration (u*32 + lane within its warp's 32*U
+// block: coalesced), with the next iteration's loads issued first.
+template <int D, int K, int MODE, int NT>
+__global__ void __launch_bounds__(NT)
 step_kernel(StepArgs a) {
   extern __shared__ double smem[];
-  constexpr int H = kThreads / K;
+  constexpr int H = NT / K;
   constexpr int NW = D + 1;
+  constexpr int U = PICROM_STEP_U;
+  constexpr int SPAN = NT * U;
   const int nx = a.nx;
   const int nh = nx + D;                       // histogram rows incl. ghost nodes
   double* hist = smem;                         // [nh][H]
-  double* coef = hist + (size_t)nh * H;        // [D][nx] field polynomials
-  double* red = coef + (MODE == MODE_LEAPFROG ? (size_t)nx * D : 0);
+  double* coef = hist + nh * H;                // [D][nx] field polynomials
+  double* red = coef + (MODE == MODE_LEAPFROG ? nx * D : 0);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -185,7 +236,9 @@ step_kernel(StepArgs a) {
   const long long start = cta_start(blockIdx.x, T, G);
   const long long end = cta_start(blockIdx.x + 1, T, G);
   const double inv_nx = 1.0 / (double)nx;
+  const int mask = (nx & (nx - 1)) == 0 ? nx - 1 : -1;
   const long long step_id = a.counter ? (*a.counter + 1) : a.step;
+  const int woff = (tid >> 5) * 32 * U + lane;
 
   long long pos = start;
   while (pos < end) {
@@ -193,13 +246,13 @@ step_kernel(StepArgs a) {
     const long long seg_lo = pos - (long long)j * a.n;
     const long long seg_hi = min(a.n, end - (long long)j * a.n);
     const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
-    const double h = ip[I_H];
+    const double h = ip[I_H], inv_h = ip[I_INVH];
 
-    for (int q = tid; q < nh * H; q += kThreads) hist[q] = 0.0;
+    for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
     if constexpr (MODE == MODE_LEAPFROG) {
       const double* ph = a.phi + (size_t)j * nx;
       const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
-      for (int c = tid; c < nx; c += kThreads) {
+      for (int c = tid; c < nx; c += NT) {
         double pv[D + 1];
 #pragma unroll
         for (int m = 0; m <= D; ++m) pv[m] = ph[wrap_node(c + Spline<D>::OFF + m, nx)];
@@ -212,76 +265,147 @@ step_kernel(StepArgs a) {
     __syncthreads();
 
     double kin = 0.0;
-    const size_t base = (size_t)j * a.ld;
-    // warp-uniform trip count so every lane joins the phase-serialised deposit
-    for (long long i0 = seg_lo + (tid & ~31); i0 < seg_hi; i0 += kThreads) {
-      const long long i = i0 + lane;
-      const bool valid = i < seg_hi;
-      double xn = 0.0;
-      if (valid) {
-        if constexpr (MODE == MODE_DEPOSIT) {
-          xn = a.x[base + i];
-        } else if constexpr (MODE == MODE_LEAPFROG) {
-          double x = a.x[base + i];
-          double v = a.v[base + i];
-          int c;
-          double f;
-          locate(x, h, nx, inv_nx, c, f);
+    double* X = a.x + (size_t)j * a.ld;
+    double* V = a.v + (size_t)j * a.ld;
+    const double* E0 = (MODE == MODE_DRIFT) ? a.e0 + (size_t)j * a.ld : nullptr;
+    const double* Y = (MODE == MODE_DEPOSIT && a.y) ? a.y + (size_t)j * a.ld : nullptr;
+    double* XO = (MODE == MODE_DRIFT) ? a.xo + (size_t)j * a.ld : nullptr;
+    double cx[U], cv[U], ce[U];
+    auto load = [&](long long i0, double* lx, double* lv, double* le) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long i = i0 + woff + u * 32;
+        const bool in = i < seg_hi;
+        lx[u] = in ? __ldcs(X + i) : 0.0;
+        if constexpr (MODE == MODE_LEAPFROG || MODE == MODE_DRIFT) lv[u] = in ? __ldcs(V + i) : 0.0;
+        if constexpr (MODE == MODE_DRIFT) le[u] = in ? __ldcs(E0 + i) : 0.0;
+        if constexpr (MODE == MODE_DEPOSIT) lv[u] = (in && Y) ? __ldcs(Y + i) : 1.0;
+      }
+    };
+    if (seg_lo < seg_hi) load(seg_lo, cx, cv, ce);
+    for (long long i0 = seg_lo; i0 < seg_hi; i0 += SPAN) {
+      double px[U], pv[U], pe[U];
+      if (i0 + SPAN < seg_hi) load(i0 + SPAN, px, pv, pe);
+      bool valid[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) valid[u] = i0 + woff + u * 32 < seg_hi;
+
+      // pass 1: the particle update (straight-line common path)
+      double xn[U];
+      if constexpr (MODE == MODE_LEAPFROG) {
+        int c0[U];
+        double f0[U];
+        bool r0[U], any0 = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          locate_fast(cx[u], h, inv_h, nx, mask, inv_nx, c0[u], f0[u], r0[u]);
+          r0[u] = r0[u] && valid[u];
+          any0 |= r0[u];
+        }
+        if (__any_sync(0xffffffffu, any0)) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (r0[u]) {
+              const CellFrac cf = locate_rare(cx[u], h, inv_h, nx, inv_nx);
+              c0[u] = cf.c;
+              f0[u] = cf.f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
           double C[D];
 #pragma unroll
-          for (int k = 0; k < D; ++k) C[k] = coef[k * nx + c];
-          double E = horner<D>(C, f);
-          double vn = v + a.kfull * E;
-          kin = fma(vn, vn, kin);
-          double vh = __dadd_rn(v, __dmul_rn(a.kick, E));
-          xn = __dadd_rn(x, __dmul_rn(a.dt, vh));
-          a.x[base + i] = xn;
-          a.v[base + i] = vh;
-        } else {  // MODE_DRIFT: x1 = x + dt*(v + (0.5*dt)*e0), fullorder.py:127
-          double x = a.x[base + i];
-          double v = a.v[base + i];
-          double e = a.e0[base + i];
-          double vh = __dadd_rn(v, __dmul_rn(a.kick, e));
-          xn = __dadd_rn(x, __dmul_rn(a.dt, vh));
-          a.xo[base + i] = xn;
+          for (int k = 0; k < D; ++k) C[k] = coef[k * nx + c0[u]];
+          const double E = horner<D>(C, f0[u]);
+          const double vn = cv[u] + a.kfull * E;
+          kin = valid[u] ? fma(vn, vn, kin) : kin;
+          const double vh = __dadd_rn(cv[u], __dmul_rn(a.kick, E));
+          xn[u] = __dadd_rn(cx[u], __dmul_rn(a.dt, vh));
+          const long long i = i0 + woff + u * 32;
+          if (valid[u]) {
+            __stcs(X + i, xn[u]);
+            __stcs(V + i, vh);
+          }
         }
-      }
-      const bool ok = valid && isfinite(xn);
-      if (valid && !ok) record_bad(a.status, step_id, i, j, a.p);
-      int c = 0;
-      double f = 0.0;
-      if (ok) locate(xn, h, nx, inv_nx, c, f);
-      double w[NW];
-      if constexpr (MODE == MODE_DEPOSIT) {
-        if (a.wkind == 1) Spline<D>::dweights(f, ip[I_INVH], w);
-        else Spline<D>::weights(f, w);
-        if (a.y && valid) {
-          const double yy = a.y[base + i];
+      } else if constexpr (MODE == MODE_DRIFT) {
 #pragma unroll
-          for (int m = 0; m < NW; ++m) w[m] *= yy;
+        for (int u = 0; u < U; ++u) {
+          const double vh = __dadd_rn(cv[u], __dmul_rn(a.kick, ce[u]));
+          xn[u] = __dadd_rn(cx[u], __dmul_rn(a.dt, vh));
+          if (valid[u]) __stcs(XO + i0 + woff + u * 32, xn[u]);
         }
       } else {
-        Spline<D>::weights(f, w);
+#pragma unroll
+        for (int u = 0; u < U; ++u) xn[u] = cx[u];
       }
+
+      // pass 2: locate the new positions, rare inputs fixed up uniformly
+      int cl[U];
+      double fr[U];
+      bool ok[U], r1[U], any1 = false;
 #pragma unroll
-      for (int q = 0; q < K; ++q) {
-        if (ok && klane == q) {
+      for (int u = 0; u < U; ++u) {
+        ok[u] = valid[u] && isfinite(xn[u]);
+        locate_fast(xn[u], h, inv_h, nx, mask, inv_nx, cl[u], fr[u], r1[u]);
+        r1[u] = r1[u] && valid[u];
+        any1 |= r1[u];
+      }
+      if (__any_sync(0xffffffffu, any1)) {
 #pragma unroll
-          for (int m = 0; m < NW; ++m) hist[(c + m) * H + myh] += w[m];
+        for (int u = 0; u < U; ++u) {
+          if (!r1[u]) continue;
+          if (ok[u]) {
+            const CellFrac cf = locate_rare(xn[u], h, inv_h, nx, inv_nx);
+            cl[u] = cf.c;
+            fr[u] = cf.f;
+          } else {
+            record_bad(a.status, step_id, i0 + woff + u * 32, j, a.p);
+            cl[u] = 0;
+            fr[u] = 0.0;
+          }
         }
-        if constexpr (K > 1) __syncwarp();
       }
+
+      // pass 3: deposit (K lanes per histogram take turns)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double w[NW];
+        if constexpr (MODE == MODE_DEPOSIT) {
+          if (a.wkind == 1) Spline<D>::dweights(fr[u], ip[I_INVH], w);
+          else Spline<D>::weights(fr[u], w);
+          if (Y) {
+#pragma unroll
+            for (int m = 0; m < NW; ++m) w[m] *= cv[u];
+          }
+        } else {
+          Spline<D>::weights(fr[u], w);
+        }
+        const int row = cl[u] * H + myh;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          if (ok[u] && klane == q) {
+            double cur[NW];
+#pragma unroll
+            for (int m = 0; m < NW; ++m) cur[m] = hist[row + m * H];
+#pragma unroll
+            for (int m = 0; m < NW; ++m) hist[row + m * H] = cur[m] + w[m];
+          }
+          if constexpr (K > 1) __syncwarp();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) { cx[u] = px[u]; cv[u] = pv[u]; ce[u] = pe[u]; }
     }
     __syncthreads();
 
     // fold ghost rows, reduce the H histograms in fixed order -> segment row
     const int seg = blockIdx.x + j;
-    for (int nd = tid; nd < nx; nd += kThreads) {
+    for (int nd = tid; nd < nx; nd += NT) {
       double s = 0.0;
       // histogram row r holds node (r + OFF) mod nx: rows r0, r0 + nx, ... < nh
       for (int r = (nd - Spline<D>::OFF) % nx; r < nh; r += nx) {
-        const double* row = hist + (size_t)r * H;
-        for (int hh = 0; hh < H; ++hh) s += row[hh];
+        const double* rowp = hist + r * H;
+        for (int hh = 0; hh < H; ++hh) s += rowp[hh];
       }
       a.seg_hist[(size_t)seg * nx + nd] = s;
     }
@@ -291,6 +415,348 @@ step_kernel(StepArgs a) {
     }
     __syncthreads();
     pos = (long long)(j + 1) * a.n;
+  }
+}
+
+// ------------------------------------------- TMA-fed fused step kernel
+//
+// Warp-specialised version of MODE_LEAPFROG for sm_100a: warp NCW (one elected
+// lane) streams each chunk of x and v into a ring of S shared-memory stages
+// with cp.async.bulk (TMA bulk copies, mbarrier complete_tx), so the bytes in
+// flight per SM (S x 2 x CH x 8) no longer depend on registers or occupancy;
+// the NCW consumer warps keep private (K = 1) or K-lane-shared histograms
+// [row][H] (bank = histogram id mod 16: conflict-free) and write x', v' with
+// streaming stores.  One CTA per SM; same segment/partial layout as
+// step_kernel, so picrom_pic_solve is unchanged.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+constexpr int kTmaU = 4;          // particles per consumer thread per chunk
+
+struct TmaChunk {                 // one chunk of one instance segment
+  long long g0;                   // first element (global index j*ld + i)
+  int cnt;                        // particles
+  int lead;                       // 1 if the copy starts one element early (16 B alignment)
+  int ncopy;                      // elements copied by TMA (even); the rest loaded directly
+};
+
+__device__ __forceinline__ TmaChunk make_chunk(long long g0, int cnt, long long last_valid) {
+  TmaChunk c;
+  c.g0 = g0;
+  c.cnt = cnt;
+  c.lead = (int)(g0 & 1);
+  int nc = ((cnt + c.lead) + 1) & ~1;
+  // never read past the last element of the array
+  while (nc > 0 && g0 - c.lead + nc - 1 > last_valid) nc -= 2;
+  c.ncopy = nc;
+  return c;
+}
+
+template <int D, int K, int NCW>
+__global__ void __launch_bounds__(NCW * 32 + 32, 1) step_tma_kernel(StepArgs a, int S) {
+  constexpr int NC = NCW * 32;
+  constexpr int H = NC / K;
+  constexpr int CH = NC * kTmaU;
+  constexpr int SL = CH + 2;                   // stage length in doubles (lead + round up)
+  constexpr int NW = D + 1;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* stages = reinterpret_cast<double*>(smraw);              // [S][2][SL]
+  const int nx = a.nx;
+  const int nh = nx + D;
+  double* hist = stages + (size_t)S * 2 * SL;                     // [nh + 1][H]
+  double* coef = hist + (size_t)(nh + 1) * H;                     // [D][nx]
+  double* red = coef + (size_t)D * nx;                            // [32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 32);         // [S]
+  uint64_t* empty = full + S;                                     // [S]
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int G = gridDim.x;
+  const long long T = a.n * (long long)a.p;
+  const long long start = cta_start(blockIdx.x, T, G);
+  const long long end = cta_start(blockIdx.x + 1, T, G);
+  const long long last_valid = (long long)(a.p - 1) * a.ld + a.n - 1;
+
+  if (warp == NCW) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      long long pos = start;
+      while (pos < end) {
+        const int j = (int)(pos / a.n);
+        const long long lo = pos - (long long)j * a.n;
+        const long long hi = min(a.n, end - (long long)j * a.n);
+        for (long long c0 = lo; c0 < hi; c0 += CH) {
+          const TmaChunk ck = make_chunk((long long)j * a.ld + c0, (int)min((long long)CH, hi - c0),
+                                         last_valid);
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t bytes = (uint32_t)ck.ncopy * 8u;
+          mbar_expect_tx(&full[stage], 2u * bytes);
+          if (bytes) {
+            double* dx = stages + (size_t)stage * 2 * SL;
+            bulk_g2s(dx, a.x + (ck.g0 - ck.lead), bytes, &full[stage]);
+            bulk_g2s(dx + SL, a.v + (ck.g0 - ck.lead), bytes, &full[stage]);
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        pos = (long long)(j + 1) * a.n;
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int myh = tid / K;
+  const int klane = lane % K;
+  const double inv_nx = 1.0 / (double)nx;
+  const int mask = (nx & (nx - 1)) == 0 ? nx - 1 : -1;
+  const long long step_id = a.counter ? (*a.counter + 1) : a.step;
+  int stage = 0;
+  uint32_t phase = 0;
+  long long pos = start;
+  while (pos < end) {
+    const int j = (int)(pos / a.n);
+    const long long lo = pos - (long long)j * a.n;
+    const long long hi = min(a.n, end - (long long)j * a.n);
+    const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
+    const double h = ip[I_H], inv_h = ip[I_INVH];
+    for (int q = tid; q < nh * H; q += NC) hist[q] = 0.0;
+    {
+      const double* ph = a.phi + (size_t)j * nx;
+      const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
+      for (int c = tid; c < nx; c += NC) {
+        double pv[D + 1];
+#pragma unroll
+        for (int m = 0; m <= D; ++m) pv[m] = ph[wrap_node(c + Spline<D>::OFF + m, nx)];
+        double C[D];
+        deriv_coeffs<D>(pv, ecoef, g, C);
+#pragma unroll
+        for (int k = 0; k < D; ++k) coef[k * nx + c] = C[k];
+      }
+    }
+    consumers_sync(NC);
+    double kin = 0.0;
+    double* X = a.x + (size_t)j * a.ld;
+    double* V = a.v + (size_t)j * a.ld;
+    for (long long c0 = lo; c0 < hi; c0 += CH) {
+      const TmaChunk ck = make_chunk((long long)j * a.ld + c0, (int)min((long long)CH, hi - c0),
+                                     last_valid);
+      mbar_wait(&full[stage], phase);
+      const double* sx = stages + (size_t)stage * 2 * SL + ck.lead;
+      const double* sv = sx + SL;
+      double xs[kTmaU], vs[kTmaU];
+#pragma unroll
+      for (int u = 0; u < kTmaU; ++u) {
+        const int k = tid + u * NC;
+        xs[u] = 0.0; vs[u] = 0.0;
+        if (k < ck.cnt) {
+          if (k + ck.lead < ck.ncopy) { xs[u] = sx[k]; vs[u] = sv[k]; }
+          else { xs[u] = X[c0 + k]; vs[u] = V[c0 + k]; }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);   // stage values are in registers
+      if (++stage == S) { stage = 0; phase ^= 1; }
+
+      // pass 0: locate x_n (branch-free; rare inputs fixed up warp-uniformly)
+      int c0v[kTmaU];
+      double f0v[kTmaU];
+      bool r0[kTmaU], any0 = false;
+#pragma unroll
+      for (int u = 0; u < kTmaU; ++u) {
+        locate_fast(xs[u], h, inv_h, nx, mask, inv_nx, c0v[u], f0v[u], r0[u]);
+        r0[u] = r0[u] && (tid + u * NC < ck.cnt);
+        any0 |= r0[u];
+      }
+      if (__any_sync(0xffffffffu, any0)) {
+#pragma unroll
+        for (int u = 0; u < kTmaU; ++u)
+          if (r0[u]) locate(xs[u], h, inv_h, nx, inv_nx, c0v[u], f0v[u]);
+      }
+      // pass 1: gather, kick, drift, store, locate x_{n+1}
+      double xn[kTmaU], fr[kTmaU];
+      int cl[kTmaU];
+      bool ok[kTmaU], rare[kTmaU], any1 = false;
+#pragma unroll
+      for (int u = 0; u < kTmaU; ++u) {
+        const int k = tid + u * NC;
+        const bool valid = k < ck.cnt;
+        double C[D];
+#pragma unroll
+        for (int kk = 0; kk < D; ++kk) C[kk] = coef[kk * nx + c0v[u]];
+        const double E = horner<D>(C, f0v[u]);
+        const double vn = vs[u] + a.kfull * E;
+        kin = valid ? fma(vn, vn, kin) : kin;
+        const double vh = __dadd_rn(vs[u], __dmul_rn(a.kick, E));
+        xn[u] = __dadd_rn(xs[u], __dmul_rn(a.dt, vh));
+        if (valid) {
+          __stcs(X + c0 + k, xn[u]);
+          __stcs(V + c0 + k, vh);
+        }
+        ok[u] = valid && isfinite(xn[u]);
+        locate_fast(xn[u], h, inv_h, nx, mask, inv_nx, cl[u], fr[u], rare[u]);
+        rare[u] = rare[u] && valid;
+        any1 |= rare[u];
+      }
+      if (__any_sync(0xffffffffu, any1)) {
+#pragma unroll
+        for (int u = 0; u < kTmaU; ++u) {
+          if (!rare[u]) continue;
+          if (ok[u]) locate(xn[u], h, inv_h, nx, inv_nx, cl[u], fr[u]);
+          else { record_bad(a.status, step_id, c0 + tid + u * NC, j, a.p); cl[u] = 0; fr[u] = 0.0; }
+        }
+      }
+      // pass 2: deposit; inactive lanes address the private dummy row nh
+#pragma unroll
+      for (int u = 0; u < kTmaU; ++u) {
+        double w[NW];
+        Spline<D>::weights(fr[u], w);
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const bool act = ok[u] && klane == q;
+          double* hp = hist + (size_t)(act ? cl[u] : nh) * H + myh;
+          double cur[NW];
+#pragma unroll
+          for (int m = 0; m < NW; ++m) cur[m] = hp[act ? m * H : 0];
+#pragma unroll
+          for (int m = 0; m < NW; ++m)
+            if (act) hp[m * H] = cur[m] + w[m];
+          if constexpr (K > 1) __syncwarp();
+        }
+      }
+    }
+    consumers_sync(NC);
+    const int seg = blockIdx.x + j;
+    for (int nd = tid; nd < nx; nd += NC) {
+      double s = 0.0;
+      for (int r = (nd - Spline<D>::OFF) % nx; r < nh; r += nx) {
+        const double* row = hist + (size_t)r * H;
+        for (int hh = 0; hh < H; ++hh) s += row[hh];
+      }
+      a.seg_hist[(size_t)seg * nx + nd] = s;
+    }
+    // consumer-only fixed-order reduction of the kinetic partials
+    kin = warp_sum(kin);
+    if (lane == 0) red[warp] = kin;
+    consumers_sync(NC);
+    if (tid == 0) {
+      double ks = 0.0;
+      for (int w2 = 0; w2 < NCW; ++w2) ks += red[w2];
+      a.seg_kin[seg] = ks;
+    }
+    consumers_sync(NC);
+    pos = (long long)(j + 1) * a.n;
+  }
+}
+
+static size_t tma_smem(int nx, int degree, int ncw, int k, int stages) {
+  const int nc = ncw * 32;
+  const size_t st = (size_t)stages * 2 * (nc * kTmaU + 2) * sizeof(double);
+  const size_t hist = (size_t)(nx + degree + 1) * (nc / k) * sizeof(double);
+  const size_t coef = (size_t)degree * nx * sizeof(double);
+  return st + hist + coef + 32 * sizeof(double) + 2 * stages * sizeof(uint64_t) + 128;
+}
+
+// The TMA-fed variant is opt-in (PICROM_TMA=1): measured slower than the
+// occupancy-hidden step_kernel on B200 for these shapes (profiles/r01).
+static bool tma_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("PICROM_TMA");
+    v = (s && atoi(s)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// pick (consumer warps, lanes per histogram, stages): fewest sharing lanes
+// first, then more consumer warps; ~48 KB of loads in flight per SM
+static bool tma_config(int nx, int degree, TmaCfg* cfg) {
+  if (tma_disabled()) return false;
+  static const int opts[][2] = {{8, 1}, {4, 1}, {8, 2}, {4, 2}, {8, 4}, {4, 4}, {8, 8}, {4, 8}};
+  const char* force = getenv("PICROM_TMA_CFG");      // "ncw,k" (tuning)
+  int fw = 0, fk = 0;
+  if (force && sscanf(force, "%d,%d", &fw, &fk) == 2) {
+    const int stages = fw == 8 ? 3 : 6;
+    const size_t sm = tma_smem(nx, degree, fw, fk, stages);
+    if (sm <= 225 * 1024) { *cfg = TmaCfg{fw, fk, stages, sm}; return true; }
+  }
+  for (auto& o : opts) {
+    const int ncw = o[0], k = o[1];
+    const int stages = ncw == 8 ? 3 : 6;
+    const size_t sm = tma_smem(nx, degree, ncw, k, stages);
+    if (sm <= 225 * 1024) {
+      *cfg = TmaCfg{ncw, k, stages, sm};
+      return true;
+    }
+  }
+  return false;
+}
+
+template <int D, int K, int NCW>
+static int launch_tma_t(const StepArgs& a, const TmaCfg& c, int G, cudaStream_t s) {
+  auto kfn = step_tma_kernel<D, K, NCW>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  kfn<<<G, NCW * 32 + 32, c.smem, s>>>(a, c.stages);
+  return check_launch("step_tma_kernel");
+}
+
+template <int D>
+static int launch_tma_d(const StepArgs& a, const TmaCfg& c, int G, cudaStream_t s) {
+  if (c.ncw == 8 && c.k == 1) return launch_tma_t<D, 1, 8>(a, c, G, s);
+  if (c.ncw == 4 && c.k == 1) return launch_tma_t<D, 1, 4>(a, c, G, s);
+  if (c.ncw == 4 && c.k == 2) return launch_tma_t<D, 2, 4>(a, c, G, s);
+  if (c.ncw == 8 && c.k == 2) return launch_tma_t<D, 2, 8>(a, c, G, s);
+  if (c.ncw == 8 && c.k == 4) return launch_tma_t<D, 4, 8>(a, c, G, s);
+  if (c.ncw == 4 && c.k == 4) return launch_tma_t<D, 4, 4>(a, c, G, s);
+  if (c.ncw == 8 && c.k == 8) return launch_tma_t<D, 8, 8>(a, c, G, s);
+  return launch_tma_t<D, 8, 4>(a, c, G, s);
+}
+
+static int launch_tma(const StepArgs& a, int degree, const TmaCfg& c, int G, cudaStream_t s) {
+  switch (degree) {
+    case 1: return launch_tma_d<1>(a, c, G, s);
+    case 2: return launch_tma_d<2>(a, c, G, s);
+    default: return launch_tma_d<3>(a, c, G, s);
   }
 }
 
@@ -321,7 +787,22 @@ struct SolveArgs {
   size_t hist_stride_rho;   // elements per history row (rho/phi)
   size_t hist_stride_e;     // elements per history row (energies)
   double* phi_hist;         // optional extra copy of phi (history)
+  int seg_dense;            // > 0: dense segments seg[(b*p + j)*nx + nd], b < seg_dense
+  const int* cols;          // optional instance id per column
 };
+
+// sum of cnt values v[0], v[stride], ... with 8 independent loads in flight,
+// combined in a fixed order (deterministic)
+__device__ __forceinline__ double ordered_sum(const double* v, size_t stride, int cnt) {
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int b = 0;
+  for (; b + 8 <= cnt; b += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += v[(size_t)(b + u) * stride];
+  }
+  for (int u = 0; b < cnt; ++b, ++u) acc[u] += v[(size_t)b * stride];
+  return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
 
 __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   extern __shared__ double sm[];
@@ -332,7 +813,7 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   double* red = phi + nx;      // 32
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
-  const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
+  const double* ip = a.inst + (size_t)(a.cols ? a.cols[j] : j) * PICROM_INST_STRIDE;
   const double h = ip[I_H];
   const long long row = a.counter ? *a.counter : 0;
   double* rho_out = a.rho_out ? a.rho_out + row * a.hist_stride_rho : nullptr;
@@ -340,21 +821,22 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   double* energy_out = a.energy_out ? a.energy_out + row * a.hist_stride_e : nullptr;
   double* kin_out = a.kin_out ? a.kin_out + row * a.hist_stride_e : nullptr;
 
-  if (a.seg_hist) {
+  if (a.seg_dense > 0) {
+    const double qw = ip[I_QW], bgh = ip[I_BGH];
+    for (int nd = tid; nd < nx; nd += blockDim.x) {
+      const double s = ordered_sum(a.seg_hist + (size_t)j * nx + nd, (size_t)a.p * nx, a.seg_dense);
+      rho[nd] = a.raw ? s : fma(qw, s, bgh);
+    }
+  } else if (a.seg_hist) {
     const long long T = a.n * (long long)a.p;
     const int b_lo = cta_of((long long)j * a.n, T, a.G);
     const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, a.G);
     const double qw = ip[I_QW], bgh = ip[I_BGH];
     for (int nd = tid; nd < nx; nd += blockDim.x) {
-      double s = 0.0;
-      for (int b = b_lo; b <= b_hi; ++b) s += a.seg_hist[(size_t)(b + j) * nx + nd];
+      const double s = ordered_sum(a.seg_hist + (size_t)(b_lo + j) * nx + nd, nx, b_hi - b_lo + 1);
       rho[nd] = a.raw ? s : fma(qw, s, bgh);
     }
-    if (kin_out && tid == 0) {
-      double s = 0.0;
-      for (int b = b_lo; b <= b_hi; ++b) s += a.seg_kin[b + j];
-      kin_out[j] = 0.5 * s;
-    }
+    if (kin_out && tid == 0) kin_out[j] = 0.5 * ordered_sum(a.seg_kin + b_lo + j, 1, b_hi - b_lo + 1);
   } else if (a.energy_only) {
     for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] = a.rho_in[(size_t)j * nx + nd];
   } else {
@@ -436,17 +918,39 @@ static int launch_solve(const SolveArgs& a, cudaStream_t s) {
   return check_launch("solve_kernel");
 }
 
+// dense-segment assembly + solve (used by the reduced-basis deposit, rom.cu)
+int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, const int* cols,
+                       const double* inst, const double* khat, const double* stencil,
+                       double* phi, double* rho, double* energy, cudaStream_t s) {
+  SolveArgs sa{};
+  sa.seg_hist = seg; sa.seg_dense = G; sa.cols = cols; sa.inst = inst; sa.khat = khat;
+  sa.stencil = stencil; sa.n = 1; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = G;
+  sa.solve = phi != nullptr || energy != nullptr; sa.phi_out = phi; sa.rho_out = rho;
+  sa.energy_out = energy;
+  return launch_solve(sa, s);
+}
+
 // --------------------------------------------------------- launch helpers
 
 template <int D, int K, int MODE>
 static int launch_step_t(const StepArgs& a, const Plan& pl, cudaStream_t s) {
-  auto kfn = step_kernel<D, K, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+  if (step_nt() == 128) {
+    auto kfn = step_kernel<D, K, MODE, 128>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr = true;
+    }
+    kfn<<<pl.G, 128, pl.smem, s>>>(a);
+  } else {
+    auto kfn = step_kernel<D, K, MODE, 256>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr = true;
+    }
+    kfn<<<pl.G, 256, pl.smem, s>>>(a);
   }
-  kfn<<<pl.G, kThreads, pl.smem, s>>>(a);
   return check_launch("step_kernel");
 }
 
@@ -470,6 +974,46 @@ static int launch_step(const StepArgs& a, int degree, const Plan& pl, cudaStream
     case 3: return launch_step_k<3, MODE>(a, pl, s);
   }
   return set_err(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
+}
+
+template <int D, int K>
+static int occ_of(size_t smem) {
+  int occ = 0;
+  if (step_nt() == 128) {
+    auto kfn = step_kernel<D, K, MODE_LEAPFROG, 128>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, smem) != cudaSuccess) occ = 1;
+  } else {
+    auto kfn = step_kernel<D, K, MODE_LEAPFROG, 256>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, smem) != cudaSuccess) occ = 1;
+  }
+  return occ;
+}
+
+template <int D>
+static int occ_k(int K, size_t smem) {
+  switch (K) {
+    case 1: return occ_of<D, 1>(smem);
+    case 2: return occ_of<D, 2>(smem);
+    case 4: return occ_of<D, 4>(smem);
+    case 8: return occ_of<D, 8>(smem);
+    case 16: return occ_of<D, 16>(smem);
+    default: return occ_of<D, 32>(smem);
+  }
+}
+
+static int step_occupancy(int degree, int K, size_t smem) {
+  static int cache[4][6][2] = {};   // degree x log2 K x (smem key valid) -- small memo
+  static size_t cache_smem[4][6] = {};
+  int lk = 0;
+  while ((1 << lk) < K) ++lk;
+  if (cache[degree][lk][0] && cache_smem[degree][lk] == smem) return cache[degree][lk][1];
+  int occ = degree == 1 ? occ_k<1>(K, smem) : degree == 2 ? occ_k<2>(K, smem) : occ_k<3>(K, smem);
+  cache[degree][lk][0] = 1;
+  cache[degree][lk][1] = occ;
+  cache_smem[degree][lk] = smem;
+  return occ;
 }
 
 static int check_cfg(long long n, int p, int nx, int degree) {
@@ -566,6 +1110,11 @@ extern "C" int picrom_pic_push(double* x, double* v, long long n, int p, long lo
   a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
   a.counter = counter;
   ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin);
+  if (pl.tma) {
+    TmaCfg tc;
+    tma_config(nx, degree, &tc);
+    return launch_tma(a, degree, tc, pl.G, (cudaStream_t)stream);
+  }
   return launch_step<MODE_LEAPFROG>(a, degree, pl, (cudaStream_t)stream);
 }
 
@@ -662,7 +1211,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
   const int nx = a.nx;
   const int j = blockIdx.y;
   const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
-  const double h = ip[I_H], g = ip[I_INVH];
+  const double h = ip[I_H], g = ip[I_INVH], inv_h = ip[I_INVH];
   const double* ph = a.phi + (size_t)j * nx;
   const int kind = KICK ? PICROM_GATHER_FIELD : a.kind;
   const int NC = (kind == PICROM_GATHER_VALUE) ? D + 1 : D;
@@ -690,7 +1239,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
     }
     int c;
     double f;
-    locate(x, h, nx, inv_nx, c, f);
+    locate(x, h, inv_h, nx, inv_nx, c, f);
     double r;
     if (kind == PICROM_GATHER_VALUE) {
       if constexpr (D == 1) {
@@ -779,7 +1328,7 @@ __global__ void __launch_bounds__(kThreads) table_kernel(const double* x, long l
     }
     int c;
     double f;
-    locate(xv, ip[I_H], nx, inv_nx, c, f);
+    locate(xv, ip[I_H], ip[I_INVH], nx, inv_nx, c, f);
     const size_t o = (size_t)j * ldo + i;
     if (i0) i0[o] = c;
     if (!w) continue;
@@ -872,23 +1421,28 @@ extern "C" int picrom_half_sumsq(const double* a, long long n, int p, long long 
 template <typename T>
 __global__ void transpose_kernel(const T* in, long long rows, long long cols, T* out) {
   __shared__ T tile[32][33];
-  const long long r0 = (long long)blockIdx.x * 32, c0 = (long long)blockIdx.y * 32;
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    long long r = r0 + k, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
-  }
-  __syncthreads();
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    long long c = c0 + k, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+  const long long r0 = (long long)blockIdx.x * 32;
+  const long long ctiles = (cols + 31) / 32;
+  for (long long cy = blockIdx.y; cy < ctiles; cy += gridDim.y) {
+    const long long c0 = cy * 32;
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+      long long r = r0 + k, c = c0 + threadIdx.x;
+      if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+      long long c = c0 + k, r = r0 + threadIdx.x;
+      if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+    }
   }
 }
 
 template <typename T>
 static int do_transpose(const T* in, long long rows, long long cols, T* out, void* stream) {
   if (rows < 1 || cols < 1) return PICROM_OK;
-  long long gx = (rows + 31) / 32, gy = (cols + 31) / 32;
-  if (gy > 65535 || gx > 2147483647LL) return set_err(PICROM_ERR_CONFIG, "transpose too large");
+  long long gx = (rows + 31) / 32, gy = std::min<long long>((cols + 31) / 32, 65535);
+  if (gx > 2147483647LL) return set_err(PICROM_ERR_CONFIG, "transpose too large");
   dim3 grid((unsigned)gx, (unsigned)gy), block(32, 8);
   transpose_kernel<T><<<grid, block, 0, (cudaStream_t)stream>>>(in, rows, cols, out);
   return check_launch("transpose");

@@ -1,0 +1,730 @@
+// Reduced-basis kernels for sm_100a.
+//
+//   rom_deposit  : X_r = U_X Z (fused, never stored), locate, B-spline deposit
+//                  into per-thread private histograms -> dense segment rows
+//                  [G][p'][Nx]; assembled + solved by the FOM solve kernel.
+//                  (driver.exact_gradients, driver.py:63-73)
+//   rom_gather   : X_r = U_X Z, field gather at X_r, projection U_X^T E
+//                  (per-CTA partials [G][p'][n]), optional DEIM harvest
+//                  lam = Lambda phi (driver.py:76) and optional E output.
+//                  (driver.py:74-76, make_full_stage driver.py:79-89)
+//   paired_gram  : W^T W of a row-concatenation of tall column blocks
+//                  (every n x n product in reduction.py:143-182 is a block of it)
+//   combine      : Y_block = sum_t B_t M_t for tall blocks B_t and small M_t
+//                  (the U + A C updates of reduction.py:143-182)
+//   rows_gather  : U rows at DEIM indices (hyper.py:312)
+//
+// All reductions are fixed-order (deterministic run to run).
+
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+using namespace picrom;
+
+extern int picrom_set_error(int code, const char* msg);
+extern int picrom_check_launch(const char* what);
+extern int picrom_num_sms();
+extern int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, const int* cols,
+                              const double* inst, const double* khat, const double* stencil,
+                              double* phi, double* rho, double* energy, cudaStream_t s);
+
+namespace {
+
+constexpr int NMAX = 32;        // max basis dimension handled in registers
+constexpr int PT = 128;         // instance columns per CTA tile
+
+struct RomArgs {
+  const double* ux;     // U_X rows (N x n, row-major, ld = n)
+  const double* z;      // Z (n x p'), row-major, ld = ldz
+  const double* inst;   // per-instance rows
+  const int* cols;      // instance id of each z column (nullable -> identity)
+  const double* phi;    // (p', nx) potentials (gather)
+  double* seg;          // deposit: [G][p'][nx]; gather: [G][p'][n]
+  double* lam;          // gather: optional (N, ldo) row-major value gather at X_r
+  double* eout;         // gather: optional (N, ldo) row-major coef * d/dx gather at X_r
+  long long N, ldo;
+  int n, p, ldz, nx;
+  int coef_kind;        // gather: 0 -> gcoef (exact_gradients), 1 -> raw derivative
+  unsigned long long* status;
+};
+
+__device__ __forceinline__ long long row_start(int b, long long N, int G) {
+  return ((long long)b * N) / G;
+}
+
+template <int D, int R>
+__global__ void __launch_bounds__(256) rom_deposit_kernel(RomArgs a) {
+  extern __shared__ double smem[];
+  const int P = blockDim.x / R;               // columns per row group (mult of 32)
+  const int H = blockDim.x;
+  const int nh = a.nx + D;
+  double* hist = smem;                        // [nh][H]
+  const int tid = threadIdx.x;
+  const int r = tid / P, jl = tid % P;
+  const int c = blockIdx.y * PT + jl;         // z column
+  const bool active = c < a.p && jl < PT;
+  const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
+  const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
+  const double h = ip[I_H], inv_h = ip[I_INVH];
+  const double inv_nx = 1.0 / (double)a.nx;
+  double zc[NMAX];
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k) zc[k] = (active && k < a.n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+  for (int q = tid; q < nh * H; q += blockDim.x) hist[q] = 0.0;
+  __syncthreads();
+  const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
+  if (active) {
+    for (long long i = lo + r; i < hi; i += R) {
+      const double* u = a.ux + (size_t)i * a.n;
+      double x = 0.0;
+#pragma unroll
+      for (int k = 0; k < NMAX; ++k)
+        if (k < a.n) x = fma(__ldg(u + k), zc[k], x);
+      if (!isfinite(x)) {
+        record_bad(a.status, 0, i, c, a.p);
+        continue;
+      }
+      int cell;
+      double f;
+      locate(x, h, inv_h, a.nx, inv_nx, cell, f);
+      double w[D + 1];
+      Spline<D>::weights(f, w);
+#pragma unroll
+      for (int m = 0; m <= D; ++m) hist[(cell + m) * H + tid] += w[m];
+    }
+  }
+  __syncthreads();
+  // fold ghost rows and row groups (fixed order) -> seg[b][c][nd]
+  const int P_used = min(PT, a.p - blockIdx.y * PT);
+  for (int q = tid; q < P_used * a.nx; q += blockDim.x) {
+    const int cl = q / a.nx, nd = q % a.nx;
+    double s = 0.0;
+    for (int rr = (nd - Spline<D>::OFF) % a.nx; rr < nh; rr += a.nx)
+      for (int g = 0; g < R; ++g) s += hist[rr * H + g * P + cl];
+    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * PT + cl) * a.nx + nd] = s;
+  }
+}
+
+template <int D, int R>
+__global__ void __launch_bounds__(256) rom_gather_kernel(RomArgs a) {
+  extern __shared__ double smem[];
+  const int P = blockDim.x / R;
+  const int tid = threadIdx.x;
+  const int r = tid / P, jl = tid % P;
+  const int c = blockIdx.y * PT + jl;
+  const bool active = c < a.p && jl < PT;
+  const int nx = a.nx;
+  double* phs = smem;                          // [nx][P]
+  double* red = phs + (size_t)nx * P;          // [R][P][n] row-group partials
+  const int P_used = min(PT, a.p - blockIdx.y * PT);
+  for (int q = tid; q < nx * P; q += blockDim.x) {
+    const int nd = q / P, cl = q % P;
+    phs[q] = cl < P_used ? a.phi[(size_t)(blockIdx.y * PT + cl) * nx + nd] : 0.0;
+  }
+  const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
+  const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
+  const double h = ip[I_H], g = ip[I_INVH], inv_h = g;
+  const double cf = a.coef_kind == 0 ? ip[I_GCOEF] : 1.0;
+  const double inv_nx = 1.0 / (double)nx;
+  double zc[NMAX], acc[NMAX];
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k) {
+    zc[k] = (active && k < a.n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+    acc[k] = 0.0;
+  }
+  __syncthreads();
+  const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
+  if (active) {
+    for (long long i = lo + r; i < hi; i += R) {
+      const double* u = a.ux + (size_t)i * a.n;
+      double uk[NMAX];
+      double x = 0.0;
+#pragma unroll
+      for (int k = 0; k < NMAX; ++k) {
+        uk[k] = k < a.n ? __ldg(u + k) : 0.0;
+        if (k < a.n) x = fma(uk[k], zc[k], x);
+      }
+      if (!isfinite(x)) {
+        record_bad(a.status, 0, i, c, a.p);
+        continue;
+      }
+      int cell;
+      double f;
+      locate(x, h, inv_h, nx, inv_nx, cell, f);
+      double pv[D + 1];
+#pragma unroll
+      for (int m = 0; m <= D; ++m) {
+        int nd = cell + Spline<D>::OFF + m;
+        nd = nd < 0 ? nd + nx : (nd >= nx ? nd - nx : nd);
+        pv[m] = phs[nd * P + jl];
+      }
+      double E;
+      if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
+        E = __dmul_rn(cf, __dadd_rn(__dmul_rn(-g, pv[0]), __dmul_rn(g, pv[1])));
+      } else {
+        double dw[D + 1];
+        Spline<D>::dweights(f, g, dw);
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m <= D; ++m) s = fma(dw[m], pv[m], s);
+        E = cf * s;
+      }
+#pragma unroll
+      for (int k = 0; k < NMAX; ++k)
+        if (k < a.n) acc[k] = fma(uk[k], E, acc[k]);
+      if (a.eout) a.eout[(size_t)i * a.ldo + c] = E;
+      if (a.lam) {
+        double lv;
+        if constexpr (D == 1) {
+          lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
+        } else {
+          double w[D + 1];
+          Spline<D>::weights(f, w);
+          lv = 0.0;
+#pragma unroll
+          for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
+        }
+        a.lam[(size_t)i * a.ldo + c] = lv;
+      }
+    }
+  }
+  // row-group partials -> smem -> fixed-order sum -> seg[b][c][k]
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k)
+    if (k < a.n) red[((size_t)r * P + jl) * a.n + k] = acc[k];
+  __syncthreads();
+  for (int q = tid; q < P_used * a.n; q += blockDim.x) {
+    const int cl = q / a.n, k = q % a.n;
+    double s = 0.0;
+    for (int rr = 0; rr < R; ++rr) s += red[((size_t)rr * P + cl) * a.n + k];
+    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * PT + cl) * a.n + k] = s;
+  }
+}
+
+// out[c][k] (and optional transpose layout) = sum_b seg[b][c][k]
+__global__ void seg_sum_kernel(const double* seg, int G, int rows, double* out, int out_ld,
+                               int transpose, int width) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= rows) return;
+  double s = 0.0;
+  for (int b = 0; b < G; ++b) s += seg[(size_t)b * rows + q];
+  if (transpose) {  // q = c*width + k  ->  out[k][c]
+    const int c = q / width, k = q % width;
+    out[(size_t)k * out_ld + c] = s;
+  } else {
+    out[q] = s;
+  }
+}
+
+// ---------------------------------------------------------------- Gram
+
+constexpr int MAXB = 8;   // column blocks
+struct Blocks {
+  const double* ptr[MAXB];
+  int ld[MAXB];
+  int w[MAXB];
+  int off[MAXB + 1];
+  int jswap[MAXB];   // 1: block is J B (row i reads row (i + N/2) mod N, lower half negated)
+  int nb;
+};
+
+// row index / sign of (J B) row i for a 2*half-row block B
+__device__ __forceinline__ long long jrow(long long i, long long half, double& sgn) {
+  if (i < half) { sgn = 1.0; return i + half; }
+  sgn = -1.0;
+  return i - half;
+}
+
+constexpr int GT = 16;     // rows per smem tile
+constexpr int TB = 4;      // output sub-block per thread
+
+// out = A^T B with A = blocks [0, na), B = blocks [na, nb) (na == 0: B^T B over
+// all blocks).  Rows are staged 16 at a time in smem; each thread accumulates
+// TB x TB output sub-blocks in registers; per-CTA partials -> seg.
+__global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N, double* seg) {
+  extern __shared__ double tile[];             // [GT][W]
+  const int W = b.off[b.nb];
+  const int a0 = 0, a1 = na > 0 ? b.off[na] : W;        // A columns [a0, a1)
+  const int b0 = na > 0 ? b.off[na] : 0, b1 = W;        // B columns [b0, b1)
+  const int wa = a1 - a0, wb = b1 - b0;
+  const int nbA = (wa + TB - 1) / TB, nbB = (wb + TB - 1) / TB;
+  const int ntiles = nbA * nbB;
+  const long long lo = row_start(blockIdx.x, N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, N, gridDim.x);
+  constexpr int MAXT = 4;
+  double acc[MAXT][TB][TB];
+#pragma unroll
+  for (int s = 0; s < MAXT; ++s)
+#pragma unroll
+    for (int i = 0; i < TB; ++i)
+#pragma unroll
+      for (int j = 0; j < TB; ++j) acc[s][i][j] = 0.0;
+  for (long long r0 = lo; r0 < hi; r0 += GT) {
+    const int rows = (int)min((long long)GT, hi - r0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < GT * W; q += blockDim.x) {
+      const int rr = q / W, col = q % W;
+      double v = 0.0;
+      if (rr < rows) {
+        int bi = 0;
+        while (col >= b.off[bi + 1]) ++bi;
+        long long row = r0 + rr;
+        double sgn = 1.0;
+        if (b.jswap[bi]) row = jrow(row, N / 2, sgn);
+        v = sgn * __ldg(b.ptr[bi] + (size_t)row * b.ld[bi] + (col - b.off[bi]));
+      }
+      tile[rr * W + col] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < MAXT; ++s) {
+      const int t = threadIdx.x + s * blockDim.x;
+      if (t >= ntiles) break;
+      const int bi = t / nbB, bj = t % nbB;
+      for (int rr = 0; rr < rows; ++rr) {
+        double av[TB], bv[TB];
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          const int ci = bi * TB + i, cj = bj * TB + i;
+          av[i] = ci < wa ? tile[rr * W + a0 + ci] : 0.0;
+          bv[i] = cj < wb ? tile[rr * W + b0 + cj] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < TB; ++i)
+#pragma unroll
+          for (int j = 0; j < TB; ++j) acc[s][i][j] = fma(av[i], bv[j], acc[s][i][j]);
+      }
+    }
+  }
+  double* out = seg + (size_t)blockIdx.x * wa * wb;
+#pragma unroll
+  for (int s = 0; s < MAXT; ++s) {
+    const int t = threadIdx.x + s * blockDim.x;
+    if (t >= ntiles) break;
+    const int bi = t / nbB, bj = t % nbB;
+#pragma unroll
+    for (int i = 0; i < TB; ++i)
+#pragma unroll
+      for (int j = 0; j < TB; ++j) {
+        const int ci = bi * TB + i, cj = bj * TB + j;
+        if (ci < wa && cj < wb) out[(size_t)ci * wb + cj] = acc[s][i][j];
+      }
+  }
+}
+
+// first index of max |v[i*stride]| over i < n, skipping `banned` (numpy
+// argmax tie rule: the smallest index among equal maxima); banned entries
+// score -1 as in hyper.py:241-243.  Two passes: per-CTA (value, index), then
+// one CTA over the partials.
+__device__ __forceinline__ void better(double v, long long i, double& bv, long long& bi) {
+  if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+}
+
+__global__ void argmax_abs_kernel(const double* v, long long n, long long stride,
+                                  const long long* banned, int nbanned, double* pv, long long* pi) {
+  __shared__ double sv[256];
+  __shared__ long long si[256];
+  double bv = -2.0;
+  long long bi = 0x7fffffffffffffffLL;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = fabs(v[i * stride]);
+    for (int k = 0; k < nbanned; ++k)
+      if (banned[k] == i) s = -1.0;
+    better(s, i, bv, bi);
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      double ov = sv[threadIdx.x + o];
+      long long oi = si[threadIdx.x + o];
+      double cv = sv[threadIdx.x];
+      long long ci = si[threadIdx.x];
+      better(ov, oi, cv, ci);
+      sv[threadIdx.x] = cv;
+      si[threadIdx.x] = ci;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pv[blockIdx.x] = sv[0];
+    pi[blockIdx.x] = si[0];
+  }
+}
+
+__global__ void argmax_final_kernel(const double* pv, const long long* pi, int m, long long* out_i,
+                                    double* out_v) {
+  double bv = -2.0;
+  long long bi = 0x7fffffffffffffffLL;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < m; ++k) better(pv[k], pi[k], bv, bi);
+    *out_i = bi;
+    if (out_v) *out_v = bv;
+  }
+}
+
+// ------------------------------------------------------------- combine
+
+constexpr int MAXTERM = 6;
+struct Terms {
+  const double* in[MAXTERM];   // tall input block (N x a_t), row stride ld_t
+  int jswap[MAXTERM];          // 1: use J in_t (rows swapped by halves, lower half negated)
+  int ld[MAXTERM];
+  int a[MAXTERM];
+  int moff[MAXTERM];           // offset of M_t (a_t x c, row-major) in the matrix buffer
+  int nt;
+  double* out;                 // (N x c), row stride ldo
+  int ldo, c;
+  int accumulate;              // out += result
+};
+
+__global__ void __launch_bounds__(256) combine_kernel(Terms t, const double* mats, int mats_len,
+                                                     long long N) {
+  extern __shared__ double ms[];
+  for (int q = threadIdx.x; q < mats_len; q += blockDim.x) ms[q] = mats[q];
+  __syncthreads();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double acc[NMAX];
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k) acc[k] = 0.0;
+  for (int s = 0; s < t.nt; ++s) {
+    long long ri = i;
+    double sgn = 1.0;
+    if (t.jswap[s]) ri = jrow(i, N / 2, sgn);
+    const double* row = t.in[s] + (size_t)ri * t.ld[s];
+    const double* M = ms + t.moff[s];
+    for (int kk = 0; kk < t.a[s]; ++kk) {
+      const double v = sgn * __ldg(row + kk);
+      const double* mr = M + kk * t.c;
+#pragma unroll
+      for (int k = 0; k < NMAX; ++k)
+        if (k < t.c) acc[k] = fma(v, mr[k], acc[k]);
+    }
+  }
+  double* o = t.out + (size_t)i * t.ldo;
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k)
+    if (k < t.c) o[k] = t.accumulate ? o[k] + acc[k] : acc[k];
+}
+
+__global__ void rows_gather_kernel(const double* src, int ld, const long long* idx, int d, int w,
+                                   double* out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= d * w) return;
+  const int r = q / w, k = q % w;
+  out[q] = src[(size_t)idx[r] * ld + k];
+}
+
+// phi (p x nx) = Re(modes (nx x r) . (coords (r x p) * w (r))), complex
+// values interleaved (re, im); im_out (nullable) receives the imaginary part.
+__global__ void dmd_extrap_kernel(const double2* modes, const double2* coords, const double2* w,
+                                  int nx, int r, int p, double* re_out, double* im_out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nx * p) return;
+  const int j = q / nx, nd = q % nx;
+  double sr = 0.0, si = 0.0;
+  for (int m = 0; m < r; ++m) {
+    const double2 c = coords[(size_t)m * p + j], ww = w[m];
+    const double cr = c.x * ww.x - c.y * ww.y, ci = c.x * ww.y + c.y * ww.x;
+    const double2 md = modes[(size_t)nd * r + m];
+    sr += md.x * cr - md.y * ci;
+    si += md.x * ci + md.y * cr;
+  }
+  re_out[(size_t)j * nx + nd] = sr;
+  if (im_out) im_out[(size_t)j * nx + nd] = si;
+}
+
+// DEIM-sampled gather + projection (hyper.py:320-328): one CTA per column j.
+// xd_r = ux_d[r] . z_j ; e_r = dphi_j(xd_r) * w_r * wscale_j ;
+// out[k][j] = inv_mp_j * sum_r ux_d[r][k] e_r   (out row stride ldo)
+template <int D>
+__global__ void deim_gather_kernel(const double* uxd, const double* z, int ldz, const double* phi,
+                                   const double* inst, const int* cols, const double* w,
+                                   const double* wscale, int d, int n, int p, int nx,
+                                   double* out, int ldo, unsigned long long* status) {
+  extern __shared__ double e[];
+  const int j = blockIdx.x;
+  const int inst_id = cols ? cols[j] : j;
+  const double* ip = inst + (size_t)inst_id * PICROM_INST_STRIDE;
+  const double h = ip[I_H], g = ip[I_INVH];
+  const double* ph = phi + (size_t)j * nx;
+  const double inv_nx = 1.0 / (double)nx;
+  for (int rr = threadIdx.x; rr < d; rr += blockDim.x) {
+    double x = 0.0;
+    for (int k = 0; k < n; ++k) x = fma(uxd[(size_t)rr * n + k], z[(size_t)k * ldz + j], x);
+    double dphi = 0.0;
+    if (!isfinite(x)) {
+      record_bad(status, 0, rr, j, p);
+    } else {
+      int c;
+      double f;
+      locate(x, h, g, nx, inv_nx, c, f);
+      double pv[D + 1];
+#pragma unroll
+      for (int m = 0; m <= D; ++m) pv[m] = ph[wrap_node(c + Spline<D>::OFF + m, nx)];
+      if constexpr (D == 1) {
+        dphi = __dadd_rn(__dmul_rn(-g, pv[0]), __dmul_rn(g, pv[1]));
+      } else {
+        double dw[D + 1];
+        Spline<D>::dweights(f, g, dw);
+#pragma unroll
+        for (int m = 0; m <= D; ++m) dphi = fma(dw[m], pv[m], dphi);
+      }
+    }
+    e[rr] = dphi * (w[rr] * (wscale ? wscale[j] : 1.0));
+  }
+  __syncthreads();
+  const double inv_mp = 2.0 * ip[I_HALFINVMP];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    double s = 0.0;
+    for (int rr = 0; rr < d; ++rr) s = fma(uxd[(size_t)rr * n + k], e[rr], s);
+    out[(size_t)k * ldo + j] = inv_mp * s;
+  }
+}
+
+int rom_grid(long long N) {
+  long long g = std::min<long long>((long long)picrom_num_sms(), std::max<long long>(1, N / 64));
+  return (int)g;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx) {
+  const size_t G = (size_t)rom_grid(N);
+  const size_t dep = G * p * nx;
+  const size_t gat = G * p * n;
+  const size_t gram = G * 256 * 256;
+  return std::max(std::max(dep, gat), gram) * sizeof(double) + 256;
+}
+
+template <int D>
+static int launch_rom_deposit(const RomArgs& a, int G, cudaStream_t s) {
+  const int tiles = (a.p + PT - 1) / PT;
+  const int P = std::min(PT, ((std::min(a.p, PT) + 31) / 32) * 32);
+  int R = std::max(1, std::min(256 / P, 2));
+  size_t sm = (size_t)(a.nx + D) * (R * P) * sizeof(double);
+  while (R > 1 && sm > 200 * 1024) { --R; sm = (size_t)(a.nx + D) * (R * P) * sizeof(double); }
+  if (sm > 227 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "rom deposit: nx too large");
+  dim3 grid(G, tiles);
+  if (R == 2) {
+    cudaFuncSetAttribute(rom_deposit_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    rom_deposit_kernel<D, 2><<<grid, 2 * P, sm, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(rom_deposit_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    rom_deposit_kernel<D, 1><<<grid, P, sm, s>>>(a);
+  }
+  return picrom_check_launch("rom_deposit_kernel");
+}
+
+template <int D>
+static int launch_rom_gather(const RomArgs& a, int G, cudaStream_t s) {
+  const int tiles = (a.p + PT - 1) / PT;
+  const int P = std::min(PT, ((std::min(a.p, PT) + 31) / 32) * 32);
+  const int R = std::max(1, std::min(256 / P, 4));
+  const size_t sm = ((size_t)a.nx * P + (size_t)R * P * a.n) * sizeof(double);
+  if (sm > 227 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "rom gather: nx too large");
+  dim3 grid(G, tiles);
+  switch (R) {
+    case 1:
+      cudaFuncSetAttribute(rom_gather_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      rom_gather_kernel<D, 1><<<grid, P, sm, s>>>(a); break;
+    case 2:
+      cudaFuncSetAttribute(rom_gather_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      rom_gather_kernel<D, 2><<<grid, 2 * P, sm, s>>>(a); break;
+    default:
+      cudaFuncSetAttribute(rom_gather_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      rom_gather_kernel<D, 4><<<grid, 4 * P, sm, s>>>(a); break;
+  }
+  return picrom_check_launch("rom_gather_kernel");
+}
+
+static int rom_check(long long N, int n, int p, int nx, int degree) {
+  if (N < 1 || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "need N >= 1 and p >= 1");
+  if (n < 1 || n > NMAX) return picrom_set_error(PICROM_ERR_CONFIG, "basis dimension must be in [1, 32]");
+  if (degree < 1 || degree > 3) return picrom_set_error(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
+  if (nx < 2) return picrom_set_error(PICROM_ERR_CONFIG, "need nx >= 2");
+  return PICROM_OK;
+}
+
+// exact_gradients' field half (driver.py:70-73): rho, phi (p', nx) and the field
+// energy of the reconstructed positions X_r = U_X Z, one solve per column.
+extern "C" int picrom_rom_field(const double* ux, long long N, int n, const double* z, int ldz,
+                                int p, const int* cols, const double* inst, int nx, int degree,
+                                const double* khat, const double* stencil, double* phi,
+                                double* rho, double* energy, void* ws,
+                                unsigned long long* status, void* stream) {
+  int rc = rom_check(N, n, p, nx, degree);
+  if (rc) return rc;
+  RomArgs a{};
+  a.ux = ux; a.z = z; a.inst = inst; a.cols = cols; a.seg = (double*)ws; a.N = N; a.n = n;
+  a.p = p; a.ldz = ldz; a.nx = nx; a.status = status;
+  const int G = rom_grid(N);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (degree) {
+    case 1: rc = launch_rom_deposit<1>(a, G, s); break;
+    case 2: rc = launch_rom_deposit<2>(a, G, s); break;
+    default: rc = launch_rom_deposit<3>(a, G, s); break;
+  }
+  if (rc) return rc;
+  return picrom_solve_dense(a.seg, G, p, nx, degree, cols, inst, khat, stencil, phi, rho, energy, s);
+}
+
+// Gather + projection: g_out (n x p', ld ldg) = U_X^T E with E = coef d/dx
+// (phi . lambda)(U_X Z); lam/eout optional (p', ldo).
+extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const double* z, int ldz,
+                                 int p, const int* cols, const double* inst, int nx, int degree,
+                                 const double* phi, int coef_kind, double* g_out, int ldg,
+                                 double* lam, double* eout, long long ldo, void* ws,
+                                 unsigned long long* status, void* stream) {
+  int rc = rom_check(N, n, p, nx, degree);
+  if (rc) return rc;
+  RomArgs a{};
+  a.ux = ux; a.z = z; a.inst = inst; a.cols = cols; a.phi = phi; a.seg = (double*)ws;
+  a.lam = lam; a.eout = eout; a.N = N; a.ldo = ldo; a.n = n; a.p = p; a.ldz = ldz; a.nx = nx;
+  a.coef_kind = coef_kind; a.status = status;
+  const int G = rom_grid(N);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (degree) {
+    case 1: rc = launch_rom_gather<1>(a, G, s); break;
+    case 2: rc = launch_rom_gather<2>(a, G, s); break;
+    default: rc = launch_rom_gather<3>(a, G, s); break;
+  }
+  if (rc) return rc;
+  if (g_out) {
+    const int rows = p * n;
+    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg, G, rows, g_out, ldg, 1, n);
+    return picrom_check_launch("seg_sum");
+  }
+  return PICROM_OK;
+}
+
+// Gram of the row-concatenation W = [B_0 | B_1 | ...] (N rows): out (w x w).
+static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* lds,
+                     const int* widths, const int* jswap, long long N, double* out, void* ws,
+                     void* stream) {
+  if (nblocks < 1 || nblocks > MAXB) return picrom_set_error(PICROM_ERR_CONFIG, "1..8 blocks");
+  Blocks b{};
+  b.nb = nblocks;
+  b.off[0] = 0;
+  for (int i = 0; i < nblocks; ++i) {
+    b.ptr[i] = ptrs[i]; b.ld[i] = lds[i]; b.w[i] = widths[i];
+    b.jswap[i] = jswap ? jswap[i] : 0;
+    b.off[i + 1] = b.off[i] + widths[i];
+  }
+  const int W = b.off[nblocks];
+  const int wa = na > 0 ? b.off[na] : W, wb = na > 0 ? W - b.off[na] : W;
+  const int nbA = (wa + TB - 1) / TB, nbB = (wb + TB - 1) / TB;
+  if (W > 256 || nbA * nbB > 4 * 256)
+    return picrom_set_error(PICROM_ERR_CONFIG, "Gram: total width <= 256 and wa*wb <= 16384");
+  const int G = rom_grid(N);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = (size_t)GT * W * sizeof(double);
+  gram_kernel<<<G, 256, sm, s>>>(b, na, N, (double*)ws);
+  int rc = picrom_check_launch("gram_kernel");
+  if (rc) return rc;
+  const int rows = wa * wb;
+  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>((const double*)ws, G, rows, out, 0, 0, 1);
+  return picrom_check_launch("seg_sum");
+}
+
+extern "C" int picrom_paired_gram(int nblocks, const double* const* ptrs, const int* lds,
+                                  const int* widths, const int* jswap, long long N, double* out,
+                                  void* ws, void* stream) {
+  return gram_impl(nblocks, 0, ptrs, lds, widths, jswap, N, out, ws, stream);
+}
+
+// out (wa x wb) = A^T B, A = blocks [0, na), B = blocks [na, nblocks)
+extern "C" int picrom_cross_gram(int nblocks, int na, const double* const* ptrs, const int* lds,
+                                 const int* widths, const int* jswap, long long N, double* out,
+                                 void* ws, void* stream) {
+  if (na < 1 || na >= nblocks) return picrom_set_error(PICROM_ERR_CONFIG, "cross Gram needs 1 <= na < nblocks");
+  return gram_impl(nblocks, na, ptrs, lds, widths, jswap, N, out, ws, stream);
+}
+
+extern "C" int picrom_argmax_abs(const double* v, long long n, long long stride,
+                                 const long long* banned, int nbanned, long long* out_index,
+                                 double* out_value, void* ws, void* stream) {
+  if (n < 1) return picrom_set_error(PICROM_ERR_CONFIG, "argmax of an empty vector");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int G = (int)std::min<long long>(2 * picrom_num_sms(), (n + 255) / 256);
+  double* pv = (double*)ws;
+  long long* pi = (long long*)(pv + G);
+  argmax_abs_kernel<<<G, 256, 0, s>>>(v, n, stride, banned, nbanned, pv, pi);
+  int rc = picrom_check_launch("argmax_abs");
+  if (rc) return rc;
+  argmax_final_kernel<<<1, 32, 0, s>>>(pv, pi, G, out_index, out_value);
+  return picrom_check_launch("argmax_final");
+}
+
+// out (N x c) (+)= sum_t in_t (N x a_t) @ M_t (a_t x c); mats is a device buffer
+// holding the M_t back to back (offsets moffs, in doubles).
+extern "C" int picrom_combine(int nterms, const double* const* ins, const int* lds,
+                              const int* widths, const int* jswap, const int* moffs,
+                              const double* mats, int mats_len, long long N, double* out,
+                              int ldo, int c, int accumulate, void* stream) {
+  if (nterms < 1 || nterms > MAXTERM) return picrom_set_error(PICROM_ERR_CONFIG, "1..6 terms");
+  if (c < 1 || c > NMAX) return picrom_set_error(PICROM_ERR_CONFIG, "output width in [1, 32]");
+  Terms t{};
+  t.nt = nterms;
+  for (int i = 0; i < nterms; ++i) {
+    t.in[i] = ins[i]; t.ld[i] = lds[i]; t.a[i] = widths[i]; t.moff[i] = moffs[i];
+    t.jswap[i] = jswap ? jswap[i] : 0;
+  }
+  t.out = out; t.ldo = ldo; t.c = c; t.accumulate = accumulate;
+  const size_t sm = (size_t)mats_len * sizeof(double);
+  if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const unsigned blocks = (unsigned)((N + 255) / 256);
+  combine_kernel<<<blocks, 256, sm, s>>>(t, mats, mats_len, N);
+  return picrom_check_launch("combine_kernel");
+}
+
+extern "C" int picrom_dmd_extrapolate(const double* modes, const double* coords, const double* w,
+                                      int nx, int r, int p, double* re_out, double* im_out,
+                                      void* stream) {
+  if (nx < 1 || r < 1 || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "empty DMD model");
+  const int tot = nx * p;
+  dmd_extrap_kernel<<<(tot + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      (const double2*)modes, (const double2*)coords, (const double2*)w, nx, r, p, re_out, im_out);
+  return picrom_check_launch("dmd_extrapolate");
+}
+
+extern "C" int picrom_deim_gather(const double* uxd, const double* z, int ldz, const double* phi,
+                                  const double* inst, const int* cols, const double* w,
+                                  const double* wscale, int d, int n, int p, int nx, int degree,
+                                  double* out, int ldo, unsigned long long* status, void* stream) {
+  if (d < 1 || n < 1 || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "empty DEIM stage");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = (size_t)d * sizeof(double);
+  switch (degree) {
+    case 1: deim_gather_kernel<1><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status); break;
+    case 2: deim_gather_kernel<2><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status); break;
+    case 3: deim_gather_kernel<3><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status); break;
+    default: return picrom_set_error(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
+  }
+  return picrom_check_launch("deim_gather");
+}
+
+// out (d x w) = src rows idx (src row-major with leading dim ld)
+extern "C" int picrom_rows_gather(const double* src, int ld, const long long* idx, int d, int w,
+                                  double* out, void* stream) {
+  if (d < 1 || w < 1) return PICROM_OK;
+  rows_gather_kernel<<<(d * w + 255) / 256, 256, 0, (cudaStream_t)stream>>>(src, ld, idx, d, w, out);
+  return picrom_check_launch("rows_gather");
+}

@@ -1,0 +1,371 @@
+"""Reduced-order main loop on the GPU -- drop-in for picrom.driver's hot path.
+
+Mirrors /root/reference/pkg/src/picrom/driver.py:63-274: ``exact_gradients``,
+``make_full_stage`` and ``run_reduced`` (Algorithm 2).  The particle-count-
+dependent work runs in the sm_100a library:
+
+* the field half of F(U z) -- reconstruct X_r = U_X z in registers, deposit,
+  one circulant solve per column (picrom_rom_field);
+* the gather half -- reconstruct again, gather the field, project
+  U_X^T E (picrom_rom_gather), harvesting the DEIM samples Lambda phi in the
+  same pass;
+* the basis update -- tall-skinny Grams and combines (reduction.py).
+
+``ParametricVlasovSystem`` carries one mesh per parameter column (BASELINE C3/C4
+draw a wavenumber per instance); with a single length it is the reference's
+VlasovSystem.  Report assembly (run_full/rom/compare, rate fits) stays out of
+scope.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import deque
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _lib, _tall
+from . import hyper as hyp
+from .errors import DivergenceError, EvaluationError, StepFailureError
+from .fem import ChargeConfig, PoissonOperator, build_mesh
+from .fullorder import VlasovSystem
+from .reduction import (
+    complex_svd_basis,
+    orthosymplectic_residuals,
+    prk2_step,
+    select_parameter_subset,
+)
+
+__all__ = ["ParametricVlasovSystem", "DeviceGradient", "exact_gradients", "make_full_stage",
+           "run_reduced", "RomRecord"]
+
+
+class ParametricVlasovSystem:
+    """One periodic mesh per parameter column: lengths L_j, shared Nx, degree, N.
+
+    ``mesh``/``charge``/``poisson`` refer to column 0 (what single-mesh code
+    reads); per-column constants live in the device instance table."""
+
+    def __init__(self, lengths, num_cells, degree, num_particles, charge=-1.0, mass=1.0,
+                 background=1.0):
+        self.lengths = np.asarray(lengths, dtype=float).reshape(-1)
+        self.num_cells, self.degree = int(num_cells), int(degree)
+        self.meshes = [build_mesh(L, num_cells, degree) for L in self.lengths]
+        self.charges = [ChargeConfig(int(num_particles), float(L), charge, mass, background)
+                        for L in self.lengths]
+        self.mesh, self.charge = self.meshes[0], self.charges[0]
+        self.poisson = PoissonOperator(self.mesh)
+        self._inst = torch.from_numpy(
+            dev.inst_rows_host(self.lengths, self.num_cells, self.charges)).to("cuda")
+
+    def inst_table(self, p):
+        return self._inst
+
+    def column_charge(self, j):
+        return self.charges[j]
+
+
+def _inst_table(system, p):
+    if isinstance(system, ParametricVlasovSystem):
+        return system._inst
+    return dev.inst_rows(system.mesh, system.charge, p)
+
+
+def _column_charge(system, j):
+    if isinstance(system, ParametricVlasovSystem):
+        return system.charges[j]
+    return system.charge
+
+
+_WS = {}
+
+
+def _rom_ws(N, p, n, nx):
+    need = int(_lib.query("picrom_rom_workspace_bytes", int(N), int(p), int(n), int(nx)))
+    key = torch.cuda.current_device()
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < need:
+        buf = _WS[key] = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device="cuda")
+    return buf
+
+
+class _Cols:
+    """Device int32 column->instance map (None = identity)."""
+
+    def __init__(self, cols, p_total):
+        self.host = None if cols is None else np.asarray(cols, dtype=np.int32)
+        self.dev = (None if cols is None
+                    else torch.from_numpy(self.host.copy()).to("cuda"))
+
+    @property
+    def ptr(self):
+        return None if self.dev is None else self.dev.data_ptr()
+
+
+def _field_device(system, ud, z, cols, want_energy=False, status=None):
+    """phi (p', nx) [, energy (p')] of X_r = U_X z on the device."""
+    N2, n = ud.shape
+    N = N2 // 2
+    p = z.shape[1]
+    mesh = system.mesh
+    nx, d = mesh.num_cells, mesh.degree
+    c = system.poisson.constants
+    zd = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to("cuda")
+    inst = _inst_table(system, p if cols.dev is None else int(cols.host.max()) + 1)
+    phi = torch.empty((p, nx), dtype=torch.float64, device="cuda")
+    energy = torch.empty(p, dtype=torch.float64, device="cuda") if want_energy else None
+    st = status if status is not None else dev.new_status()
+    _lib.call("picrom_rom_field", ud.data_ptr(), N, n, zd.data_ptr(), p, p, cols.ptr,
+              inst.data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(), phi.data_ptr(),
+              None, dev.ptr(energy), _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(),
+              dev.stream_handle())
+    return zd, inst, phi, energy, st
+
+
+def _raise_eval(st, p):
+    bad = dev.decode_status(st, p)
+    if bad is not None:
+        _, row, col = bad
+        raise EvaluationError(f"non-finite particle position at index {(row, col)}",
+                              index=(row, col))
+
+
+class DeviceGradient:
+    """F(U z) = [coef d/dx(phi.Lambda)(U_X z); U_V z] (2N x p') kept implicit:
+    E (N x p') on the device plus (U, z).  ``times_matrix(M)`` = G @ M as two
+    combines; ``dense()`` materialises G (API / tests)."""
+
+    def __init__(self, u, z, e):
+        self.u, self.z, self.e = u, np.asarray(z, dtype=float), e
+
+    @property
+    def shape(self):
+        return (self.u.shape[0], self.z.shape[1])
+
+    def times_matrix(self, m):
+        m = np.asarray(m, dtype=float)
+        N = self.u.shape[0] // 2
+        out = torch.empty((2 * N, m.shape[1]), dtype=torch.float64, device="cuda")
+        _tall.combine([(self.e, m, False)], out=out[:N])
+        _tall.combine([(self.u[N:], self.z @ m, False)], out=out[N:])
+        return out
+
+    def __matmul__(self, m):
+        return self.times_matrix(m)
+
+    def dense(self):
+        N = self.u.shape[0] // 2
+        zd = torch.from_numpy(self.z).to("cuda")
+        return torch.cat([self.e, self.u[N:] @ zd], dim=0)
+
+
+def exact_gradients_device(system, ud, z, cols=None, harvest=True):
+    """(DeviceGradient, phi (p', nx) device, lam (N x p') device|None) -- driver.py:63-76."""
+    N2, n = ud.shape
+    N = N2 // 2
+    p = z.shape[1]
+    colmap = cols if isinstance(cols, _Cols) else _Cols(cols, p)
+    zd, inst, phi, _, st = _field_device(system, ud, z, colmap)
+    e = torch.empty((N, p), dtype=torch.float64, device="cuda")
+    lam = torch.empty((N, p), dtype=torch.float64, device="cuda") if harvest else None
+    mesh = system.mesh
+    _lib.call("picrom_rom_gather", ud.data_ptr(), N, n, zd.data_ptr(), p, p, colmap.ptr,
+              inst.data_ptr(), mesh.num_cells, mesh.degree, phi.data_ptr(), 0, None, 0,
+              dev.ptr(lam), e.data_ptr(), p, _rom_ws(N, p, n, mesh.num_cells).data_ptr(),
+              st.data_ptr(), dev.stream_handle())
+    _raise_eval(st, p)
+    return DeviceGradient(ud, z, e), phi, lam
+
+
+def exact_gradients(system, u, z):
+    """Full-state gradients at the reconstructed columns U z (driver.py:63-76):
+    (g (2N, p'), phi (Nx, p'), lam (N, p')) as arrays of the input's kind."""
+    was_np = not isinstance(u, torch.Tensor)
+    ud = (torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).to("cuda") if was_np
+          else u.to(device="cuda", dtype=torch.float64).contiguous())
+    z = z.cpu().numpy() if isinstance(z, torch.Tensor) else np.asarray(z, dtype=float)
+    g, phi, lam = exact_gradients_device(system, ud, z)
+    gd = g.dense()
+    phi_t = phi.t().contiguous()
+    if was_np:
+        return gd.cpu().numpy(), phi_t.cpu().numpy(), lam.cpu().numpy()
+    return gd, phi_t, lam
+
+
+def make_full_stage(system):
+    """Warm-up coefficient gradient U_mid^T F(U_mid z) on all columns (driver.py:79-89):
+    g(z) = U_X^T E(U_X z) + (U_V^T U_V) z, E by the fused rom_field/rom_gather
+    passes, the Gram once per stage."""
+
+    def factory(u_mid):
+        N = u_mid.shape[0] // 2
+        n = u_mid.shape[1]
+        uvtuv = _tall.gram([(u_mid[N:], False)])
+
+        def g(z):
+            z = np.asarray(z, dtype=float)
+            p = z.shape[1]
+            cols = _Cols(None, p)
+            zd, inst, phi, _, st = _field_device(system, u_mid, z, cols)
+            gout = torch.empty((n, p), dtype=torch.float64, device="cuda")
+            mesh = system.mesh
+            _lib.call("picrom_rom_gather", u_mid.data_ptr(), N, n, zd.data_ptr(), p, p, None,
+                      inst.data_ptr(), mesh.num_cells, mesh.degree, phi.data_ptr(), 0,
+                      gout.data_ptr(), p, None, None, 0,
+                      _rom_ws(N, p, n, mesh.num_cells).data_ptr(), st.data_ptr(),
+                      dev.stream_handle())
+            _raise_eval(st, p)
+            return gout.cpu().numpy() + uvtuv @ z
+
+        return g
+
+    return factory
+
+
+@dataclass
+class RomRecord:
+    """Time series of a reduced run (driver.py:92-114, diagnostics subset)."""
+
+    times: np.ndarray
+    energy_times: np.ndarray
+    electric_energy: np.ndarray
+    hamiltonian: np.ndarray
+    snapshot_times: np.ndarray
+    bases: list
+    ortho_residuals: np.ndarray
+    sympl_residuals: np.ndarray
+    fp_iterations: np.ndarray
+    dmd_ranks: np.ndarray
+    s_conds: np.ndarray
+    hyper_engaged: bool
+    deim_indices: list = field(default_factory=list)
+    step_seconds: np.ndarray = None
+    notes: dict = field(default_factory=dict)
+
+
+def _diag_energies(system, ud, z):
+    """Electric + kinetic energy of the reconstructed state (driver.py:160-170):
+    kinetic 0.5 z_j^T (U_V^T U_V) z_j needs no reconstruction."""
+    p = z.shape[1]
+    N = ud.shape[0] // 2
+    _, _, _, ee, st = _field_device(system, ud, z, _Cols(None, p), want_energy=True)
+    _raise_eval(st, p)
+    gv = _tall.gram([(ud[N:], False)])
+    kin = 0.5 * np.einsum("ij,ij->j", z, gv @ z)
+    return ee.cpu().numpy(), kin
+
+
+def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_dim, deim_period,
+                deim_update, dt, t_final, svd_tol_dmd=1e-5, fp_tol=1e-9, fp_max_iter=100,
+                hyper_reduction=True, printed_subset_variant=False, printed_deim_ranking=False,
+                energy_stride=10, snapshot_stride=None, decomp_stride=50, record_snapshots=True,
+                timers=None, u0=None, z0=None):
+    """Reduced-order run over all parameter columns (driver.py:117-274).
+
+    U lives on the device for the whole run; Z and every small matrix on the
+    host.  ``u0``/``z0`` may supply the initial basis (otherwise the complex
+    SVD of the snapshots, as in the reference)."""
+    from .diagnostics import PhaseTimers
+    params = np.asarray(params, dtype=float)
+    num_steps = int(round(t_final / dt))
+    snap_stride = (max(1, int(snapshot_stride)) if snapshot_stride is not None
+                   else max(1, num_steps // 40))
+    timers = timers or PhaseTimers()
+    if u0 is None:
+        u, z = complex_svd_basis(x0, v0, basis_dim, device=True)
+    else:
+        u = u0 if isinstance(u0, torch.Tensor) else torch.from_numpy(np.asarray(u0)).to("cuda")
+        z = np.asarray(z0, dtype=float)
+    sub = np.sort(select_parameter_subset(z, subsample, printed_variant=printed_subset_variant))
+    subcols = _Cols(sub, z.shape[1])
+    pot_window = deque(maxlen=window + 1)
+    deim_window = hyp.DeimWindow(window + 1) if hyper_reduction else None
+    dmd_model = deim_model = None
+    main_counter = 0
+    hyper_engaged = False
+    full_stage = make_full_stage(system)
+
+    def grad_sub(u_eval, z_sub):
+        return exact_gradients_device(system, u_eval, z_sub, subcols, harvest=False)[0]
+
+    energy_times, energies, hams = [], [], []
+    snap_times, bases = [], []
+    ortho_res = np.zeros(num_steps + 1)
+    sympl_res = np.zeros(num_steps + 1)
+    fp_iters = np.zeros(num_steps, dtype=int)
+    dmd_ranks = np.zeros(num_steps, dtype=int)
+    s_conds = np.zeros(num_steps)
+    deim_hist = []
+    step_seconds = np.zeros(num_steps)
+
+    def diagnostics(tau, u_now, z_now):
+        t_now = tau * dt
+        if tau % energy_stride == 0 or tau == num_steps:
+            ee, kin = _diag_energies(system, u_now, z_now)
+            energy_times.append(t_now)
+            energies.append(ee)
+            hams.append(kin + ee)
+        if record_snapshots and (tau % snap_stride == 0 or tau == num_steps):
+            snap_times.append(t_now)
+            bases.append((u_now.clone(), z_now.copy()))
+
+    ortho_res[0], sympl_res[0] = orthosymplectic_residuals(u)
+    diagnostics(0, u, z)
+    import time as _time
+    for tau in range(1, num_steps + 1):
+        t_prev = (tau - 1) * dt
+        tic = _time.perf_counter()
+        try:
+            with timers.phase("rom_basis"):
+                g_sub0, phi_sub, lam_sub = exact_gradients_device(
+                    system, u, z[:, sub], subcols, harvest=hyper_reduction)
+            pot_window.append(phi_sub.t().cpu().numpy())
+            if hyper_reduction:
+                deim_window.append(lam_sub)
+            hyper_now = hyper_reduction and len(pot_window) == window + 1
+            if hyper_now:
+                hyper_engaged = True
+                with timers.phase("dmd_fit"):
+                    dmd_model = hyp.fit_parametric_dmd(list(pot_window), dt, t_prev, params, sub,
+                                                       svd_tol=svd_tol_dmd)
+                with timers.phase("deim_fit"):
+                    deim_model = hyp.fit_deim_device(
+                        deim_window, deim_dim, system.charge, prev=deim_model,
+                        full=(main_counter % deim_period == 0), n_update=deim_update,
+                        printed_ranking=printed_deim_ranking)
+                main_counter += 1
+                stage = hyp.make_hyper_stage_device(dmd_model, deim_model, t_prev + 0.5 * dt,
+                                                    system, params)
+                deim_hist.append(deim_model.indices.copy())
+            else:
+                stage = full_stage
+            res = prk2_step(u, z, dt, sub, grad_sub, g_sub0, stage, fp_tol=fp_tol,
+                            fp_max_iter=fp_max_iter, timers=timers)
+        except EvaluationError as err:
+            raise DivergenceError(f"reduced state diverged during step {tau} (t = {tau * dt:.6g})",
+                                  time=tau * dt) from err
+        except StepFailureError as err:
+            raise StepFailureError(f"step {tau} (t = {tau * dt:.6g}): {err}",
+                                   iterations=err.iterations,
+                                   residual_trace=err.residual_trace) from err
+        u, z = res.u, res.z
+        timers.flush_step()
+        step_seconds[tau - 1] = _time.perf_counter() - tic
+        ortho_res[tau], sympl_res[tau] = orthosymplectic_residuals(u)
+        fp_iters[tau - 1] = res.fp_iterations
+        s_conds[tau - 1] = res.s_cond
+        if hyper_now:
+            dmd_ranks[tau - 1] = dmd_model.rank
+        diagnostics(tau, u, z)
+
+    notes = {} if hyper_engaged else {"no_hyper_reduction_engaged": True}
+    return RomRecord(
+        times=dt * np.arange(num_steps + 1), energy_times=np.asarray(energy_times),
+        electric_energy=np.asarray(energies), hamiltonian=np.asarray(hams),
+        snapshot_times=np.asarray(snap_times), bases=bases, ortho_residuals=ortho_res,
+        sympl_residuals=sympl_res, fp_iterations=fp_iters, dmd_ranks=dmd_ranks, s_conds=s_conds,
+        hyper_engaged=hyper_engaged, deim_indices=deim_hist, step_seconds=step_seconds,
+        notes=notes)

@@ -1,0 +1,473 @@
+"""DMD-DEIM hyper-reduction -- drop-in for picrom.hyper, GPU where it scales.
+
+Same public names and argument meaning as /root/reference/pkg/src/picrom/
+hyper.py (DMDModel, fit_dmd, RBFInterpolant, fit_parametric_dmd, DEIMModel,
+deim_greedy, fit_deim, make_hyper_stage, hyper_hamiltonian).
+
+Split by size:
+* parameter/grid-sized algebra (the DMD fit on the Nx x p*T potential window,
+  the RBF system over p* parameter nodes, DEIM weight solve d x d) is tiny and
+  stays in host LAPACK, as in the reference;
+* everything that scales with the particle count N runs on the device:
+  the DEIM window Gram (sliding, picrom_cross_gram), the basis
+  Psi = W V Sigma^-1 (picrom_combine), the greedy residuals + argmax
+  (picrom_combine, picrom_argmax_abs), U_X[I] (picrom_rows_gather), and per
+  stage the DMD extrapolation (picrom_dmd_extrapolate) and the DEIM-sampled
+  gather + projection (picrom_deim_gather).
+
+The DEIM SVD is computed from the window Gram (eigen-decomposition on the
+host) followed by one Rayleigh-Ritz refinement on the device; its accuracy
+(and therefore index parity with the reference's direct SVD) is discussed in
+DESIGN.md -- greedy index selection itself is bit-exact given the same basis.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+from collections import deque
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+from scipy.linalg import eig, lstsq, svd
+
+from . import _device as dev
+from . import _lib, _tall
+from .errors import ConfigurationError, DegenerateDataError
+
+__all__ = ["DMDModel", "fit_dmd", "RBFInterpolant", "fit_parametric_dmd", "DEIMModel",
+           "deim_greedy", "fit_deim", "hyper_hamiltonian", "make_hyper_stage", "DeimWindow",
+           "fit_deim_device", "make_hyper_stage_device"]
+
+MODE_DISCARD = 1e-12          # |lambda| below this is dropped (hyper.py:40)
+IMAG_WARN = 1e-3              # relative imaginary defect warning level (hyper.py:41)
+
+
+# ----------------------------------------------------------------- DMD (host)
+
+@dataclass
+class DMDModel:
+    """phi(t) = Re(Theta (Pi * exp(omega (t - t0)))) (hyper.py:44-96)."""
+
+    modes: np.ndarray
+    omegas: np.ndarray
+    eigenvalues: np.ndarray
+    anchor_time: float
+    coords: np.ndarray = None
+    pi_sub: np.ndarray = None
+    sub: np.ndarray = None
+    interpolant: object = None
+    imag_defect: float = field(default=0.0)
+
+    @property
+    def rank(self):
+        return self.modes.shape[1]
+
+    def ensure_coords(self, params):
+        """Coordinates for every parameter column; subsample columns keep the
+        directly projected ones."""
+        if self.coords is None:
+            if self.interpolant is None:
+                raise ConfigurationError("DMD model has no coordinate interpolant attached")
+            c = self.interpolant(np.asarray(params, dtype=float)).T
+            c[:, self.sub] = self.pi_sub
+            self.coords = c
+        return self.coords
+
+    def _note_defect(self, re_norm, im_norm):
+        if re_norm > 0.0:
+            self.imag_defect = max(self.imag_defect, float(im_norm / re_norm))
+            if self.imag_defect > IMAG_WARN and not getattr(self, "_warned", False):
+                self._warned = True
+                warnings.warn(f"DMD reconstruction has relative imaginary part {self.imag_defect:.2e}")
+
+    def potential(self, t, coords=None):
+        """Host evaluation (Nx x p'), the reference's formula."""
+        coords = self.coords if coords is None else coords
+        if coords is None:
+            raise ConfigurationError("DMD model has no modal coordinates attached")
+        grow = np.exp(self.omegas * (t - self.anchor_time))
+        full = self.modes @ (coords * grow[:, None])
+        self._note_defect(np.linalg.norm(full.real), np.linalg.norm(full.imag))
+        return full.real
+
+    def potential_device(self, t, coords=None):
+        """Device evaluation: (p', Nx) real potential (picrom_dmd_extrapolate)."""
+        coords = self.coords if coords is None else coords
+        if coords is None:
+            raise ConfigurationError("DMD model has no modal coordinates attached")
+        nx, r = self.modes.shape
+        p = coords.shape[1]
+        grow = np.exp(self.omegas * (t - self.anchor_time))
+        m = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(self.modes, dtype=np.complex128))).to("cuda")
+        c = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(coords, dtype=np.complex128))).to("cuda")
+        w = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(grow, dtype=np.complex128))).to("cuda")
+        re = torch.empty((p, nx), dtype=torch.float64, device="cuda")
+        im = torch.empty((p, nx), dtype=torch.float64, device="cuda")
+        _lib.call("picrom_dmd_extrapolate", m.data_ptr(), c.data_ptr(), w.data_ptr(), nx, r, p,
+                  re.data_ptr(), im.data_ptr(), dev.stream_handle())
+        self._note_defect(float(torch.linalg.vector_norm(re)), float(torch.linalg.vector_norm(im)))
+        return re
+
+    def project_coords(self, snapshots):
+        """Least-squares modal coordinates of potential columns (hyper.py:93-96)."""
+        return lstsq(self.modes, np.asarray(snapshots, dtype=complex))[0]
+
+
+def fit_dmd(y, y_shift, dt, svd_tol=1e-5, anchor_time=0.0):
+    """Exact projected DMD of (Y, Y') with SVD truncation (hyper.py:99-124)."""
+    y = np.asarray(y, dtype=float)
+    y_shift = np.asarray(y_shift, dtype=float)
+    if y.shape != y_shift.shape:
+        raise ConfigurationError("snapshot blocks must have equal shapes")
+    if not np.any(y) or not np.any(y_shift):
+        raise DegenerateDataError("DMD window is identically zero")
+    left, sing, right_h = svd(y, full_matrices=False)
+    kept = sing >= svd_tol * sing[0]
+    left, sing, right_h = left[:, kept], sing[kept], right_h[kept]
+    projected = y_shift @ (right_h.T / sing)
+    eigvals, eigvecs = eig(left.T @ projected)
+    modes = projected @ eigvecs
+    alive = np.abs(eigvals) >= MODE_DISCARD
+    if not alive.any():
+        raise DegenerateDataError("all DMD eigenvalues collapsed below the discard threshold")
+    eigvals, modes = eigvals[alive], modes[:, alive]
+    return DMDModel(modes=modes, omegas=np.log(eigvals) / dt, eigenvalues=eigvals,
+                    anchor_time=anchor_time)
+
+
+class RBFInterpolant:
+    """Gaussian RBF over parameter nodes, affine tail, fallbacks (hyper.py:127-177)."""
+
+    def __init__(self, nodes, values):
+        self.nodes = np.atleast_2d(np.asarray(nodes, dtype=float))
+        values = np.asarray(values)
+        count, dim = self.nodes.shape
+        dist = np.sqrt(((self.nodes[:, None, :] - self.nodes[None, :, :]) ** 2).sum(-1))
+        pairs = dist[np.triu_indices(count, k=1)]
+        med = np.median(pairs) if pairs.size else 1.0
+        self.eps = 1.0 / med if med > 0 else 1.0
+        gram = np.exp(-((self.eps * dist) ** 2))
+        self.values = values
+        self.coeffs = None
+        self.poly = None
+        self.degenerate = False
+        if count > dim + 1:
+            tail = np.hstack([np.ones((count, 1)), self.nodes])
+            m = tail.shape[1]
+            lhs = np.block([[gram, tail], [tail.T, np.zeros((m, m))]])
+            rhs = np.concatenate([values, np.zeros((m,) + values.shape[1:])])
+            try:
+                sol = np.linalg.solve(lhs, rhs)
+                self.coeffs, self.poly = sol[:count], sol[count:]
+            except np.linalg.LinAlgError:
+                pass
+        if self.coeffs is None:
+            try:
+                self.coeffs = np.linalg.solve(gram, values)
+            except np.linalg.LinAlgError:
+                warnings.warn("singular RBF kernel system; falling back to nearest-neighbor lookup")
+                self.degenerate = True
+
+    def __call__(self, targets):
+        targets = np.atleast_2d(np.asarray(targets, dtype=float))
+        d2 = ((targets[:, None, :] - self.nodes[None, :, :]) ** 2).sum(-1)
+        if self.degenerate:
+            return self.values[np.argmin(d2, axis=1)]
+        out = np.exp(-(self.eps ** 2) * d2) @ self.coeffs
+        if self.poly is not None:
+            out = out + np.hstack([np.ones((len(targets), 1)), targets]) @ self.poly
+        return out
+
+
+def fit_parametric_dmd(window, dt, anchor_time, params, sub, svd_tol=1e-5):
+    """Sliding-window DMD + RBF coordinates over the parameter plane (hyper.py:180-202)."""
+    stack = np.stack([np.asarray(w, dtype=float) for w in window])
+    t1, nx, _ = stack.shape
+    if t1 < 2:
+        raise ConfigurationError("DMD window needs at least two samples")
+    flat = stack.transpose(1, 2, 0)
+    model = fit_dmd(flat[:, :, :-1].reshape(nx, -1), flat[:, :, 1:].reshape(nx, -1), dt,
+                    svd_tol=svd_tol, anchor_time=anchor_time)
+    model.pi_sub = model.project_coords(stack[-1])
+    model.sub = np.asarray(sub, dtype=int)
+    model.interpolant = RBFInterpolant(np.asarray(params, dtype=float)[model.sub], model.pi_sub.T)
+    return model
+
+
+# --------------------------------------------------------------- DEIM (device)
+
+@dataclass
+class DEIMModel:
+    """Interpolation basis psi (N x d), indices I (d,), collapsed weights (d,)."""
+
+    psi: object
+    indices: np.ndarray
+    weights: np.ndarray
+
+    @property
+    def dim(self):
+        return self.psi.shape[1]
+
+
+class DeimWindow:
+    """Ring of the last T+1 harvested sample blocks (each N x p*, device) with
+    the window Gram maintained incrementally (one new block x window per step)."""
+
+    def __init__(self, capacity):
+        self.capacity = int(capacity)
+        self.blocks = deque()
+        self._gram = {}          # (id_a, id_b) -> block Gram (host)
+        self._next = 0
+        self.ids = deque()
+
+    def __len__(self):
+        return len(self.blocks)
+
+    def append(self, block):
+        block = block.contiguous()
+        if len(self.blocks) == self.capacity:
+            old = self.ids.popleft()
+            self.blocks.popleft()
+            self._gram = {k: v for k, v in self._gram.items() if old not in k}
+        bid = self._next
+        self._next += 1
+        self.blocks.append(block)
+        self.ids.append(bid)
+        others = list(zip(self.ids, self.blocks))
+        # new block against every block in the window, <= 7 partners per call
+        for s in range(0, len(others), 7):
+            part = others[s:s + 7]
+            g = _cross(block, [b for _, b in part])
+            off = 0
+            for oid, ob in part:
+                w = ob.shape[1]
+                self._gram[(bid, oid)] = g[:, off:off + w]
+                self._gram[(oid, bid)] = g[:, off:off + w].T
+                off += w
+
+    def gram(self):
+        ids = list(self.ids)
+        return np.block([[self._gram[(a, b)] for b in ids] for a in ids])
+
+    def columns(self):
+        return list(self.blocks)
+
+
+def _cross(a, bs):
+    """a^T [b_0 | b_1 | ...] on the device (host result)."""
+    blocks = [a] + list(bs)
+    wa = a.shape[1]
+    wb = sum(b.shape[1] for b in bs)
+    out = torch.empty((wa, wb), dtype=torch.float64, device="cuda")
+    rows = a.shape[0]
+    arr = lambda t, v: (t * len(v))(*v)  # noqa: E731
+    _lib.call("picrom_cross_gram", len(blocks), 1, arr(C.c_void_p, [b.data_ptr() for b in blocks]),
+              arr(C.c_int, [int(b.stride(0)) for b in blocks]),
+              arr(C.c_int, [int(b.shape[1]) for b in blocks]), None, rows, out.data_ptr(),
+              _tall._ws(rows, 256).data_ptr(), dev.stream_handle())
+    return out.cpu().numpy()
+
+
+def _blocks_times(blocks, m):
+    """[B_0 | B_1 | ...] @ m on the device (tall x small), m host (c x k)."""
+    rows = blocks[0].shape[0]
+    k = m.shape[1]
+    out = torch.zeros((rows, k), dtype=torch.float64, device="cuda")
+    off = 0
+    terms = []
+    for b in blocks:
+        w = b.shape[1]
+        terms.append((b, m[off:off + w]))
+        off += w
+    for c0 in range(0, k, 32):
+        c1 = min(k, c0 + 32)
+        for s in range(0, len(terms), 6):
+            chunk = [(b, mm[:, c0:c1], False) for b, mm in terms[s:s + 6]]
+            _tall.combine(chunk, out=out[:, c0:c1], accumulate=(s > 0))
+    return out
+
+
+_ARGMAX_WS = {}
+
+
+def _argmax_abs(v, banned):
+    n = v.shape[0]
+    key = torch.cuda.current_device()
+    ws = _ARGMAX_WS.get(key)
+    if ws is None:
+        ws = _ARGMAX_WS[key] = torch.empty(1 << 16, dtype=torch.float64, device="cuda")
+    out_i = torch.empty(1, dtype=torch.int64, device="cuda")
+    b = (torch.as_tensor(np.asarray(banned, dtype=np.int64)).to("cuda") if len(banned)
+         else None)
+    _lib.call("picrom_argmax_abs", v.data_ptr(), n, int(v.stride(0)), dev.ptr(b), len(banned),
+              out_i.data_ptr(), None, ws.data_ptr(), dev.stream_handle())
+    return int(out_i.item())
+
+
+def _rows(psi, idx):
+    """psi[idx, :] as host numpy (picrom_rows_gather)."""
+    idx_d = torch.as_tensor(np.asarray(idx, dtype=np.int64)).to("cuda")
+    out = torch.empty((len(idx), psi.shape[1]), dtype=torch.float64, device="cuda")
+    _lib.call("picrom_rows_gather", psi.data_ptr(), int(psi.stride(0)), idx_d.data_ptr(), len(idx),
+              psi.shape[1], out.data_ptr(), dev.stream_handle())
+    return out.cpu().numpy()
+
+
+def deim_greedy(psi, keep=None):
+    """Greedy interpolation indices (hyper.py:218-246) on a device basis psi (N x d):
+    residual psi_k - Psi_<k (Psi[I,<k])^-1 psi_k[I] by one combine, argmax by
+    picrom_argmax_abs with the assigned indices banned (first-max tie rule)."""
+    if not isinstance(psi, torch.Tensor):
+        psi = torch.from_numpy(np.ascontiguousarray(psi, dtype=np.float64)).to("cuda")
+    n, d = psi.shape
+    keep = keep or {}
+    indices = np.empty(d, dtype=np.int64)
+    banned = [int(v) for v in keep.values()]
+    for k in range(d):
+        if k in keep:
+            indices[k] = keep[k]
+            continue
+        if k == 0:
+            res = psi[:, 0]
+        else:
+            rows = indices[:k]
+            sub = _rows(psi, rows)
+            coeff = np.linalg.solve(sub[:, :k], sub[:, k])
+            m = np.concatenate([-coeff, [1.0]])[:, None]
+            res = _tall.combine([(psi[:, :k + 1].contiguous(), m, False)])[:, 0]
+        pick = _argmax_abs(res, banned)
+        indices[k] = pick
+        banned.append(pick)
+    return indices
+
+
+def _window_svd(window, dim):
+    """Leading left singular vectors of the window W (N x c): Gram eigenpairs
+    give V, Sigma; Psi0 = W V Sigma^-1; one Rayleigh-Ritz pass re-orthonormalises
+    Psi0 and rotates it to the singular directions of Psi0^T W."""
+    blocks = window.columns()
+    c = sum(b.shape[1] for b in blocks)
+    gram = window.gram()
+    lam, vec = np.linalg.eigh(gram)
+    order = np.argsort(lam)[::-1]
+    lam, vec = lam[order], vec[:, order]
+    sing = np.sqrt(np.clip(lam, 0.0, None))
+    nrows = blocks[0].shape[0]
+    rank = int((sing >= max(nrows, c) * np.finfo(float).eps * sing[0]).sum())
+    d_eff = min(int(dim), rank)
+    if d_eff < dim:
+        warnings.warn(f"DEIM samples have numerical rank {rank} < {dim}; basis reduced to {d_eff}")
+    psi0 = _blocks_times(blocks, vec[:, :d_eff] / sing[:d_eff])
+    # Rayleigh-Ritz: orthonormalise, then rotate to the SVD of Q^T W
+    g0 = _tall.gram([(psi0, False)])
+    r = np.linalg.cholesky(g0).T
+    q = _tall.combine([(psi0, np.linalg.inv(r), False)]) if d_eff <= 32 else \
+        _blocks_times([psi0], np.linalg.inv(r))
+    qtw = np.concatenate([_cross(q, [b]) for b in blocks], axis=1)
+    ub, _, _ = svd(qtw, full_matrices=False)
+    psi = _blocks_times([q], ub)
+    return psi, d_eff
+
+
+def fit_deim_device(window, dim, charge, prev=None, full=True, n_update=None,
+                    printed_ranking=False):
+    """fit_deim (hyper.py:249-277) on a device DeimWindow."""
+    if len(window) == 0:
+        raise DegenerateDataError("DEIM sample window is empty")
+    psi, d_eff = _window_svd(window, dim)
+    keep = None
+    if (not full and prev is not None and prev.dim == d_eff and n_update is not None
+            and n_update < d_eff):
+        both = _tall.gram([(psi, False), (prev.psi, False)])
+        align = np.abs(np.diag(both[:d_eff, d_eff:]))
+        order = np.argsort(align)
+        refresh = {int(i) for i in (order[::-1] if printed_ranking else order)[:n_update]}
+        keep = {k: int(prev.indices[k]) for k in range(d_eff) if k not in refresh}
+    indices = deim_greedy(psi, keep=keep)
+    ones = torch.ones((psi.shape[0], 1), dtype=torch.float64, device="cuda")
+    colsum = _tall.gram([(psi, False), (ones, False)])[:d_eff, d_eff]
+    weights = np.linalg.solve(_rows(psi, indices).T, charge.charge_weight * colsum)
+    return DEIMModel(psi=psi, indices=indices, weights=weights)
+
+
+def fit_deim(samples, dim, charge, prev=None, full=True, n_update=None, printed_ranking=False):
+    """Reference signature: samples (N x cols) host or device -> DEIMModel."""
+    if not isinstance(samples, torch.Tensor):
+        samples = torch.from_numpy(np.ascontiguousarray(samples, dtype=np.float64)).to("cuda")
+    if not bool(torch.any(samples != 0)):
+        raise DegenerateDataError("DEIM sample window is identically zero")
+    win = DeimWindow(1)
+    # split wide sample blocks so each Gram call stays <= 256 columns
+    cols = samples.shape[1]
+    win.capacity = (cols + 63) // 64
+    for c0 in range(0, cols, 64):
+        win.append(samples[:, c0:c0 + 64].contiguous())
+    return fit_deim_device(win, dim, charge, prev=prev, full=full, n_update=n_update,
+                           printed_ranking=printed_ranking)
+
+
+# ------------------------------------------------------------ hyper stage
+
+def make_hyper_stage_device(dmd, deim, t_stage, system, params=None):
+    """Coefficient-gradient factory for one RK stage (hyper.py:299-332):
+    g(z) = (U_V^T U_V) z + m_p^-1 U_X[I]^T (dphi|_I * w), with the DMD potential
+    extrapolated on the device once per stage and the DEIM-sampled gather +
+    projection in picrom_deim_gather."""
+    from .driver import _inst_table, _column_charge
+    idx = np.asarray(deim.indices, dtype=np.int64)
+    qw_ref = system.charge.charge_weight
+
+    def factory(u_mid):
+        n2, n = u_mid.shape
+        N = n2 // 2
+        uxd = torch.from_numpy(_rows(u_mid, idx)).to("cuda")
+        uvtuv = _tall.gram([(u_mid[N:], False)])
+        w = torch.from_numpy(np.asarray(deim.weights, dtype=np.float64)).to("cuda")
+        cache = {}
+
+        def g(z):
+            z = np.asarray(z, dtype=float)
+            p = z.shape[1]
+            if "phi" not in cache:
+                if params is not None:
+                    dmd.ensure_coords(params)
+                cache["phi"] = dmd.potential_device(t_stage)
+                scale = np.array([_column_charge(system, j).charge_weight / qw_ref
+                                  for j in range(p)])
+                cache["scale"] = (None if np.all(scale == 1.0)
+                                  else torch.from_numpy(scale).to("cuda"))
+            zd = torch.from_numpy(np.ascontiguousarray(z)).to("cuda")
+            out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+            st = dev.new_status()
+            inst = _inst_table(system, p)
+            _lib.call("picrom_deim_gather", uxd.data_ptr(), zd.data_ptr(), p, cache["phi"].data_ptr(),
+                      inst.data_ptr(), None, w.data_ptr(), dev.ptr(cache["scale"]), len(idx), n, p,
+                      system.mesh.num_cells, system.mesh.degree, out.data_ptr(), p, st.data_ptr(),
+                      dev.stream_handle())
+            return uvtuv @ z + out.cpu().numpy()
+
+        return g
+
+    return factory
+
+
+def make_hyper_stage(dmd, deim, t_stage, mesh, charge, params=None):
+    """Reference signature (single mesh): see make_hyper_stage_device."""
+    from .fullorder import VlasovSystem
+    return make_hyper_stage_device(dmd, deim, t_stage, VlasovSystem(mesh, charge), params)
+
+
+def hyper_hamiltonian(dmd, deim, u, z, t, mesh, charge):
+    """Surrogate energy 0.5 z^T(U_V^T U_V)z + (0.5/m_p) w . (phi.lambda)|_I (hyper.py:280-296);
+    diagnostics only."""
+    from .fem import eval_basis
+    if not isinstance(u, torch.Tensor):
+        u = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).to("cuda")
+    N = u.shape[0] // 2
+    uxd = _rows(u, np.asarray(deim.indices, dtype=np.int64))
+    gv = _tall.gram([(u[N:], False)])
+    kin = 0.5 * np.einsum("ij,ij->j", z, gv @ z)
+    lam = eval_basis(mesh, uxd @ z).matvec(dmd.potential(t))
+    return kin + (0.5 / charge.particle_mass) * (deim.weights @ lam)

@@ -1,0 +1,290 @@
+"""Dynamical ortho-symplectic reduced basis on the GPU -- drop-in for picrom.reduction.
+
+Same functions and argument meaning as /root/reference/pkg/src/picrom/
+reduction.py (jmul, jrmul, complex_svd_basis, reconstruct,
+orthosymplectic_residuals, SMatrix, select_parameter_subset, basis_velocity,
+retraction, tangent_velocity, fixed_point, prk2_step, PRKResult).
+
+The basis U (2N x n) stays on the device; every O(N) product is either one
+tall-skinny Gram (picrom_paired_gram) or one tall-skinny combine
+(picrom_combine).  The n x n / 2n x 2n algebra between them (Cholesky of S,
+capacitance solve, transport solves) runs on the host in numpy/LAPACK exactly
+as in the reference, from device-computed Grams:
+
+* basis_velocity  (reduction.py:143-153): one Gram of [U, GZ^T, J GZ^T],
+  one combine  xi = (J GZ^T) S^-1 + GZ^T (J S^-1) - U Q
+* retraction      (reduction.py:156-167): one Gram of [U, xi], one combine
+  U (I - M Y1/2 - Y2) + xi Y1 with the capacitance solve in between
+* tangent_velocity (reduction.py:170-182): one Gram of [U, xi, r, x_eval],
+  one combine
+Small inputs (Z, S, subsets) are host numpy arrays as in the reference;
+tall ones are CUDA tensors (numpy tall inputs are uploaded and the result
+returned as numpy).
+"""
+
+from __future__ import annotations
+
+import warnings
+from contextlib import nullcontext
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+from scipy.linalg import cho_factor, cho_solve, eigvalsh, svd
+
+from . import _tall
+from .errors import ConfigurationError, StepFailureError
+
+__all__ = [
+    "jmul", "jrmul", "complex_svd_basis", "reconstruct", "orthosymplectic_residuals", "SMatrix",
+    "select_parameter_subset", "basis_velocity", "retraction", "tangent_velocity", "fixed_point",
+    "prk2_step", "PRKResult",
+]
+
+
+def jmul(m):
+    """J @ m for J = [[0, I], [-I, 0]] (reduction.py:44-47)."""
+    half = m.shape[0] // 2
+    if isinstance(m, torch.Tensor):
+        return torch.cat([m[half:], -m[:half]], dim=0)
+    return np.concatenate([m[half:], -m[:half]], axis=0)
+
+
+def jrmul(m):
+    """m @ J (reduction.py:50-53)."""
+    half = m.shape[1] // 2
+    if isinstance(m, torch.Tensor):
+        return torch.cat([-m[:, half:], m[:, :half]], dim=1)
+    return np.concatenate([-m[:, half:], m[:, :half]], axis=1)
+
+
+def _tall_in(a):
+    """(CUDA tensor, was_numpy) for a tall operand."""
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.float64).contiguous(), False
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda"), True
+
+
+def _tall_out(t, was_numpy):
+    return t.cpu().numpy() if was_numpy else t
+
+
+def complex_svd_basis(x, v, n, device=False):
+    """U = [[Phi, -Psi], [Psi, Phi]] from the complex SVD of x + i v (reduction.py:56-76).
+
+    One-time initialisation: the SVD runs in host LAPACK exactly as in the
+    reference (bit-identical U, Z); ``device=True`` returns U as a CUDA tensor.
+    """
+    if isinstance(x, torch.Tensor):
+        x = x.cpu().numpy()
+    if isinstance(v, torch.Tensor):
+        v = v.cpu().numpy()
+    x = np.atleast_2d(np.asarray(x, dtype=float).T).T
+    v = np.atleast_2d(np.asarray(v, dtype=float).T).T
+    if n % 2 or n < 2:
+        raise ConfigurationError(f"basis dimension must be even and >= 2, got {n}")
+    half = n // 2
+    if half > min(x.shape):
+        raise ConfigurationError(f"rank {half} complex basis needs at least {half} snapshots")
+    uc = svd(x + 1j * v, full_matrices=False)[0]
+    phi, psi = uc[:, :half].real, uc[:, :half].imag
+    u = np.block([[phi, -psi], [psi, phi]])
+    bign = x.shape[0]
+    z = u[:bign].T @ x + u[bign:].T @ v
+    if device:
+        return torch.from_numpy(u).to("cuda"), z
+    return u, z
+
+
+def reconstruct(u, z):
+    """(U_X z, U_V z) (reduction.py:79-82); a plain library GEMM off the hot path
+    (the hot path never forms the reconstruction, see rom_field/rom_gather)."""
+    ud, was_np = _tall_in(u)
+    zd = torch.as_tensor(np.asarray(z, dtype=np.float64) if not isinstance(z, torch.Tensor) else z,
+                         dtype=torch.float64, device="cuda")
+    half = ud.shape[0] // 2
+    return _tall_out(ud[:half] @ zd, was_np), _tall_out(ud[half:] @ zd, was_np)
+
+
+def orthosymplectic_residuals(u):
+    """(||U^T U - I||_F, ||U^T J U - J_n||_F) (reduction.py:85-90) from one Gram."""
+    ud, _ = _tall_in(u)
+    n = ud.shape[1]
+    G = _tall.gram([(ud, False), (ud, True)])
+    utu, utju = G[:n, :n], G[:n, n:]
+    return (float(np.linalg.norm(utu - np.eye(n))),
+            float(np.linalg.norm(utju - jmul(np.eye(n)))))
+
+
+class SMatrix:
+    """Coefficient Gram S = Z Z^T + J^T Z Z^T J, Cholesky-factored (reduction.py:93-107).
+
+    Z is a host (n x p*) array; the algebra is the reference's, in LAPACK."""
+
+    def __init__(self, z, cond_warn=1e12):
+        z = np.asarray(z, dtype=float)
+        a = z @ z.T
+        self.matrix = a - jmul(jrmul(a))
+        eigs = eigvalsh(self.matrix)
+        self.cond = float(eigs[-1] / max(eigs[0], np.finfo(float).tiny))
+        if self.cond > cond_warn:
+            warnings.warn(f"coefficient Gram matrix is ill-conditioned (cond ~ {self.cond:.2e})")
+        self._cho = cho_factor(self.matrix)
+
+    def solve_right(self, m):
+        return cho_solve(self._cho, np.asarray(m).T).T
+
+
+def select_parameter_subset(z, count, printed_variant=False):
+    """Farthest-point greedy subsample of coefficient columns (reduction.py:110-140)."""
+    z = np.asarray(z, dtype=float)
+    p = z.shape[1]
+    if not 1 <= count <= p:
+        raise ConfigurationError(f"subset size must be in [1, {p}], got {count}")
+    sel = [int(np.argmax(np.einsum("ij,ij->j", z, z)))]
+    if printed_variant:
+        for j in range(p):
+            if len(sel) == count:
+                break
+            if j not in sel:
+                sel.append(j)
+        return np.asarray(sel, dtype=int)
+    diff = z - z[:, [sel[0]]]
+    d2 = np.einsum("ij,ij->j", diff, diff)
+    while len(sel) < count:
+        nxt = int(np.argmax(d2))
+        sel.append(nxt)
+        diff = z - z[:, [nxt]]
+        d2 = np.minimum(d2, np.einsum("ij,ij->j", diff, diff))
+    return np.asarray(sel, dtype=int)
+
+
+def _times_zt(g, z):
+    """G Z^T as a (2N x n) device tensor; G dense (2N x p') or a lazy device gradient."""
+    if hasattr(g, "times_matrix"):
+        return g.times_matrix(np.asarray(z, dtype=float).T)
+    gd, _ = _tall_in(g)
+    return _tall.combine([(gd, np.asarray(z, dtype=float).T, False)])
+
+
+def basis_velocity(u, z, g, s=None):
+    """(I - U U^T)(J G Z^T - G Z^T J^T) S^{-1} (reduction.py:143-153)."""
+    ud, was_np = _tall_in(u)
+    z = np.asarray(z, dtype=float)
+    s = s or SMatrix(z)
+    n = ud.shape[1]
+    gzt = _times_zt(g, z)
+    G = _tall.gram([(ud, False), (gzt, False), (gzt, True)])
+    u_gzt, u_jgzt = G[:n, n:2 * n], G[:n, 2 * n:]
+    s_inv = s.solve_right(np.eye(n))
+    js_inv = jmul(s_inv)                         # (G Z^T J) S^-1 = G Z^T (J S^-1)
+    q = u_jgzt @ s_inv + u_gzt @ js_inv          # U^T m
+    xi = _tall.combine([(gzt, s_inv, True), (gzt, js_inv, False), (ud, -q, False)])
+    return _tall_out(xi, was_np)
+
+
+def _retraction_coeffs(G, n):
+    P, M, X = G[:n, :n], G[:n, n:], G[n:, n:]
+    utw = M - 0.5 * P @ M
+    wtw = X - M.T @ M + 0.25 * M.T @ P @ M
+    bta = np.block([[utw, -P], [wtw, -utw.T]])
+    cap = np.eye(2 * n) - 0.5 * bta
+    y = np.linalg.solve(cap, np.concatenate([P, utw.T], axis=0))
+    y1, y2 = y[:n], y[n:]
+    return np.eye(n) - 0.5 * M @ y1 - y2, y1
+
+
+def retraction(u, xi):
+    """Low-rank Cayley retraction cay(W U^T - U W^T) U (reduction.py:156-167):
+    u + [w, -u] cap^{-1} [u, w]^T u with w = xi - U (U^T xi)/2, assembled from
+    the Gram of [U, xi] as U (I - M Y1/2 - Y2) + xi Y1."""
+    ud, was_np = _tall_in(u)
+    xd, _ = _tall_in(xi)
+    n = ud.shape[1]
+    cu, cx = _retraction_coeffs(_tall.gram([(ud, False), (xd, False)]), n)
+    return _tall_out(_tall.combine([(ud, cu, False), (xd, cx, False)]), was_np)
+
+
+def tangent_velocity(u, xi, r_xi, x_eval):
+    """Pull a velocity at r_xi = retraction(u, xi) back to u (reduction.py:170-182)."""
+    ud, was_np = _tall_in(u)
+    xd, _ = _tall_in(xi)
+    rd, _ = _tall_in(r_xi)
+    ed, _ = _tall_in(x_eval)
+    n = ud.shape[1]
+    G = _tall.gram([(ud, False), (xd, False), (rd, False), (ed, False)])
+    b = _tall.split(G, [n, n, n, n])
+    P, M, R, E = b[0][0], b[0][1], b[0][2], b[0][3]
+    F, rxi, rxe = b[1][3], b[2][1], b[2][3]
+    eye = np.eye(n)
+    t_u = 0.5 * M @ E + F - 0.5 * M.T @ E         # t = 2 x_eval - xi E + u t_u
+    K = np.linalg.inv(R + eye)                     # ups = t (U^T r + I)^-1
+    c_e, c_x, c_u = 2.0 * K, -E @ K, t_u @ K       # ups = x_eval c_e + xi c_x + u c_u
+    rt_ups = rxe @ c_e + rxi @ c_x + R.T @ c_u
+    ut_ups = E @ c_e + M @ c_x + P @ c_u
+    lead = np.linalg.solve(R.T + eye, rt_ups + ut_ups)
+    out = _tall.combine([(ed, c_e, False), (xd, c_x, False), (ud, c_u - lead - ut_ups.T, False)])
+    return _tall_out(out, was_np)
+
+
+def scaled(a, c):
+    """c * a for a tall device operand (the combine kernel with c*I)."""
+    ad, was_np = _tall_in(a)
+    return _tall_out(_tall.combine([(ad, c * np.eye(ad.shape[1]), False)]), was_np)
+
+
+def fixed_point(map_fn, z0, tol=1e-9, max_iter=100):
+    """z <- map_fn(z) until the relative update is below tol (reduction.py:185-202)."""
+    z = z0
+    trace = []
+    for it in range(1, max_iter + 1):
+        z_new = map_fn(z)
+        num = float(np.linalg.norm(z_new - z))
+        den = max(float(np.linalg.norm(z_new)), np.finfo(float).tiny)
+        trace.append(num / den)
+        z = z_new
+        if num <= tol * den:
+            return z, it, trace
+    raise StepFailureError(
+        f"implicit coefficient stage did not converge in {max_iter} iterations "
+        f"(last relative update {trace[-1]:.3e})", iterations=max_iter, residual_trace=trace)
+
+
+@dataclass
+class PRKResult:
+    u: object
+    z: np.ndarray
+    u_mid: object
+    z_mid: np.ndarray
+    fp_iterations: int
+    s_cond: float
+
+
+class _NullTimers:
+    def phase(self, name):
+        return nullcontext()
+
+
+def prk2_step(u, z, dt, sub, grad_sub, g_sub0, coeff_stage, fp_tol=1e-9, fp_max_iter=100,
+              timers=None):
+    """One partitioned RK2 step of (U, Z) (reduction.py:220-259), same seams:
+    grad_sub(u, z_sub) and coeff_stage(u_mid) -> g(z) are injected callables."""
+    timers = timers or _NullTimers()
+    with timers.phase("rom_basis"):
+        s0 = SMatrix(z[:, sub])
+        xi1 = basis_velocity(u, z[:, sub], g_sub0, s=s0)
+        half_step = scaled(xi1, 0.5 * dt)
+        u_mid = retraction(u, half_step)
+        g = coeff_stage(u_mid)
+    with timers.phase("rom_coeff"):
+        k, iterations, _ = fixed_point(lambda kk: jmul(g(z + 0.5 * dt * kk)), np.zeros_like(z),
+                                       fp_tol, fp_max_iter)
+        z_new = z + dt * k
+        z_mid = z + 0.5 * dt * k
+    with timers.phase("rom_basis"):
+        g_mid = grad_sub(u_mid, z_mid[:, sub])
+        xi_mid = basis_velocity(u_mid, z_mid[:, sub], g_mid)
+        xi2 = tangent_velocity(u, half_step, u_mid, xi_mid)
+        u_new = retraction(u, scaled(xi2, dt))
+    return PRKResult(u=u_new, z=z_new, u_mid=u_mid, z_mid=z_mid, fp_iterations=iterations,
+                     s_cond=s0.cond)

@@ -59,6 +59,44 @@ def test_locate_and_tables(gfem, d):
             np.testing.assert_allclose(gg.weights[m], og.w[m], rtol=0, atol=1e-15 / om.h)
 
 
+def test_locate_division_is_ieee(lib_built):
+    """The device x/h (Markstein correction with RN(1/h)) equals IEEE division:
+    frac = s - floor(s) is exact, so bitwise-equal frac means bitwise-equal s."""
+    import torch
+    from paper_2201_05555_b200 import _device as dev
+    from paper_2201_05555_b200 import _lib
+    rng = np.random.default_rng(0)
+    for L, nx in ((4 * np.pi, 64), (10 * np.pi, 128), (2 * np.pi / 0.3, 512), (1.0, 3), (7.77, 100)):
+        h = L / nx
+        parts = [rng.uniform(-3 * L, 3 * L, 2_000_000),
+                 rng.integers(-10 * nx, 10 * nx, 200_000) * h,
+                 np.nextafter(rng.integers(-10 * nx, 10 * nx, 200_000) * h, np.inf),
+                 np.nextafter(rng.integers(-10 * nx, 10 * nx, 200_000) * h, -np.inf),
+                 rng.uniform(-1e6, 1e6, 200_000), rng.standard_normal(200_000) * 1e-300]
+        x = np.concatenate(parts)
+        xd = torch.from_numpy(x).cuda().reshape(1, -1)
+        n = x.size
+        i0 = torch.empty((1, n), dtype=torch.int64, device="cuda")
+        fr = torch.empty((1, n), dtype=torch.float64, device="cuda")
+        st = dev.new_status()
+        inst = dev.inst_rows(gfem_mesh(L, nx), gfem_charge(L), 1)
+        _lib.call("picrom_locate", xd.data_ptr(), n, 1, n, inst.data_ptr(), nx, i0.data_ptr(),
+                  fr.data_ptr(), n, st.data_ptr(), dev.stream_handle())
+        s = x / h
+        np.testing.assert_array_equal(fr.cpu().numpy()[0], s - np.floor(s))
+        np.testing.assert_array_equal(i0.cpu().numpy()[0], np.floor(s).astype(np.int64) % nx)
+
+
+def gfem_mesh(L, nx):
+    from paper_2201_05555_b200 import fem
+    return fem.build_mesh(L, nx)
+
+
+def gfem_charge(L):
+    from paper_2201_05555_b200 import fem
+    return fem.ChargeConfig(1000, L)
+
+
 def test_golden_p1_end_to_end(gfem):
     g = np.load(GOLDEN / "fem_p1.npz")
     L, nx = float(g["length"]), int(g["nx"])

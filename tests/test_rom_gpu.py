@@ -1,0 +1,180 @@
+"""GPU reduced-basis path vs the reference golden runs and the CPU oracle.
+
+* building blocks (basis_velocity / retraction / tangent_velocity / residuals)
+  against the reference's own outputs (tests/golden/rom_p1.npz);
+* exact_gradients and the warm-up stage vs the oracle at degrees 1-3, single
+  mesh and per-instance meshes (BASELINE C3/C4), 1e-12;
+* run_reduced (no hyper-reduction) vs the reference golden run (degree 1) and
+  vs the oracle with per-instance meshes (degree 2);
+* DEIM: greedy indices bit-exact given the oracle's basis, DMD extrapolation,
+  DEIM-sampled stage gradient, and a short hyper-reduced run.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import dmd_deim as odd
+from oracle import fe_bspline as ofe
+from oracle import manifold as omf
+from oracle import rom_loop as orl
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def m(lib_built):
+    from paper_2201_05555_b200 import driver, fem, fullorder, hyper, reduction
+    return type("M", (), dict(driver=driver, fem=fem, fullorder=fullorder, hyper=hyper,
+                              red=reduction))
+
+
+@pytest.fixture(scope="module")
+def g():
+    return np.load(GOLDEN / "rom_p1.npz")
+
+
+def test_building_blocks_vs_reference(m, g):
+    u, z = g["bb_u"], g["bb_z"]
+    xi = m.red.basis_velocity(u, z, g["bb_g"])
+    assert rel(xi, g["bb_xi"]) <= 1e-12
+    r = m.red.retraction(u, 0.1 * g["bb_xi"])
+    assert rel(r, g["bb_r"]) <= 1e-13
+    t = m.red.tangent_velocity(u, 0.1 * g["bb_xi"], g["bb_r"], g["bb_xe"])
+    assert rel(t, g["bb_tan"]) <= 1e-12
+    o, s = m.red.orthosymplectic_residuals(g["bb_r"])
+    oo, os_ = omf.structure_defects(g["bb_r"])
+    assert abs(o - oo) < 1e-14 and abs(s - os_) < 1e-14
+    np.testing.assert_array_equal(m.red.SMatrix(z).matrix, g["bb_s"])
+    np.testing.assert_array_equal(m.red.select_parameter_subset(z, 5), g["bb_sub"])
+
+
+def _setup(m, d, per_instance, n=3000, p=6, nx=32, nb=4, seed=0):
+    rng = np.random.default_rng(seed)
+    ks = rng.uniform(0.4, 0.6, p) if per_instance else np.full(p, 0.5)
+    lengths = 2 * np.pi / ks
+    x0 = np.stack([rng.uniform(0, L, n) for L in lengths], axis=1)
+    v0 = rng.standard_normal((n, p))
+    u, z = omf.csvd_basis(x0, v0, nb)
+    osys = orl.ParamSystem(lengths, nx, d, n)
+    gsys = m.driver.ParametricVlasovSystem(lengths, nx, d, n)
+    return u, z, osys, gsys, x0, v0, lengths
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("per_instance", [False, True])
+def test_exact_gradients_vs_oracle(m, d, per_instance):
+    u, z, osys, gsys, *_ = _setup(m, d, per_instance)
+    og, ophi, olam = orl.exact_gradients(osys, u, z)
+    gg, gphi, glam = m.driver.exact_gradients(gsys, u, z)
+    assert rel(gphi, ophi) <= 1e-12
+    assert rel(gg, og) <= 1e-12
+    assert rel(glam, olam) <= 1e-12
+    # warm-up stage g(z) = U^T F(U z)
+    o_stage = orl.full_stage(osys)(u)(z)
+    import torch
+    g_stage = m.driver.make_full_stage(gsys)(torch.from_numpy(u).cuda())(z)
+    assert rel(g_stage, o_stage) <= 1e-12
+
+
+def test_reduced_run_no_hyper_vs_reference(m, g):
+    L, nx = float(g["length"]), int(g["nx"])
+    mesh = m.fem.build_mesh(L, nx)
+    sysm = m.fullorder.VlasovSystem(mesh, m.fem.ChargeConfig(g["a_x0"].shape[0], L))
+    rec = m.driver.run_reduced(sysm, g["a_params"], g["a_x0"], g["a_v0"], basis_dim=4, subsample=4,
+                               window=3, deim_dim=8, deim_period=3, deim_update=2, dt=0.02,
+                               t_final=0.1, hyper_reduction=False, snapshot_stride=5,
+                               energy_stride=1, decomp_stride=10**9)
+    u, z = rec.bases[-1]
+    np.testing.assert_allclose(u.cpu().numpy(), g["nohyper_u"], atol=1e-12)
+    np.testing.assert_allclose(z, g["nohyper_z"], atol=1e-12)
+    assert np.max(np.abs(rec.electric_energy - g["nohyper_ee"]) / np.abs(g["nohyper_ee"])) <= 1e-9
+    np.testing.assert_array_equal(rec.fp_iterations, g["nohyper_fp"])
+
+
+def test_reduced_run_per_instance_vs_oracle(m):
+    """C3-like: per-instance wavenumbers, quadratic splines, no hyper-reduction."""
+    u, z, osys, gsys, x0, v0, lengths = _setup(m, 2, True, n=4000, p=8, nx=32, nb=4, seed=3)
+    params = np.stack([2 * np.pi / lengths, np.linspace(0.01, 0.1, 8)], axis=1)
+    kw = dict(basis_dim=4, subsample=8, window=3, deim_dim=8, deim_period=3, deim_update=2,
+              dt=0.05)
+    h = orl.run_reduced(osys, params, x0, v0, num_steps=6, hyper_reduction=False,
+                        energy_stride=1, **kw)
+    rec = m.driver.run_reduced(gsys, params, x0, v0, t_final=0.3, hyper_reduction=False,
+                               energy_stride=1, decomp_stride=10**9, **kw)
+    u_g, z_g = rec.bases[-1]
+    assert rel(u_g.cpu().numpy(), h.u) <= 1e-11
+    assert rel(z_g, h.z) <= 1e-11
+    ee_o = np.asarray(h.electric)
+    assert np.max(np.abs(rec.electric_energy - ee_o) / np.abs(ee_o)) <= 1e-9
+    np.testing.assert_array_equal(rec.fp_iterations, np.asarray(h.fp_iterations))
+
+
+def test_deim_greedy_bit_exact_given_basis(m):
+    rng = np.random.default_rng(11)
+    psi = np.linalg.qr(rng.standard_normal((20000, 12)))[0]
+    want = odd.greedy_indices(psi)
+    got = m.hyper.deim_greedy(psi)
+    np.testing.assert_array_equal(got, want)
+    keep = {0: int(want[0]), 3: int(want[3]), 7: int(want[7])}
+    np.testing.assert_array_equal(m.hyper.deim_greedy(psi, keep=dict(keep)),
+                                  odd.greedy_indices(psi, keep=dict(keep)))
+
+
+def test_deim_fit_and_golden(m, g):
+    ch = m.fem.ChargeConfig(80, 2 * np.pi)
+    dm = m.hyper.fit_deim(g["de_samples"], 10, ch)
+    np.testing.assert_array_equal(dm.indices, g["de_idx"])
+    np.testing.assert_allclose(dm.weights, g["de_w"], rtol=1e-9)
+    # span agreement with the reference basis (principal angles)
+    s = np.linalg.svd(dm.psi.cpu().numpy().T @ g["de_psi"], compute_uv=False)
+    assert np.min(s) > 1 - 1e-10
+
+
+def test_dmd_device_extrapolation_matches_host(m, g):
+    model = m.hyper.fit_parametric_dmd(list(g["dmd_win"]), 0.05, 0.4, g["dmd_prm"],
+                                       np.array([1, 3, 5]))
+    model.ensure_coords(g["dmd_prm"])
+    np.testing.assert_array_equal(model.eigenvalues, g["dmd_eigs"])
+    host = model.potential(0.45)
+    assert rel(host, g["dmd_phi"]) <= 1e-14
+    devv = model.potential_device(0.45).cpu().numpy().T
+    assert rel(devv, g["dmd_phi"]) <= 1e-13
+
+
+def test_hyper_stage_vs_oracle(m):
+    u, z, osys, gsys, x0, v0, lengths = _setup(m, 2, True, n=3000, p=6, nx=32, nb=4, seed=5)
+    rng = np.random.default_rng(1)
+    idx = rng.choice(3000, 12, replace=False)
+    w = rng.standard_normal(12)
+    win = [rng.standard_normal((32, 3)) for _ in range(5)]
+    params = rng.uniform(size=(6, 2))
+    od = odd.parametric_dmd(win, 0.05, 0.2, params, np.array([0, 2, 4]))
+    gd = m.hyper.fit_parametric_dmd(win, 0.05, 0.2, params, np.array([0, 2, 4]))
+    deim_o = odd.Deim(psi=None, indices=idx, weights=w)
+    deim_g = m.hyper.DEIMModel(psi=None, indices=idx, weights=w)
+    go = orl.hyper_stage(osys, od, deim_o, 0.225, params)(u)(z)
+    import torch
+    gg = m.hyper.make_hyper_stage_device(gd, deim_g, 0.225, gsys, params)(torch.from_numpy(u).cuda())(z)
+    assert rel(gg, go) <= 1e-12
+
+
+def test_reduced_run_with_hyper_reduction(m):
+    """Hyper-reduction engages after the window fills; energies track the oracle."""
+    u, z, osys, gsys, x0, v0, lengths = _setup(m, 1, False, n=3000, p=6, nx=16, nb=4, seed=7)
+    params = np.stack([np.linspace(0.03, 0.06, 6), np.linspace(0.8, 1.0, 6)], axis=1)
+    kw = dict(basis_dim=4, subsample=4, window=2, deim_dim=8, deim_period=2, deim_update=3,
+              dt=0.01)
+    h = orl.run_reduced(osys, params, x0, v0, num_steps=8, energy_stride=1, **kw)
+    rec = m.driver.run_reduced(gsys, params, x0, v0, t_final=0.08, energy_stride=1,
+                               decomp_stride=10**9, **kw)
+    assert rec.hyper_engaged and h.hyper_engaged
+    for a, b in zip(rec.deim_indices, h.deim_indices):
+        np.testing.assert_array_equal(a, b)
+    ee_o = np.asarray(h.electric)
+    assert np.max(np.abs(rec.electric_energy - ee_o) / np.abs(ee_o)) <= 1e-9
