@@ -182,23 +182,22 @@ def run_ours(args, w, rank, world, local_rank):
     run = fullorder.PicRun(sysm, xd, vd, w.dt, total_steps)
     run.init_field()
     run.advance(1)                      # the half-kick first step
+    e = run.e
     s = dev.stream_handle()
     gp = p * run.nx
 
     def push():
-        _lib.call("picrom_pic_push", run.x.data_ptr(), run.v.data_ptr(), n, p, n,
-                  run.inst.data_ptr(), run.nx, run.degree, run.phi.data_ptr(), run.dt, run.dt,
-                  0.5 * run.dt, 0, run.counter.data_ptr(), run.ws.data_ptr(),
-                  run.status.data_ptr(), s)
+        _lib.call("picrom_pic_push", e.x.data_ptr(), e.v.data_ptr(), n, p, n,
+                  e.inst.data_ptr(), e.nx, e.degree, e.phi.data_ptr(), e.dt, e.dt,
+                  0.5 * e.dt, 0, e.counter.data_ptr(), e.ws.data_ptr(), e.status.data_ptr(), s)
 
     def solve(hist=True):
-        _lib.call("picrom_pic_solve", n, p, run.nx, run.degree, run.inst.data_ptr(),
-                  run.c.khat.data_ptr(), run.c.stencil.data_ptr(), run.phi.data_ptr(), 0,
-                  run.counter.data_ptr(),
-                  run.rho_hist.data_ptr() + 8 * gp if hist else None,
-                  run.phi_hist.data_ptr() + 8 * gp if hist else None,
-                  run.ee_hist.data_ptr() + 8 * p if hist else None,
-                  run.kin_hist.data_ptr() if hist else None, run.ws.data_ptr(), s)
+        _lib.call("picrom_pic_solve", n, p, e.nx, e.degree, e.inst.data_ptr(),
+                  e.c.khat.data_ptr(), e.c.stencil.data_ptr(), e.phi.data_ptr(), 0,
+                  e.counter.data_ptr(), e.ring,
+                  e.r_rho.data_ptr() if hist else None, e.r_phi.data_ptr() if hist else None,
+                  e.r_ee.data_ptr() if hist else None, e.r_kin.data_ptr() if hist else None,
+                  e.ws.data_ptr(), s)
 
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
     for _ in range(args.warmup):
@@ -222,7 +221,6 @@ def run_ours(args, w, rank, world, local_rank):
             push()
             solve(hist=False)
         torch.cuda.synchronize()
-    run.counter[0] = args.warmup + 1        # history rows of the timed steps
     torch.cuda.synchronize()
     for k in range(args.steps):
         flush.zero_()                       # L2 flush outside the timed events
@@ -252,8 +250,10 @@ def run_ours(args, w, rank, world, local_rank):
     torch.cuda.empty_cache()
     ens = fullorder.ParticleEnsemble(xn, vn, 0.0)
     rec_opts = fullorder.RecordOptions(energy_stride=1, record_snapshots=False)
-    fullorder.run_full_order(sysm, fullorder.ParticleEnsemble(xn[:1000].clone(), vn[:1000].clone(), 0.0),
-                             w.dt, 2 * w.dt, record=rec_opts)   # warm the graph path
+    # warm-up call of the same shape (engine + CUDA graph capture happen once
+    # per system/shape; the timed call is the steady-state user call)
+    fullorder.run_full_order(sysm, fullorder.ParticleEnsemble(xn, vn, 0.0), w.dt, 20 * w.dt,
+                             record=rec_opts)
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()

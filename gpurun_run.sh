@@ -1,13 +1,11 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-B="python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 20"
-timeout 200 $B > gpurun_out/b_tma_default.log 2>&1
-PICROM_TMA_CFG=8,2 timeout 200 $B > gpurun_out/b_tma_8_2.log 2>&1
-PICROM_TMA_CFG=8,4 timeout 200 $B > gpurun_out/b_tma_8_4.log 2>&1
-PICROM_NO_TMA=1 timeout 200 $B > gpurun_out/b_notma_u4b3.log 2>&1
-for v in u2_b3 u4_b2 u2_b2; do PICROM_NO_TMA=1 PICROM_LIB=$PWD/build/variants/lib_$v.so timeout 200 $B > gpurun_out/b_notma_$v.log 2>&1; done
-PICROM_NO_TMA=1 PICROM_HIST_KB=36 timeout 200 $B > gpurun_out/b_notma_kb36.log 2>&1
-timeout 300 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 5 > gpurun_out/b_c5_tma.log 2>&1
-PICROM_NO_TMA=1 timeout 300 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 5 > gpurun_out/b_c5_notma.log 2>&1
-timeout 300 python bench.py --config C1 --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 200 > gpurun_out/b_c1.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 400 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 300 python tools/e2e_breakdown.py C2 500 > gpurun_out/e2e_breakdown.log 2>&1
+timeout 300 python bench.py --config C1 --no-cpu-baseline > gpurun_out/bench_c1.log 2>&1
+timeout 300 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 20 > gpurun_out/bench_c5.log 2>&1
+CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 10"
+$CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
+$CMD > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"step_kernel|solve_kernel" -s 8 -c 2 -o gpurun_out/prof_step $CMD > gpurun_out/ncu_full.log 2>&1
 echo done

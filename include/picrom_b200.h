@@ -137,7 +137,9 @@ int picrom_pic_step(double* x, double* v, long long n, int p, long long ld,
 /* The two halves of picrom_pic_step, for callers that time or schedule them
  * separately: the fused particle pass (writes the deposit segments and the
  * kinetic partials into the workspace) and the per-instance solve that
- * consumes them (same history/counter semantics as picrom_pic_step). */
+ * consumes them (same history/counter semantics as picrom_pic_step, except
+ * that with a counter and hist_rows > 0 the history row is *counter modulo
+ * hist_rows -- a ring that a replayed CUDA graph can keep writing). */
 int picrom_pic_push(double* x, double* v, long long n, int p, long long ld,
                     const double* inst, int nx, int degree, const double* phi,
                     double dt, double kick, double kfull, long long step,
@@ -145,9 +147,9 @@ int picrom_pic_push(double* x, double* v, long long n, int p, long long ld,
                     unsigned long long* status, void* stream);
 int picrom_pic_solve(long long n, int p, int nx, int degree, const double* inst,
                      const double* khat, const double* stencil, double* phi,
-                     long long step, long long* counter, double* rho_hist,
-                     double* phi_hist, double* ee_hist, double* kin_hist,
-                     void* workspace, void* stream);
+                     long long step, long long* counter, long long hist_rows,
+                     double* rho_hist, double* phi_hist, double* ee_hist,
+                     double* kin_hist, void* workspace, void* stream);
 
 /* Reference-arithmetic Verlet (fullorder.py:122-134, bit-for-bit operation
  * order): drift  x1 = x + dt*(v + (0.5*dt)*e0), rho1 = deposit(x1), phi1 = solve;

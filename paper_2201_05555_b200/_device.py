@@ -79,16 +79,19 @@ def from_device(t_pn, meta, dtype=torch.float64):
     """(p, rows) device array -> the caller's kind/shape, reference layout."""
     p, rows = t_pn.shape
     if meta.ndim == 1:
-        out = t_pn.reshape(rows)
+        out = t_pn.reshape(rows).clone()
     elif p == 1:
-        out = t_pn.reshape(rows, 1)
+        out = t_pn.reshape(rows, 1).clone()
     else:
         out = torch.empty((rows, p), dtype=t_pn.dtype, device="cuda")
         name = "picrom_transpose_i64" if t_pn.dtype == torch.int64 else "picrom_transpose"
         _lib.call(name, t_pn.data_ptr(), p, rows, out.data_ptr(), stream_handle())
-    if meta.kind == "numpy":
-        return out.cpu().numpy()
-    return out if meta.device is None or str(meta.device).startswith("cuda") else out.to(meta.device)
+    if meta.kind == "numpy" or (meta.device is not None and not str(meta.device).startswith("cuda")):
+        # device -> pinned host staging (torch's caching host allocator reuses it)
+        host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        host.copy_(out)
+        return host.numpy() if meta.kind == "numpy" else host
+    return out
 
 
 def per_instance(v_p, meta):

@@ -34,8 +34,8 @@ SIGNATURES = {
                              _d, _d, _d, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "picrom_pic_push": (_i, [_vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _d, _d, _d, _ll, _vp,
                              _vp, _vp, _vp]),
-    "picrom_pic_solve": (_i, [_ll, _i, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp,
-                              _vp, _vp]),
+    "picrom_pic_solve": (_i, [_ll, _i, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _ll, _vp, _vp, _vp,
+                              _vp, _vp, _vp]),
     "picrom_verlet_drift": (_i, [_vp, _vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _vp,
                                  _d, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "picrom_verlet_kick": (_i, [_vp, _vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _d, _vp, _vp, _vp]),

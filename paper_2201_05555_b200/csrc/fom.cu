@@ -96,7 +96,7 @@ static int step_nt() {
   static int nt = 0;
   if (!nt) {
     const char* s = getenv("PICROM_STEP_NT");
-    nt = (s && atoi(s) == 128) ? 128 : 256;
+    nt = (s && atoi(s) == 256) ? 256 : 128;      // 128 measured best (profiles/r01)
   }
   return nt;
 }
@@ -238,7 +238,7 @@ step_kernel(StepArgs a) {
   const double inv_nx = 1.0 / (double)nx;
   const int mask = (nx & (nx - 1)) == 0 ? nx - 1 : -1;
   const long long step_id = a.counter ? (*a.counter + 1) : a.step;
-  const int woff = (tid >> 5) * 32 * U + lane;
+  const int woff = (tid >> 5) * 32 * U + lane;   // lane's offset inside a SPAN block
 
   long long pos = start;
   while (pos < end) {
@@ -265,30 +265,31 @@ step_kernel(StepArgs a) {
     __syncthreads();
 
     double kin = 0.0;
-    double* X = a.x + (size_t)j * a.ld;
-    double* V = a.v + (size_t)j * a.ld;
-    const double* E0 = (MODE == MODE_DRIFT) ? a.e0 + (size_t)j * a.ld : nullptr;
-    const double* Y = (MODE == MODE_DEPOSIT && a.y) ? a.y + (size_t)j * a.ld : nullptr;
-    double* XO = (MODE == MODE_DRIFT) ? a.xo + (size_t)j * a.ld : nullptr;
-    double cx[U], cv[U], ce[U];
-    auto load = [&](long long i0, double* lx, double* lv, double* le) {
+    double* X = a.x + (size_t)j * a.ld + seg_lo;
+    double* V = a.v + (size_t)j * a.ld + seg_lo;
+    const double* E0 = (MODE == MODE_DRIFT) ? a.e0 + (size_t)j * a.ld + seg_lo : nullptr;
+    const double* Y = (MODE == MODE_DEPOSIT && a.y) ? a.y + (size_t)j * a.ld + seg_lo : nullptr;
+    double* XO = (MODE == MODE_DRIFT) ? a.xo + (size_t)j * a.ld + seg_lo : nullptr;
+    const int len = (int)(seg_hi - seg_lo);             // < 2^31 (checked on the host)
+
+    // loads of one SPAN block starting at local offset b0 into (lx, lv, le)
+    auto load = [&](int b0, double* lx, double* lv, double* le) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const long long i = i0 + woff + u * 32;
-        const bool in = i < seg_hi;
+        const int i = b0 + woff + u * 32;
+        const bool in = i < len;
         lx[u] = in ? __ldcs(X + i) : 0.0;
         if constexpr (MODE == MODE_LEAPFROG || MODE == MODE_DRIFT) lv[u] = in ? __ldcs(V + i) : 0.0;
         if constexpr (MODE == MODE_DRIFT) le[u] = in ? __ldcs(E0 + i) : 0.0;
         if constexpr (MODE == MODE_DEPOSIT) lv[u] = (in && Y) ? __ldcs(Y + i) : 1.0;
       }
     };
-    if (seg_lo < seg_hi) load(seg_lo, cx, cv, ce);
-    for (long long i0 = seg_lo; i0 < seg_hi; i0 += SPAN) {
-      double px[U], pv[U], pe[U];
-      if (i0 + SPAN < seg_hi) load(i0 + SPAN, px, pv, pe);
+
+    // the particle work of one SPAN block already in registers
+    auto process = [&](int b0, const double* cx, const double* cv, const double* ce) {
       bool valid[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) valid[u] = i0 + woff + u * 32 < seg_hi;
+      for (int u = 0; u < U; ++u) valid[u] = b0 + woff + u * 32 < len;
 
       // pass 1: the particle update (straight-line common path)
       double xn[U];
@@ -321,7 +322,7 @@ step_kernel(StepArgs a) {
           kin = valid[u] ? fma(vn, vn, kin) : kin;
           const double vh = __dadd_rn(cv[u], __dmul_rn(a.kick, E));
           xn[u] = __dadd_rn(cx[u], __dmul_rn(a.dt, vh));
-          const long long i = i0 + woff + u * 32;
+          const int i = b0 + woff + u * 32;
           if (valid[u]) {
             __stcs(X + i, xn[u]);
             __stcs(V + i, vh);
@@ -332,7 +333,7 @@ step_kernel(StepArgs a) {
         for (int u = 0; u < U; ++u) {
           const double vh = __dadd_rn(cv[u], __dmul_rn(a.kick, ce[u]));
           xn[u] = __dadd_rn(cx[u], __dmul_rn(a.dt, vh));
-          if (valid[u]) __stcs(XO + i0 + woff + u * 32, xn[u]);
+          if (valid[u]) __stcs(XO + b0 + woff + u * 32, xn[u]);
         }
       } else {
 #pragma unroll
@@ -359,7 +360,7 @@ step_kernel(StepArgs a) {
             cl[u] = cf.c;
             fr[u] = cf.f;
           } else {
-            record_bad(a.status, step_id, i0 + woff + u * 32, j, a.p);
+            record_bad(a.status, step_id, seg_lo + b0 + woff + u * 32, j, a.p);
             cl[u] = 0;
             fr[u] = 0.0;
           }
@@ -393,8 +394,18 @@ step_kernel(StepArgs a) {
           if constexpr (K > 1) __syncwarp();
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) { cx[u] = px[u]; cv[u] = pv[u]; ce[u] = pe[u]; }
+    };
+
+    // ping-pong register buffers: the loads of one block are in flight while
+    // the other block is processed; no register copies on the loop edge
+    double ax[U], av[U], ae[U], bx[U], bv[U], be[U];
+    if (len > 0) load(0, ax, av, ae);
+    for (int b0 = 0; b0 < len; b0 += 2 * SPAN) {
+      if (b0 + SPAN < len) load(b0 + SPAN, bx, bv, be);
+      process(b0, ax, av, ae);
+      if (b0 + SPAN >= len) break;
+      if (b0 + 2 * SPAN < len) load(b0 + 2 * SPAN, ax, av, ae);
+      process(b0 + SPAN, bx, bv, be);
     }
     __syncthreads();
 
@@ -788,6 +799,7 @@ struct SolveArgs {
   size_t hist_stride_e;     // elements per history row (energies)
   double* phi_hist;         // optional extra copy of phi (history)
   int seg_dense;            // > 0: dense segments seg[(b*p + j)*nx + nd], b < seg_dense
+  long long hist_mod;       // > 0: history row = counter % hist_mod (ring)
   const int* cols;          // optional instance id per column
 };
 
@@ -808,14 +820,15 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   extern __shared__ double sm[];
   const int nx = a.nx;
   double* rho = sm;            // nx
-  double* kh = rho + nx;       // nx
-  double* phi = kh + nx;       // nx
+  double* kh = rho + nx;       // 2 nx (khat repeated)
+  double* phi = kh + 2 * nx;   // nx
   double* red = phi + nx;      // 32
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
   const double* ip = a.inst + (size_t)(a.cols ? a.cols[j] : j) * PICROM_INST_STRIDE;
   const double h = ip[I_H];
-  const long long row = a.counter ? *a.counter : 0;
+  const long long crow = a.counter ? *a.counter : 0;
+  const long long row = a.hist_mod > 0 ? crow % a.hist_mod : crow;
   double* rho_out = a.rho_out ? a.rho_out + row * a.hist_stride_rho : nullptr;
   double* phi_hist = a.phi_hist ? a.phi_hist + row * a.hist_stride_rho : nullptr;
   double* energy_out = a.energy_out ? a.energy_out + row * a.hist_stride_e : nullptr;
@@ -843,7 +856,7 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
     for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] = a.rho_in[(size_t)j * nx + nd];
   }
   if (a.solve)
-    for (int nd = tid; nd < nx; nd += blockDim.x) kh[nd] = a.khat[nd];
+    for (int r = tid; r < 2 * nx; r += blockDim.x) kh[r] = a.khat[r < nx ? r : r - nx];
   __syncthreads();
   if (rho_out)
     for (int nd = tid; nd < nx; nd += blockDim.x) rho_out[(size_t)j * nx + nd] = rho[nd];
@@ -855,16 +868,22 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   const double mean_rho = block_sum(part, red) / (double)nx;
   for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] -= mean_rho;
   __syncthreads();
-  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m
+  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m; kh holds khat
+  // twice (kh[r] = khat[r mod nx], r < 2 nx) so the inner loop has no modulo,
+  // and 4 independent partial sums keep the FMA pipe busy (fixed order)
   part = 0.0;
   for (int nd = tid; nd < nx; nd += blockDim.x) {
-    double s = 0.0;
-    int idx = nd;  // (nd - m) mod nx, m = 0..nx-1
-    for (int m = 0; m < nx; ++m) {
-      s = fma(kh[idx], rho[m], s);
-      idx = (idx == 0) ? nx - 1 : idx - 1;
+    const double* kr = kh + nd + nx;     // kr[-m] = khat[(nd - m) mod nx]
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int m = 0;
+    for (; m + 4 <= nx; m += 4) {
+      s0 = fma(kr[-m], rho[m], s0);
+      s1 = fma(kr[-m - 1], rho[m + 1], s1);
+      s2 = fma(kr[-m - 2], rho[m + 2], s2);
+      s3 = fma(kr[-m - 3], rho[m + 3], s3);
     }
-    phi[nd] = h * s;
+    for (; m < nx; ++m) s0 = fma(kr[-m], rho[m], s0);
+    phi[nd] = h * ((s0 + s1) + (s2 + s3));
     part += phi[nd];
   }
   const double mean_phi = block_sum(part, red) / (double)nx;
@@ -900,7 +919,7 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
       if (t == gridDim.x - 1) {
         *a.done = 0u;
         __threadfence();
-        *a.counter = row + 1;
+        *a.counter = crow + 1;
       }
     }
   }
@@ -908,7 +927,7 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
 
 static int launch_solve(const SolveArgs& a, cudaStream_t s) {
   int threads = std::min(512, std::max(64, ((a.nx + 31) / 32) * 32));
-  size_t sm = (3 * (size_t)a.nx + 32) * sizeof(double);
+  size_t sm = (4 * (size_t)a.nx + 32) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1018,6 +1037,7 @@ static int step_occupancy(int degree, int K, size_t smem) {
 
 static int check_cfg(long long n, int p, int nx, int degree) {
   if (n < 1 || p < 1) return set_err(PICROM_ERR_CONFIG, "need n >= 1 and p >= 1");
+  if (n > 2000000000LL) return set_err(PICROM_ERR_CONFIG, "n > 2e9 particles per instance");
   if (nx < 2) return set_err(PICROM_ERR_CONFIG, "need nx >= 2");
   if (degree < 1 || degree > 3) return set_err(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
   if (degree > 1 && nx < 2 * degree + 1) return set_err(PICROM_ERR_CONFIG, "need nx >= 2*degree+1");
@@ -1120,9 +1140,9 @@ extern "C" int picrom_pic_push(double* x, double* v, long long n, int p, long lo
 
 extern "C" int picrom_pic_solve(long long n, int p, int nx, int degree, const double* inst,
                                 const double* khat, const double* stencil, double* phi,
-                                long long step, long long* counter, double* rho_hist,
-                                double* phi_hist, double* ee_hist, double* kin_hist, void* ws,
-                                void* stream) {
+                                long long step, long long* counter, long long hist_rows,
+                                double* rho_hist, double* phi_hist, double* ee_hist,
+                                double* kin_hist, void* ws, void* stream) {
   int rc = check_cfg(n, p, nx, degree);
   if (rc) return rc;
   Plan pl = make_plan(n, p, nx, degree, true);
@@ -1139,6 +1159,7 @@ extern "C" int picrom_pic_solve(long long n, int p, int nx, int degree, const do
   if (counter) {
     sa.counter = counter;
     sa.done = reinterpret_cast<unsigned int*>(counter + 1);
+    sa.hist_mod = hist_rows;
     sa.rho_out = rho_hist; sa.phi_hist = phi_hist; sa.energy_out = ee_hist; sa.kin_out = kin_hist;
   } else {
     sa.rho_out = rho_hist ? rho_hist + (size_t)step * gp : nullptr;
@@ -1159,7 +1180,7 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
   int rc = picrom_pic_push(x, v, n, p, ld, inst, nx, degree, phi, dt, kick, kfull, step, counter,
                            ws, status, stream);
   if (rc) return rc;
-  return picrom_pic_solve(n, p, nx, degree, inst, khat, stencil, phi, step, counter, rho_hist,
+  return picrom_pic_solve(n, p, nx, degree, inst, khat, stencil, phi, step, counter, 0, rho_hist,
                           phi_hist, ee_hist, kin_hist, ws, stream);
 }
 

@@ -256,105 +256,174 @@ class FullOrderRecord:
     final_state: object = None                     # ParticleEnsemble at t_final
 
 
+class PicEngine:
+    """Persistent device state of the leapfrog loop for one (system, p, N, dt):
+    x, v (p, N), phi, workspace, status, step counter and ring histories, plus
+    one captured CUDA graph of `graph_steps` steps that every later run
+    replays (all its pointers live here, so the graph stays valid)."""
+
+    def __init__(self, system, p, n, dt, graph_steps=16):
+        self.system = system
+        self.p, self.n, self.dt = p, n, float(dt)
+        mesh = system.mesh
+        self.nx, self.degree = mesh.num_cells, mesh.degree
+        self.inst = system.inst(p)
+        self.c = system.poisson.constants
+        self.ws = torch.empty(int(_lib.query("picrom_fom_workspace_bytes", n, p, self.nx,
+                                             self.degree)), dtype=torch.uint8, device="cuda")
+        self.x = torch.empty((p, n), dtype=torch.float64, device="cuda")
+        self.v = torch.empty((p, n), dtype=torch.float64, device="cuda")
+        self.phi = torch.empty((p, self.nx), dtype=torch.float64, device="cuda")
+        self.status = dev.new_status()
+        self.counter = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self.ring = int(graph_steps)
+        self.r_rho = torch.zeros((self.ring, p, self.nx), dtype=torch.float64, device="cuda")
+        self.r_phi = torch.zeros_like(self.r_rho)
+        self.r_ee = torch.zeros((self.ring, p), dtype=torch.float64, device="cuda")
+        self.r_kin = torch.zeros_like(self.r_ee)
+        self.graph = None
+        self.launches = 0
+
+    def launch(self, first):
+        dt = self.dt
+        kick, kfull = (0.5 * dt, 0.0) if first else (dt, 0.5 * dt)
+        s = dev.stream_handle()
+        _lib.call("picrom_pic_push", self.x.data_ptr(), self.v.data_ptr(), self.n, self.p, self.n,
+                  self.inst.data_ptr(), self.nx, self.degree, self.phi.data_ptr(), dt, kick, kfull,
+                  0, self.counter.data_ptr(), self.ws.data_ptr(), self.status.data_ptr(), s)
+        _lib.call("picrom_pic_solve", self.n, self.p, self.nx, self.degree, self.inst.data_ptr(),
+                  self.c.khat.data_ptr(), self.c.stencil.data_ptr(), self.phi.data_ptr(), 0,
+                  self.counter.data_ptr(), self.ring, self.r_rho.data_ptr(), self.r_phi.data_ptr(),
+                  self.r_ee.data_ptr(), self.r_kin.data_ptr(), self.ws.data_ptr(), s)
+        self.launches += 2
+
+    def replay(self):
+        if self.graph is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(self.ring):
+                    self.launch(first=False)
+            self.launches -= 2 * self.ring
+            self.graph = g
+        self.graph.replay()
+        self.launches += 2 * self.ring
+
+
+def _engine(system, p, n, dt):
+    cache = system.__dict__.setdefault("_engines", {})
+    key = (p, n, float(dt), torch.cuda.current_device())
+    eng = cache.get(key)
+    if eng is None:
+        cache.clear()                      # one resident engine per system
+        eng = cache[key] = PicEngine(system, p, n, dt)
+    return eng
+
+
 class PicRun:
     """Device-resident leapfrog PIC loop (the production path of run_full_order).
 
-    State: x (p, N), v (p, N) -- v holds v_0 before the first step and the
-    half-step velocity v_{n-1/2} afterwards.  Histories (device): rho/phi
-    (steps+1, p, Nx), electric/kinetic energy (steps+1, p).
+    State lives in a cached PicEngine: x (p, N), v (p, N) -- v holds v_0 before
+    the first step and the half-step velocity v_{n-1/2} afterwards.  Each step
+    is picrom_pic_push + picrom_pic_solve; blocks of `ring` steps replay one
+    CUDA graph.  Histories (device): rho/phi (steps+1, p, Nx), electric and
+    kinetic energy (steps+1, p), filled from the engine's ring after each block.
     """
 
-    def __init__(self, system, xd, vd, dt, num_steps, graph_steps=16, keep_rho=True):
+    def __init__(self, system, xd, vd, dt, num_steps, keep_rho=True):
         self.system = system
-        self.x = xd
-        self.v = vd
         self.p, self.n = xd.shape
+        self.e = _engine(system, self.p, self.n, dt)
+        self.e.x.copy_(xd)
+        self.e.v.copy_(vd)
+        self.e.status.fill_(-1)
+        self.e.counter.zero_()
         self.dt = float(dt)
         self.num_steps = int(num_steps)
-        mesh = system.mesh
-        self.nx, self.degree = mesh.num_cells, mesh.degree
-        self.inst = system.inst(self.p)
-        self.c = system.poisson.constants
-        self.ws = torch.empty(int(_lib.query("picrom_fom_workspace_bytes", self.n, self.p,
-                                             self.nx, self.degree)),
-                              dtype=torch.uint8, device="cuda")
-        self.status = dev.new_status()
-        self.counter = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self.nx, self.degree = self.e.nx, self.e.degree
         rows = self.num_steps + 1
         self.rho_hist = (torch.zeros((rows, self.p, self.nx), dtype=torch.float64, device="cuda")
                          if keep_rho else None)
         self.phi_hist = torch.zeros((rows, self.p, self.nx), dtype=torch.float64, device="cuda")
         self.ee_hist = torch.zeros((rows, self.p), dtype=torch.float64, device="cuda")
         self.kin_hist = torch.zeros((rows, self.p), dtype=torch.float64, device="cuda")
-        self.phi = torch.empty((self.p, self.nx), dtype=torch.float64, device="cuda")
         self.tau = 0
-        self.graph_steps = int(graph_steps)
-        self._graph = None
-        self.launches = 0
 
-    # ---------------------------------------------------------------- steps
+    @property
+    def x(self):
+        return self.e.x
+
+    @property
+    def v(self):
+        return self.e.v
+
+    @property
+    def phi(self):
+        return self.e.phi
+
+    @property
+    def status(self):
+        return self.e.status
+
+    @property
+    def launches(self):
+        return self.e.launches
+
     def init_field(self):
         """Initial deposit + solve (fullorder.py:183-186): phi_0, rho_0, energy_0."""
+        e = self.e
         s = dev.stream_handle()
         rho0 = self.rho_hist[0] if self.rho_hist is not None else torch.empty(
             (self.p, self.nx), dtype=torch.float64, device="cuda")
-        _lib.call("picrom_deposit", self.x.data_ptr(), self.n, self.p, self.n, self.inst.data_ptr(),
-                  self.nx, self.degree, rho0.data_ptr(), self.ws.data_ptr(),
-                  self.status.data_ptr(), s)
+        _lib.call("picrom_deposit", e.x.data_ptr(), self.n, self.p, self.n, e.inst.data_ptr(),
+                  self.nx, self.degree, rho0.data_ptr(), e.ws.data_ptr(), e.status.data_ptr(), s)
         _lib.call("picrom_poisson", rho0.data_ptr(), self.p, self.nx, self.degree,
-                  self.inst.data_ptr(), self.c.khat.data_ptr(), self.c.stencil.data_ptr(),
-                  self.phi.data_ptr(), self.ee_hist[0].data_ptr(), s)
-        self.phi_hist[0].copy_(self.phi)
-        self.launches += 3
+                  e.inst.data_ptr(), e.c.khat.data_ptr(), e.c.stencil.data_ptr(),
+                  e.phi.data_ptr(), self.ee_hist[0].data_ptr(), s)
+        self.phi_hist[0].copy_(e.phi)
+        e.launches += 3
 
-    def _launch_step(self, first):
-        dt = self.dt
-        kick, kfull = (0.5 * dt, 0.0) if first else (dt, 0.5 * dt)
-        gp = self.p * self.nx
-        rho_base = self.rho_hist.data_ptr() + 8 * gp if self.rho_hist is not None else None
-        _lib.call("picrom_pic_step", self.x.data_ptr(), self.v.data_ptr(), self.n, self.p, self.n,
-                  self.inst.data_ptr(), self.nx, self.degree, self.c.khat.data_ptr(),
-                  self.c.stencil.data_ptr(), self.phi.data_ptr(), dt, kick, kfull, 0,
-                  self.counter.data_ptr(), rho_base, self.phi_hist.data_ptr() + 8 * gp,
-                  self.ee_hist.data_ptr() + 8 * self.p, self.kin_hist.data_ptr(),
-                  self.ws.data_ptr(), self.status.data_ptr(), dev.stream_handle())
-        self.launches += 2
+    def _drain(self, c0, count):
+        """Copy ring rows of counters [c0, c0+count) into the full histories."""
+        e = self.e
+        idx = torch.arange(c0, c0 + count, device="cuda") % e.ring
+        self.kin_hist[c0:c0 + count] = e.r_kin[idx]
+        self.ee_hist[c0 + 1:c0 + count + 1] = e.r_ee[idx]
+        self.phi_hist[c0 + 1:c0 + count + 1] = e.r_phi[idx]
+        if self.rho_hist is not None:
+            self.rho_hist[c0 + 1:c0 + count + 1] = e.r_rho[idx]
 
     def advance(self, k, use_graph=True):
-        """Advance k steps (counter-driven, graph-replayed in blocks)."""
-        done = 0
-        if self.tau == 0 and k > 0:
-            self._launch_step(first=True)
+        """Advance k steps; full ring-sized blocks replay the cached graph."""
+        e = self.e
+        while k > 0:
+            if self.tau == 0:
+                e.launch(first=True)
+                self._drain(0, 1)
+                self.tau, k = 1, k - 1
+                continue
+            if use_graph and k >= e.ring:
+                e.replay()
+                self._drain(self.tau, e.ring)
+                self.tau += e.ring
+                k -= e.ring
+                continue
+            e.launch(first=False)
+            self._drain(self.tau, 1)
             self.tau += 1
-            done += 1
-        g = self.graph_steps
-        while use_graph and g > 1 and k - done >= g:
-            if self._graph is None:
-                self._graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(self._graph):
-                    for _ in range(g):
-                        self._launch_step(first=False)
-                self.launches -= 2 * g       # capture launches nothing
-            self._graph.replay()
-            self.launches += 2 * g
-            self.tau += g
-            done += g
-        while done < k:
-            self._launch_step(first=False)
-            self.tau += 1
-            done += 1
+            k -= 1
 
     def full_velocity(self):
         """v_tau = v_{tau-1/2} + 0.5 dt E(x_tau) (device), or v_0 before any step."""
+        e = self.e
         if self.tau == 0:
-            return self.v.clone()
-        e = torch.empty_like(self.x)
-        zeros = torch.zeros_like(self.x)
-        vfull = torch.empty_like(self.x)
-        _lib.call("picrom_verlet_kick", self.x.data_ptr(), self.v.data_ptr(), zeros.data_ptr(),
-                  self.n, self.p, self.n, self.inst.data_ptr(), self.nx, self.degree,
-                  self.phi.data_ptr(), self.dt, e.data_ptr(), vfull.data_ptr(), dev.stream_handle())
-        self.launches += 1
+            return e.v.clone()
+        ef = torch.empty_like(e.x)
+        zeros = torch.zeros_like(e.x)
+        vfull = torch.empty_like(e.x)
+        _lib.call("picrom_verlet_kick", e.x.data_ptr(), e.v.data_ptr(), zeros.data_ptr(),
+                  self.n, self.p, self.n, e.inst.data_ptr(), self.nx, self.degree,
+                  e.phi.data_ptr(), self.dt, ef.data_ptr(), vfull.data_ptr(), dev.stream_handle())
+        e.launches += 1
         return vfull
 
     def finish_kinetic(self):
@@ -362,11 +431,11 @@ class PicRun:
         vfull = self.full_velocity()
         _lib.call("picrom_half_sumsq", vfull.data_ptr(), self.n, self.p, self.n,
                   self.kin_hist[self.tau].data_ptr(), None, dev.stream_handle())
-        self.launches += 1
+        self.e.launches += 1
         return vfull
 
     def check(self):
-        bad = dev.decode_status(self.status, self.p)
+        bad = dev.decode_status(self.e.status, self.p)
         if bad is not None:
             step, row, col = bad
             t = step * self.dt
@@ -387,10 +456,6 @@ def run_full_order(system, initial: ParticleEnsemble, dt, t_final,
     snap_stride = record.resolved_snapshot_stride(num_steps)
     xd, meta = dev.to_device(initial.x)
     vd, _ = dev.to_device(initial.v)
-    if xd.data_ptr() == (initial.x.data_ptr() if isinstance(initial.x, torch.Tensor) else -1):
-        xd = xd.clone()
-    if vd.data_ptr() == (initial.v.data_ptr() if isinstance(initial.v, torch.Tensor) else -1):
-        vd = vd.clone()
     p = xd.shape[0]
     run = PicRun(system, xd, vd, dt, num_steps)
 

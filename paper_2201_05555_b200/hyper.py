@@ -343,10 +343,23 @@ def deim_greedy(psi, keep=None):
     return indices
 
 
-def _window_svd(window, dim):
-    """Leading left singular vectors of the window W (N x c): Gram eigenpairs
-    give V, Sigma; Psi0 = W V Sigma^-1; one Rayleigh-Ritz pass re-orthonormalises
-    Psi0 and rotates it to the singular directions of Psi0^T W."""
+def _orthonormalize(y):
+    """CholeskyQR2 of a tall device block (N x k, k <= 64): Q with Q^T Q = I to O(eps)."""
+    for _ in range(2):
+        g = _tall.gram([(y, False)])
+        r = np.linalg.cholesky(g).T
+        y = _blocks_times([y], np.linalg.inv(r))
+    return y
+
+
+def _window_svd(window, dim, oversample=8, iterations=2):
+    """Leading left singular vectors of the window W (N x c) without forming
+    more than an N x (d+q) block:
+      1. W^T W (sliding Gram) -> eigenpairs -> initial basis Y = W V_{d+q};
+      2. `iterations` subspace-iteration steps Y <- W (W^T Q), Q = CholQR2(Y),
+         which removes the squared-condition error of step 1;
+      3. Rayleigh-Ritz: SVD of the small Q^T W, Psi = Q U_B[:, :d].
+    The rank test is the reference's (hyper.py:263) on the Gram singular values."""
     blocks = window.columns()
     c = sum(b.shape[1] for b in blocks)
     gram = window.gram()
@@ -359,15 +372,14 @@ def _window_svd(window, dim):
     d_eff = min(int(dim), rank)
     if d_eff < dim:
         warnings.warn(f"DEIM samples have numerical rank {rank} < {dim}; basis reduced to {d_eff}")
-    psi0 = _blocks_times(blocks, vec[:, :d_eff] / sing[:d_eff])
-    # Rayleigh-Ritz: orthonormalise, then rotate to the SVD of Q^T W
-    g0 = _tall.gram([(psi0, False)])
-    r = np.linalg.cholesky(g0).T
-    q = _tall.combine([(psi0, np.linalg.inv(r), False)]) if d_eff <= 32 else \
-        _blocks_times([psi0], np.linalg.inv(r))
-    qtw = np.concatenate([_cross(q, [b]) for b in blocks], axis=1)
+    k = min(c, rank, d_eff + oversample, 64)
+    q = _orthonormalize(_blocks_times(blocks, vec[:, :k] / sing[:k]))
+    for _ in range(iterations):
+        wtq = np.concatenate([_cross(b, [q]) for b in blocks], axis=0)      # (c x k)
+        q = _orthonormalize(_blocks_times(blocks, wtq))
+    qtw = np.concatenate([_cross(q, [b]) for b in blocks], axis=1)          # (k x c)
     ub, _, _ = svd(qtw, full_matrices=False)
-    psi = _blocks_times([q], ub)
+    psi = _blocks_times([q], ub[:, :d_eff])
     return psi, d_eff
 
 
