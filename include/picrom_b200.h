@@ -60,7 +60,9 @@ int picrom_device_info(int* num_sms, int* cc_major, int* cc_minor);
 
 /* ---------------------------------------------------------------- FOM --- */
 
-/* Bytes of scratch the deposit / PIC-step calls need for (n, p, nx, degree). */
+/* Bytes of scratch the deposit / PIC-step calls need for (n, p, nx, degree).
+ * The workspace must be zero-filled once before its first picrom_pic_step
+ * (it holds per-instance tickets, which every call leaves zeroed). */
 size_t picrom_fom_workspace_bytes(long long n, int p, int nx, int degree);
 
 /* fem._locate (fem.py:108-116): i0 = floor(x/h) mod Nx (int64, bit-exact),
@@ -117,20 +119,23 @@ int picrom_gather(const double* x, long long n, int p, long long ld,
  *   kin += (v + kfull*E_n)^2       (kinetic energy of v_n, per instance)
  *   v  <- v + kick*E_n ;  x <- x + dt*v          (in place)
  *   rho_{n+1} += deposit(x)        (private smem histograms, deterministic)
- * then the per-instance Poisson solve overwrites phi with phi_{n+1}.
+ * then the per-instance Poisson solve overwrites phi with phi_{n+1} -- done
+ * inside the same kernel by the last CTA to finish each instance (one launch
+ * per step).
  * First step: v holds v_0, kick = 0.5*dt, kfull = 0; later steps: v holds
  * v_{n-1/2}, kick = dt, kfull = 0.5*dt.  History pointers may be NULL:
  * rho_hist/phi_hist (rows of p*nx) get rho/phi at step+1, ee_hist (rows of p)
  * the electric energy at step+1, kin_hist (rows of p) the kinetic energy
  * 0.5*sum v_n^2 at `step`.  Row index = `step`, or, when `counter` is non-NULL
  * (a device {long long step; unsigned done;} pair, 16 bytes), the device
- * value *counter, which the call advances by one -- so a CUDA graph of k
- * steps can be replayed with unchanged parameters. */
+ * value *counter (modulo hist_rows when hist_rows > 0: a ring), which the
+ * call advances by one -- so a CUDA graph of k steps can be replayed with
+ * unchanged parameters. */
 int picrom_pic_step(double* x, double* v, long long n, int p, long long ld,
                     const double* inst, int nx, int degree,
                     const double* khat, const double* stencil, double* phi,
                     double dt, double kick, double kfull, long long step,
-                    long long* counter,
+                    long long* counter, long long hist_rows,
                     double* rho_hist, double* phi_hist, double* ee_hist, double* kin_hist,
                     void* workspace, unsigned long long* status, void* stream);
 

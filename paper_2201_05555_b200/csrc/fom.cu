@@ -67,6 +67,18 @@ static int num_sms() {
   return sms;
 }
 
+// Allow a kernel the largest dynamic shared memory the SM offers next to its
+// static shared memory (227 KB per block on sm_100 in total).
+template <typename F>
+static void allow_max_dynamic_smem(F kfn) {
+  cudaFuncAttributes at{};
+  cudaFuncGetAttributes(&at, kfn);
+  const int total = 227 * 1024;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           total - (int)at.sharedSizeBytes) != cudaSuccess)
+    (void)cudaGetLastError();   // do not leave a stale error for the next launch check
+}
+
 // ------------------------------------------------------------ work plan
 //
 // The deposit / step kernels run a fixed grid of G CTAs over the flattened
@@ -148,7 +160,7 @@ static Plan make_plan(long long n, int p, int nx, int degree, bool with_coef) {
 extern "C" size_t picrom_fom_workspace_bytes(long long n, int p, int nx, int degree) {
   Plan pl = make_plan(n, p, nx, degree, true);
   size_t rows = (size_t)pl.G + (size_t)p;
-  return rows * (size_t)(nx + 1) * sizeof(double) + 256;
+  return rows * (size_t)(nx + 1) * sizeof(double) + (size_t)(p + 1) * sizeof(unsigned int) + 256;
 }
 
 // b*T and flat*G stay far below 2^63 (T < 2^40, G < 2^16)
@@ -189,10 +201,173 @@ struct StepArgs {
   const double* y;    // DEPOSIT: optional per-particle weights (rmatvec)
   int wkind;          // DEPOSIT: 0 value weights, 1 gradient weights
   const long long* counter;  // optional device step counter (graph replay)
+  // fused solve (LEAPFROG): the last CTA finishing an instance solves it
+  int fuse_solve;
+  unsigned int* inst_done;   // p tickets (zeroed; left zeroed)
 };
 
+// ----------------------------------------------------- per-instance solve
+//
+// One CTA per instance.  rho = qw * (sum of segment rows) + bg*h   (or rho_in)
+// phi = h * khat (*) (rho - mean) ;  phi -= mean ;  energy = 0.5/m_p phi^T L phi
+
+struct SolveArgs {
+  const double* seg_hist;   // if non-null: assemble rho from segments
+  const double* seg_kin;
+  const double* rho_in;     // else: rho given
+  const double* inst;
+  const double* khat;
+  const double* stencil;
+  long long n;
+  int p, nx, degree, G;
+  double* rho_out;          // may be null
+  double* phi_out;          // may be null (deposit-only)
+  double* energy_out;       // may be null
+  double* kin_out;          // may be null
+  bool solve;
+  bool raw;                 // rho = plain segment sums (rmatvec)
+  bool energy_only;         // rho_in holds phi: only the field energy
+  long long* counter;       // optional device step counter: history row = *counter,
+                            // incremented by the last CTA to finish
+  unsigned int* done;       // ticket for the counter increment
+  size_t hist_stride_rho;   // elements per history row (rho/phi)
+  size_t hist_stride_e;     // elements per history row (energies)
+  double* phi_hist;         // optional extra copy of phi (history)
+  int seg_dense;            // > 0: dense segments seg[(b*p + j)*nx + nd], b < seg_dense
+  long long hist_mod;       // > 0: history row = counter % hist_mod (ring)
+  const int* cols;          // optional instance id per column
+};
+
+// sum of cnt values v[0], v[stride], ... with 8 independent loads in flight,
+// combined in a fixed order (deterministic)
+__device__ __forceinline__ double ordered_sum(const double* v, size_t stride, int cnt) {
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int b = 0;
+  for (; b + 8 <= cnt; b += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += v[(size_t)(b + u) * stride];
+  }
+  for (int u = 0; b < cnt; ++b, ++u) acc[u] += v[(size_t)b * stride];
+  return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
+// One instance's assembly + solve by a whole CTA; `sm` holds 4 nx + 32
+// doubles; `ntickets` = how many instance solves make up this step (the last
+// one to finish advances the step counter).
+__device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int ntickets) {
+  const int nx = a.nx;
+  double* rho = sm;            // nx
+  double* kh = rho + nx;       // 2 nx (khat repeated)
+  double* phi = kh + 2 * nx;   // nx
+  double* red = phi + nx;      // 32
+  const int tid = threadIdx.x;
+  const double* ip = a.inst + (size_t)(a.cols ? a.cols[j] : j) * PICROM_INST_STRIDE;
+  const double h = ip[I_H];
+  const long long crow = a.counter ? *a.counter : 0;
+  const long long row = a.hist_mod > 0 ? crow % a.hist_mod : crow;
+  double* rho_out = a.rho_out ? a.rho_out + row * a.hist_stride_rho : nullptr;
+  double* phi_hist = a.phi_hist ? a.phi_hist + row * a.hist_stride_rho : nullptr;
+  double* energy_out = a.energy_out ? a.energy_out + row * a.hist_stride_e : nullptr;
+  double* kin_out = a.kin_out ? a.kin_out + row * a.hist_stride_e : nullptr;
+
+  if (a.seg_dense > 0) {
+    const double qw = ip[I_QW], bgh = ip[I_BGH];
+    for (int nd = tid; nd < nx; nd += blockDim.x) {
+      const double s = ordered_sum(a.seg_hist + (size_t)j * nx + nd, (size_t)a.p * nx, a.seg_dense);
+      rho[nd] = a.raw ? s : fma(qw, s, bgh);
+    }
+  } else if (a.seg_hist) {
+    const long long T = a.n * (long long)a.p;
+    const int b_lo = cta_of((long long)j * a.n, T, a.G);
+    const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, a.G);
+    const double qw = ip[I_QW], bgh = ip[I_BGH];
+    for (int nd = tid; nd < nx; nd += blockDim.x) {
+      const double s = ordered_sum(a.seg_hist + (size_t)(b_lo + j) * nx + nd, nx, b_hi - b_lo + 1);
+      rho[nd] = a.raw ? s : fma(qw, s, bgh);
+    }
+    if (kin_out && tid == 0) kin_out[j] = 0.5 * ordered_sum(a.seg_kin + b_lo + j, 1, b_hi - b_lo + 1);
+  } else if (a.energy_only) {
+    for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] = a.rho_in[(size_t)j * nx + nd];
+  } else {
+    for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] = a.rho_in[(size_t)j * nx + nd];
+  }
+  if (a.solve)
+    for (int r = tid; r < 2 * nx; r += blockDim.x) kh[r] = a.khat[r < nx ? r : r - nx];
+  __syncthreads();
+  if (rho_out)
+    for (int nd = tid; nd < nx; nd += blockDim.x) rho_out[(size_t)j * nx + nd] = rho[nd];
+  if (!a.solve && !a.energy_only) return;
+
+  double part = 0.0;
+  if (!a.energy_only) {
+  for (int nd = tid; nd < nx; nd += blockDim.x) part += rho[nd];
+  const double mean_rho = block_sum(part, red) / (double)nx;
+  for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] -= mean_rho;
+  __syncthreads();
+  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m; kh holds khat
+  // twice (kh[r] = khat[r mod nx], r < 2 nx) so the inner loop has no modulo,
+  // and 4 independent partial sums keep the FMA pipe busy (fixed order)
+  part = 0.0;
+  for (int nd = tid; nd < nx; nd += blockDim.x) {
+    const double* kr = kh + nd + nx;     // kr[-m] = khat[(nd - m) mod nx]
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int m = 0;
+    for (; m + 4 <= nx; m += 4) {
+      s0 = fma(kr[-m], rho[m], s0);
+      s1 = fma(kr[-m - 1], rho[m + 1], s1);
+      s2 = fma(kr[-m - 2], rho[m + 2], s2);
+      s3 = fma(kr[-m - 3], rho[m + 3], s3);
+    }
+    for (; m < nx; ++m) s0 = fma(kr[-m], rho[m], s0);
+    phi[nd] = h * ((s0 + s1) + (s2 + s3));
+    part += phi[nd];
+  }
+  const double mean_phi = block_sum(part, red) / (double)nx;
+  for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] -= mean_phi;
+  __syncthreads();
+  if (a.phi_out)
+    for (int nd = tid; nd < nx; nd += blockDim.x) a.phi_out[(size_t)j * nx + nd] = phi[nd];
+  }  // !energy_only
+  if (phi_hist)
+    for (int nd = tid; nd < nx; nd += blockDim.x) phi_hist[(size_t)j * nx + nd] = phi[nd];
+  if (energy_out) {
+    // L phi with L = stencil / h (circulant, half bandwidth d)
+    const double inv_h = 1.0 / h;
+    part = 0.0;
+    for (int nd = tid; nd < nx; nd += blockDim.x) {
+      double lp = a.stencil[0] * phi[nd];
+      for (int k = 1; k <= a.degree; ++k) {
+        int up = nd + k; if (up >= nx) up -= nx;
+        int dn = nd - k; if (dn < 0) dn += nx;
+        lp = fma(a.stencil[k], phi[up] + phi[dn], lp);
+      }
+      part = fma(phi[nd], lp * inv_h, part);
+    }
+    double e = block_sum(part, red);
+    if (tid == 0) energy_out[j] = ip[I_HALFINVMP] * e;
+  }
+  if (a.counter) {
+    // last CTA to finish advances the step counter (all CTAs read it above)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      unsigned int t = atomicAdd(a.done, 1u);
+      if (t == ntickets - 1) {
+        *a.done = 0u;
+        __threadfence();
+        *a.counter = crow + 1;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
+  extern __shared__ double sm[];
+  solve_body(a, blockIdx.x, sm, gridDim.x);
+}
+
 #ifndef PICROM_STEP_U
-#define PICROM_STEP_U 2
+#define PICROM_STEP_U 4
 #endif
 
 // exact locate for the rare inputs of locate_fast (kept out of line so the
@@ -215,7 +390,7 @@ __device__ __noinline__ CellFrac locate_rare(double x, double h, double inv_h, i
 // block: coalesced), with the next iteration's loads issued first.
 template <int D, int K, int MODE, int NT>
 __global__ void __launch_bounds__(NT)
-step_kernel(StepArgs a) {
+step_kernel(StepArgs a, SolveArgs sa) {
   extern __shared__ double smem[];
   constexpr int H = NT / K;
   constexpr int NW = D + 1;
@@ -423,6 +598,25 @@ step_kernel(StepArgs a) {
     if constexpr (MODE == MODE_LEAPFROG) {
       double ks = block_sum(kin, red);
       if (tid == 0) a.seg_kin[seg] = ks;
+      if (a.fuse_solve) {
+        // the last CTA to finish instance j's particles solves instance j
+        // (threadFenceReduction pattern); the histograms are free scratch now
+        __shared__ int s_last;
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          const int b_lo = cta_of((long long)j * a.n, T, G);
+          const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, G);
+          const unsigned int prev = atomicAdd(&a.inst_done[j], 1u);
+          s_last = prev == (unsigned int)(b_hi - b_lo);
+          if (s_last) a.inst_done[j] = 0u;
+        }
+        __syncthreads();
+        if (s_last) {
+          __threadfence();
+          solve_body(sa, j, hist, (unsigned int)a.p);
+        }
+      }
     }
     __syncthreads();
     pos = (long long)(j + 1) * a.n;
@@ -744,7 +938,7 @@ static int launch_tma_t(const StepArgs& a, const TmaCfg& c, int G, cudaStream_t 
   auto kfn = step_tma_kernel<D, K, NCW>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    allow_max_dynamic_smem(kfn);
     attr = true;
   }
   kfn<<<G, NCW * 32 + 32, c.smem, s>>>(a, c.stages);
@@ -768,160 +962,6 @@ static int launch_tma(const StepArgs& a, int degree, const TmaCfg& c, int G, cud
     case 1: return launch_tma_d<1>(a, c, G, s);
     case 2: return launch_tma_d<2>(a, c, G, s);
     default: return launch_tma_d<3>(a, c, G, s);
-  }
-}
-
-// ----------------------------------------------------- per-instance solve
-//
-// One CTA per instance.  rho = qw * (sum of segment rows) + bg*h   (or rho_in)
-// phi = h * khat (*) (rho - mean) ;  phi -= mean ;  energy = 0.5/m_p phi^T L phi
-
-struct SolveArgs {
-  const double* seg_hist;   // if non-null: assemble rho from segments
-  const double* seg_kin;
-  const double* rho_in;     // else: rho given
-  const double* inst;
-  const double* khat;
-  const double* stencil;
-  long long n;
-  int p, nx, degree, G;
-  double* rho_out;          // may be null
-  double* phi_out;          // may be null (deposit-only)
-  double* energy_out;       // may be null
-  double* kin_out;          // may be null
-  bool solve;
-  bool raw;                 // rho = plain segment sums (rmatvec)
-  bool energy_only;         // rho_in holds phi: only the field energy
-  long long* counter;       // optional device step counter: history row = *counter,
-                            // incremented by the last CTA to finish
-  unsigned int* done;       // ticket for the counter increment
-  size_t hist_stride_rho;   // elements per history row (rho/phi)
-  size_t hist_stride_e;     // elements per history row (energies)
-  double* phi_hist;         // optional extra copy of phi (history)
-  int seg_dense;            // > 0: dense segments seg[(b*p + j)*nx + nd], b < seg_dense
-  long long hist_mod;       // > 0: history row = counter % hist_mod (ring)
-  const int* cols;          // optional instance id per column
-};
-
-// sum of cnt values v[0], v[stride], ... with 8 independent loads in flight,
-// combined in a fixed order (deterministic)
-__device__ __forceinline__ double ordered_sum(const double* v, size_t stride, int cnt) {
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int b = 0;
-  for (; b + 8 <= cnt; b += 8) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] += v[(size_t)(b + u) * stride];
-  }
-  for (int u = 0; b < cnt; ++b, ++u) acc[u] += v[(size_t)b * stride];
-  return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-}
-
-__global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
-  extern __shared__ double sm[];
-  const int nx = a.nx;
-  double* rho = sm;            // nx
-  double* kh = rho + nx;       // 2 nx (khat repeated)
-  double* phi = kh + 2 * nx;   // nx
-  double* red = phi + nx;      // 32
-  const int j = blockIdx.x;
-  const int tid = threadIdx.x;
-  const double* ip = a.inst + (size_t)(a.cols ? a.cols[j] : j) * PICROM_INST_STRIDE;
-  const double h = ip[I_H];
-  const long long crow = a.counter ? *a.counter : 0;
-  const long long row = a.hist_mod > 0 ? crow % a.hist_mod : crow;
-  double* rho_out = a.rho_out ? a.rho_out + row * a.hist_stride_rho : nullptr;
-  double* phi_hist = a.phi_hist ? a.phi_hist + row * a.hist_stride_rho : nullptr;
-  double* energy_out = a.energy_out ? a.energy_out + row * a.hist_stride_e : nullptr;
-  double* kin_out = a.kin_out ? a.kin_out + row * a.hist_stride_e : nullptr;
-
-  if (a.seg_dense > 0) {
-    const double qw = ip[I_QW], bgh = ip[I_BGH];
-    for (int nd = tid; nd < nx; nd += blockDim.x) {
-      const double s = ordered_sum(a.seg_hist + (size_t)j * nx + nd, (size_t)a.p * nx, a.seg_dense);
-      rho[nd] = a.raw ? s : fma(qw, s, bgh);
-    }
-  } else if (a.seg_hist) {
-    const long long T = a.n * (long long)a.p;
-    const int b_lo = cta_of((long long)j * a.n, T, a.G);
-    const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, a.G);
-    const double qw = ip[I_QW], bgh = ip[I_BGH];
-    for (int nd = tid; nd < nx; nd += blockDim.x) {
-      const double s = ordered_sum(a.seg_hist + (size_t)(b_lo + j) * nx + nd, nx, b_hi - b_lo + 1);
-      rho[nd] = a.raw ? s : fma(qw, s, bgh);
-    }
-    if (kin_out && tid == 0) kin_out[j] = 0.5 * ordered_sum(a.seg_kin + b_lo + j, 1, b_hi - b_lo + 1);
-  } else if (a.energy_only) {
-    for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] = a.rho_in[(size_t)j * nx + nd];
-  } else {
-    for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] = a.rho_in[(size_t)j * nx + nd];
-  }
-  if (a.solve)
-    for (int r = tid; r < 2 * nx; r += blockDim.x) kh[r] = a.khat[r < nx ? r : r - nx];
-  __syncthreads();
-  if (rho_out)
-    for (int nd = tid; nd < nx; nd += blockDim.x) rho_out[(size_t)j * nx + nd] = rho[nd];
-  if (!a.solve && !a.energy_only) return;
-
-  double part = 0.0;
-  if (!a.energy_only) {
-  for (int nd = tid; nd < nx; nd += blockDim.x) part += rho[nd];
-  const double mean_rho = block_sum(part, red) / (double)nx;
-  for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] -= mean_rho;
-  __syncthreads();
-  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m; kh holds khat
-  // twice (kh[r] = khat[r mod nx], r < 2 nx) so the inner loop has no modulo,
-  // and 4 independent partial sums keep the FMA pipe busy (fixed order)
-  part = 0.0;
-  for (int nd = tid; nd < nx; nd += blockDim.x) {
-    const double* kr = kh + nd + nx;     // kr[-m] = khat[(nd - m) mod nx]
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int m = 0;
-    for (; m + 4 <= nx; m += 4) {
-      s0 = fma(kr[-m], rho[m], s0);
-      s1 = fma(kr[-m - 1], rho[m + 1], s1);
-      s2 = fma(kr[-m - 2], rho[m + 2], s2);
-      s3 = fma(kr[-m - 3], rho[m + 3], s3);
-    }
-    for (; m < nx; ++m) s0 = fma(kr[-m], rho[m], s0);
-    phi[nd] = h * ((s0 + s1) + (s2 + s3));
-    part += phi[nd];
-  }
-  const double mean_phi = block_sum(part, red) / (double)nx;
-  for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] -= mean_phi;
-  __syncthreads();
-  if (a.phi_out)
-    for (int nd = tid; nd < nx; nd += blockDim.x) a.phi_out[(size_t)j * nx + nd] = phi[nd];
-  }  // !energy_only
-  if (phi_hist)
-    for (int nd = tid; nd < nx; nd += blockDim.x) phi_hist[(size_t)j * nx + nd] = phi[nd];
-  if (energy_out) {
-    // L phi with L = stencil / h (circulant, half bandwidth d)
-    const double inv_h = 1.0 / h;
-    part = 0.0;
-    for (int nd = tid; nd < nx; nd += blockDim.x) {
-      double lp = a.stencil[0] * phi[nd];
-      for (int k = 1; k <= a.degree; ++k) {
-        int up = nd + k; if (up >= nx) up -= nx;
-        int dn = nd - k; if (dn < 0) dn += nx;
-        lp = fma(a.stencil[k], phi[up] + phi[dn], lp);
-      }
-      part = fma(phi[nd], lp * inv_h, part);
-    }
-    double e = block_sum(part, red);
-    if (tid == 0) energy_out[j] = ip[I_HALFINVMP] * e;
-  }
-  if (a.counter) {
-    // last CTA to finish advances the step counter (all CTAs read it above)
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      unsigned int t = atomicAdd(a.done, 1u);
-      if (t == gridDim.x - 1) {
-        *a.done = 0u;
-        __threadfence();
-        *a.counter = crow + 1;
-      }
-    }
   }
 }
 
@@ -952,45 +992,48 @@ int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, cons
 // --------------------------------------------------------- launch helpers
 
 template <int D, int K, int MODE>
-static int launch_step_t(const StepArgs& a, const Plan& pl, cudaStream_t s) {
+static int launch_step_t(const StepArgs& a, const SolveArgs& sa, const Plan& pl, cudaStream_t s) {
   if (step_nt() == 128) {
     auto kfn = step_kernel<D, K, MODE, 128>;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      allow_max_dynamic_smem(kfn);
       attr = true;
     }
-    kfn<<<pl.G, 128, pl.smem, s>>>(a);
+    kfn<<<pl.G, 128, pl.smem, s>>>(a, sa);
   } else {
     auto kfn = step_kernel<D, K, MODE, 256>;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      allow_max_dynamic_smem(kfn);
       attr = true;
     }
-    kfn<<<pl.G, 256, pl.smem, s>>>(a);
+    kfn<<<pl.G, 256, pl.smem, s>>>(a, sa);
   }
   return check_launch("step_kernel");
 }
 
 template <int D, int MODE>
-static int launch_step_k(const StepArgs& a, const Plan& pl, cudaStream_t s) {
+static int launch_step_k(const StepArgs& a, const SolveArgs& sa, const Plan& pl, cudaStream_t s) {
   switch (pl.K) {
-    case 1: return launch_step_t<D, 1, MODE>(a, pl, s);
-    case 2: return launch_step_t<D, 2, MODE>(a, pl, s);
-    case 4: return launch_step_t<D, 4, MODE>(a, pl, s);
-    case 8: return launch_step_t<D, 8, MODE>(a, pl, s);
-    case 16: return launch_step_t<D, 16, MODE>(a, pl, s);
-    default: return launch_step_t<D, 32, MODE>(a, pl, s);
+    case 1: return launch_step_t<D, 1, MODE>(a, sa, pl, s);
+    case 2: return launch_step_t<D, 2, MODE>(a, sa, pl, s);
+    case 4: return launch_step_t<D, 4, MODE>(a, sa, pl, s);
+    case 8: return launch_step_t<D, 8, MODE>(a, sa, pl, s);
+    case 16: return launch_step_t<D, 16, MODE>(a, sa, pl, s);
+    default: return launch_step_t<D, 32, MODE>(a, sa, pl, s);
   }
 }
 
 template <int MODE>
-static int launch_step(const StepArgs& a, int degree, const Plan& pl, cudaStream_t s) {
+static int launch_step(const StepArgs& a, int degree, const Plan& pl, cudaStream_t s,
+                       const SolveArgs* sa = nullptr) {
+  SolveArgs none{};
+  const SolveArgs& sref = sa ? *sa : none;
   switch (degree) {
-    case 1: return launch_step_k<1, MODE>(a, pl, s);
-    case 2: return launch_step_k<2, MODE>(a, pl, s);
-    case 3: return launch_step_k<3, MODE>(a, pl, s);
+    case 1: return launch_step_k<1, MODE>(a, sref, pl, s);
+    case 2: return launch_step_k<2, MODE>(a, sref, pl, s);
+    case 3: return launch_step_k<3, MODE>(a, sref, pl, s);
   }
   return set_err(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
 }
@@ -1000,11 +1043,11 @@ static int occ_of(size_t smem) {
   int occ = 0;
   if (step_nt() == 128) {
     auto kfn = step_kernel<D, K, MODE_LEAPFROG, 128>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    allow_max_dynamic_smem(kfn);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, smem) != cudaSuccess) occ = 1;
   } else {
     auto kfn = step_kernel<D, K, MODE_LEAPFROG, 256>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    allow_max_dynamic_smem(kfn);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, smem) != cudaSuccess) occ = 1;
   }
   return occ;
@@ -1045,10 +1088,12 @@ static int check_cfg(long long n, int p, int nx, int degree) {
   return PICROM_OK;
 }
 
-static void ws_split(void* ws, const Plan& pl, int p, int nx, double** hist, double** kin) {
+static void ws_split(void* ws, const Plan& pl, int p, int nx, double** hist, double** kin,
+                     unsigned int** tickets = nullptr) {
   double* base = reinterpret_cast<double*>(ws);
   *hist = base;
   *kin = base + (size_t)(pl.G + p) * nx;
+  if (tickets) *tickets = reinterpret_cast<unsigned int*>(*kin + (pl.G + p));
 }
 
 // ---------------------------------------------------------------- C-ABI
@@ -1174,14 +1219,44 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
                                const double* inst, int nx, int degree, const double* khat,
                                const double* stencil, double* phi, double dt, double kick,
                                double kfull, long long step, long long* counter,
-                               double* rho_hist, double* phi_hist, double* ee_hist,
-                               double* kin_hist, void* ws, unsigned long long* status,
-                               void* stream) {
-  int rc = picrom_pic_push(x, v, n, p, ld, inst, nx, degree, phi, dt, kick, kfull, step, counter,
-                           ws, status, stream);
+                               long long hist_rows, double* rho_hist, double* phi_hist,
+                               double* ee_hist, double* kin_hist, void* ws,
+                               unsigned long long* status, void* stream) {
+  int rc = check_cfg(n, p, nx, degree);
   if (rc) return rc;
-  return picrom_pic_solve(n, p, nx, degree, inst, khat, stencil, phi, step, counter, 0, rho_hist,
-                          phi_hist, ee_hist, kin_hist, ws, stream);
+  Plan pl = make_plan(n, p, nx, degree, true);
+  if (pl.tma) {   // the TMA variant has no fused solve: push + solve
+    rc = picrom_pic_push(x, v, n, p, ld, inst, nx, degree, phi, dt, kick, kfull, step, counter,
+                         ws, status, stream);
+    if (rc) return rc;
+    return picrom_pic_solve(n, p, nx, degree, inst, khat, stencil, phi, step, counter, hist_rows,
+                            rho_hist, phi_hist, ee_hist, kin_hist, ws, stream);
+  }
+  StepArgs a{};
+  a.x = x; a.v = v; a.phi = phi; a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx;
+  a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
+  a.counter = counter;
+  a.fuse_solve = 1;
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
+  SolveArgs sa{};
+  sa.seg_hist = a.seg_hist; sa.seg_kin = a.seg_kin; sa.inst = inst; sa.khat = khat;
+  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G;
+  sa.solve = true; sa.phi_out = phi;
+  const size_t gp = (size_t)p * nx;
+  sa.hist_stride_rho = gp;
+  sa.hist_stride_e = (size_t)p;
+  if (counter) {
+    sa.counter = counter;
+    sa.done = reinterpret_cast<unsigned int*>(counter + 1);
+    sa.hist_mod = hist_rows;
+    sa.rho_out = rho_hist; sa.phi_hist = phi_hist; sa.energy_out = ee_hist; sa.kin_out = kin_hist;
+  } else {
+    sa.rho_out = rho_hist ? rho_hist + (size_t)step * gp : nullptr;
+    sa.phi_hist = phi_hist ? phi_hist + (size_t)step * gp : nullptr;
+    sa.energy_out = ee_hist ? ee_hist + (size_t)step * p : nullptr;
+    sa.kin_out = kin_hist ? kin_hist + (size_t)step * p : nullptr;
+  }
+  return launch_step<MODE_LEAPFROG>(a, degree, pl, (cudaStream_t)stream, &sa);
 }
 
 extern "C" int picrom_verlet_drift(const double* x, const double* v, const double* e0,

@@ -269,7 +269,7 @@ class PicEngine:
         self.nx, self.degree = mesh.num_cells, mesh.degree
         self.inst = system.inst(p)
         self.c = system.poisson.constants
-        self.ws = torch.empty(int(_lib.query("picrom_fom_workspace_bytes", n, p, self.nx,
+        self.ws = torch.zeros(int(_lib.query("picrom_fom_workspace_bytes", n, p, self.nx,
                                              self.degree)), dtype=torch.uint8, device="cuda")
         self.x = torch.empty((p, n), dtype=torch.float64, device="cuda")
         self.v = torch.empty((p, n), dtype=torch.float64, device="cuda")
@@ -285,17 +285,16 @@ class PicEngine:
         self.launches = 0
 
     def launch(self, first):
+        """One PIC step: a single fused kernel (push + last-CTA solve)."""
         dt = self.dt
         kick, kfull = (0.5 * dt, 0.0) if first else (dt, 0.5 * dt)
-        s = dev.stream_handle()
-        _lib.call("picrom_pic_push", self.x.data_ptr(), self.v.data_ptr(), self.n, self.p, self.n,
-                  self.inst.data_ptr(), self.nx, self.degree, self.phi.data_ptr(), dt, kick, kfull,
-                  0, self.counter.data_ptr(), self.ws.data_ptr(), self.status.data_ptr(), s)
-        _lib.call("picrom_pic_solve", self.n, self.p, self.nx, self.degree, self.inst.data_ptr(),
-                  self.c.khat.data_ptr(), self.c.stencil.data_ptr(), self.phi.data_ptr(), 0,
+        _lib.call("picrom_pic_step", self.x.data_ptr(), self.v.data_ptr(), self.n, self.p, self.n,
+                  self.inst.data_ptr(), self.nx, self.degree, self.c.khat.data_ptr(),
+                  self.c.stencil.data_ptr(), self.phi.data_ptr(), dt, kick, kfull, 0,
                   self.counter.data_ptr(), self.ring, self.r_rho.data_ptr(), self.r_phi.data_ptr(),
-                  self.r_ee.data_ptr(), self.r_kin.data_ptr(), self.ws.data_ptr(), s)
-        self.launches += 2
+                  self.r_ee.data_ptr(), self.r_kin.data_ptr(), self.ws.data_ptr(),
+                  self.status.data_ptr(), dev.stream_handle())
+        self.launches += 1
 
     def replay(self):
         if self.graph is None:
@@ -303,10 +302,10 @@ class PicEngine:
             with torch.cuda.graph(g):
                 for _ in range(self.ring):
                     self.launch(first=False)
-            self.launches -= 2 * self.ring
+            self.launches -= self.ring
             self.graph = g
         self.graph.replay()
-        self.launches += 2 * self.ring
+        self.launches += self.ring
 
 
 def _engine(system, p, n, dt):
