@@ -56,13 +56,63 @@ __device__ __forceinline__ long long row_start(int b, long long N, int G) {
   return ((long long)b * N) / G;
 }
 
-template <int D, int R>
+template <typename F>
+static void rom_allow_smem(F kfn) {
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    (void)cudaGetLastError();
+}
+
+// ---- U_X row tiles: double-buffered cp.async (16 B chunks) into smem ----
+constexpr int TR = 64;          // rows per tile
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory");
+}
+
+// stage rows [r0, r0 + rows) of U_X (row-major, n even) into buf (rows x n)
+__device__ __forceinline__ void stage_rows(double* buf, const double* ux, long long r0, int rows,
+                                           int n) {
+  const int chunks = rows * n / 2;               // 16-byte chunks
+  const double* src = ux + r0 * n;
+  for (int q = threadIdx.x; q < chunks; q += blockDim.x) cp_async16(buf + 2 * q, src + 2 * q);
+  cp_async_commit();
+}
+
+// dot of a staged U row (smem, 16-B aligned) with a register column, two
+// interleaved partial sums (fixed order)
+template <int NB>
+__device__ __forceinline__ double row_dot(const double* urow, const double* zc, int n) {
+  const double2* u2 = reinterpret_cast<const double2*>(urow);
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NB / 2; ++k) {
+    if (2 * k < n) {
+      const double2 uv = u2[k];
+      s0 = fma(uv.x, zc[2 * k], s0);
+      s1 = fma(uv.y, zc[2 * k + 1], s1);
+    }
+  }
+  return s0 + s1;
+}
+
+// Reconstruct + deposit: thread (r, jl) owns column c = tile*PT + jl and a
+// private histogram [row][tid] (conflict-free); U_X rows stream through a
+// double-buffered smem tile shared by all columns of the CTA.
+template <int D, int NB, int R>
 __global__ void __launch_bounds__(256) rom_deposit_kernel(RomArgs a) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int P = blockDim.x / R;               // columns per row group (mult of 32)
   const int H = blockDim.x;
   const int nh = a.nx + D;
-  double* hist = smem;                        // [nh][H]
+  const int n = a.n;
+  double* ut = smem;                          // [2][TR * n]
+  double* hist = ut + 2 * TR * n;             // [nh][H]
   const int tid = threadIdx.x;
   const int r = tid / P, jl = tid % P;
   const int c = blockIdx.y * PT + jl;         // z column
@@ -71,34 +121,61 @@ __global__ void __launch_bounds__(256) rom_deposit_kernel(RomArgs a) {
   const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
   const double h = ip[I_H], inv_h = ip[I_INVH];
   const double inv_nx = 1.0 / (double)a.nx;
-  double zc[NMAX];
+  const int mask = (a.nx & (a.nx - 1)) == 0 ? a.nx - 1 : -1;
+  double zc[NB];
 #pragma unroll
-  for (int k = 0; k < NMAX; ++k) zc[k] = (active && k < a.n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+  for (int k = 0; k < NB; ++k) zc[k] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
   for (int q = tid; q < nh * H; q += blockDim.x) hist[q] = 0.0;
-  __syncthreads();
   const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
   const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
-  if (active) {
-    for (long long i = lo + r; i < hi; i += R) {
-      const double* u = a.ux + (size_t)i * a.n;
-      double x = 0.0;
-#pragma unroll
-      for (int k = 0; k < NMAX; ++k)
-        if (k < a.n) x = fma(__ldg(u + k), zc[k], x);
-      if (!isfinite(x)) {
-        record_bad(a.status, 0, i, c, a.p);
-        continue;
-      }
-      int cell;
-      double f;
-      locate(x, h, inv_h, a.nx, inv_nx, cell, f);
-      double w[D + 1];
-      Spline<D>::weights(f, w);
-#pragma unroll
-      for (int m = 0; m <= D; ++m) hist[(cell + m) * H + tid] += w[m];
+  const int ntiles = (int)((hi - lo + TR - 1) / TR);
+  if (ntiles > 0) stage_rows(ut, a.ux, lo, (int)min((long long)TR, hi - lo), n);
+  for (int t = 0; t < ntiles; ++t) {
+    const long long t0 = lo + (long long)t * TR;
+    const int rows = (int)min((long long)TR, hi - t0);
+    if (t + 1 < ntiles) {
+      const long long t1 = t0 + TR;
+      stage_rows(ut + ((t + 1) & 1) * TR * n, a.ux, t1, (int)min((long long)TR, hi - t1), n);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const double* tile = ut + (t & 1) * TR * n;
+    if (active) {
+      for (int rr = r; rr < rows; rr += 2 * R) {
+        const bool two = rr + R < rows;
+        double xv[2];
+        xv[0] = row_dot<NB>(tile + rr * n, zc, n);
+        xv[1] = two ? row_dot<NB>(tile + (rr + R) * n, zc, n) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q == 1 && !two) break;
+          const double x = xv[q];
+          int cell;
+          double f;
+          bool rare;
+          locate_fast(x, h, inv_h, a.nx, mask, inv_nx, cell, f, rare);
+          if (rare) {
+            if (!isfinite(x)) {
+              record_bad(a.status, 0, t0 + rr + q * R, c, a.p);
+              continue;
+            }
+            locate(x, h, inv_h, a.nx, inv_nx, cell, f);
+          }
+          double w[D + 1];
+          Spline<D>::weights(f, w);
+          double* hp = hist + cell * H + tid;
+          double cur[D + 1];
+#pragma unroll
+          for (int m = 0; m <= D; ++m) cur[m] = hp[m * H];
+#pragma unroll
+          for (int m = 0; m <= D; ++m) hp[m * H] = cur[m] + w[m];
+        }
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
   // fold ghost rows and row groups (fixed order) -> seg[b][c][nd]
   const int P_used = min(PT, a.p - blockIdx.y * PT);
   for (int q = tid; q < P_used * a.nx; q += blockDim.x) {
@@ -110,16 +187,20 @@ __global__ void __launch_bounds__(256) rom_deposit_kernel(RomArgs a) {
   }
 }
 
-template <int D, int R>
+// Reconstruct + field gather + projection U_X^T E (+ optional DEIM harvest
+// lam and E output), same tiling; phi of the CTA's columns in smem [node][col].
+template <int D, int NB, int R>
 __global__ void __launch_bounds__(256) rom_gather_kernel(RomArgs a) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int P = blockDim.x / R;
   const int tid = threadIdx.x;
   const int r = tid / P, jl = tid % P;
   const int c = blockIdx.y * PT + jl;
   const bool active = c < a.p && jl < PT;
   const int nx = a.nx;
-  double* phs = smem;                          // [nx][P]
+  const int n = a.n;
+  double* ut = smem;                           // [2][TR * n]
+  double* phs = ut + 2 * TR * n;               // [nx][P]
   double* red = phs + (size_t)nx * P;          // [R][P][n] row-group partials
   const int P_used = min(PT, a.p - blockIdx.y * PT);
   for (int q = tid; q < nx * P; q += blockDim.x) {
@@ -131,79 +212,100 @@ __global__ void __launch_bounds__(256) rom_gather_kernel(RomArgs a) {
   const double h = ip[I_H], g = ip[I_INVH], inv_h = g;
   const double cf = a.coef_kind == 0 ? ip[I_GCOEF] : 1.0;
   const double inv_nx = 1.0 / (double)nx;
-  double zc[NMAX], acc[NMAX];
+  const int mask = (nx & (nx - 1)) == 0 ? nx - 1 : -1;
+  double zc[NB], acc[NB];
 #pragma unroll
-  for (int k = 0; k < NMAX; ++k) {
-    zc[k] = (active && k < a.n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+  for (int k = 0; k < NB; ++k) {
+    zc[k] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
     acc[k] = 0.0;
   }
-  __syncthreads();
   const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
   const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
-  if (active) {
-    for (long long i = lo + r; i < hi; i += R) {
-      const double* u = a.ux + (size_t)i * a.n;
-      double uk[NMAX];
-      double x = 0.0;
-#pragma unroll
-      for (int k = 0; k < NMAX; ++k) {
-        uk[k] = k < a.n ? __ldg(u + k) : 0.0;
-        if (k < a.n) x = fma(uk[k], zc[k], x);
-      }
-      if (!isfinite(x)) {
-        record_bad(a.status, 0, i, c, a.p);
-        continue;
-      }
-      int cell;
-      double f;
-      locate(x, h, inv_h, nx, inv_nx, cell, f);
-      double pv[D + 1];
-#pragma unroll
-      for (int m = 0; m <= D; ++m) {
-        int nd = cell + Spline<D>::OFF + m;
-        nd = nd < 0 ? nd + nx : (nd >= nx ? nd - nx : nd);
-        pv[m] = phs[nd * P + jl];
-      }
-      double E;
-      if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
-        E = __dmul_rn(cf, __dadd_rn(__dmul_rn(-g, pv[0]), __dmul_rn(g, pv[1])));
-      } else {
-        double dw[D + 1];
-        Spline<D>::dweights(f, g, dw);
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m <= D; ++m) s = fma(dw[m], pv[m], s);
-        E = cf * s;
-      }
-#pragma unroll
-      for (int k = 0; k < NMAX; ++k)
-        if (k < a.n) acc[k] = fma(uk[k], E, acc[k]);
-      if (a.eout) a.eout[(size_t)i * a.ldo + c] = E;
-      if (a.lam) {
-        double lv;
-        if constexpr (D == 1) {
-          lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
-        } else {
-          double w[D + 1];
-          Spline<D>::weights(f, w);
-          lv = 0.0;
-#pragma unroll
-          for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
+  const int ntiles = (int)((hi - lo + TR - 1) / TR);
+  if (ntiles > 0) stage_rows(ut, a.ux, lo, (int)min((long long)TR, hi - lo), n);
+  for (int t = 0; t < ntiles; ++t) {
+    const long long t0 = lo + (long long)t * TR;
+    const int rows = (int)min((long long)TR, hi - t0);
+    if (t + 1 < ntiles) {
+      const long long t1 = t0 + TR;
+      stage_rows(ut + ((t + 1) & 1) * TR * n, a.ux, t1, (int)min((long long)TR, hi - t1), n);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* tile = ut + (t & 1) * TR * n;
+    if (active) {
+      for (int rr = r; rr < rows; rr += R) {
+        const double* urow = tile + rr * n;
+        const double x = row_dot<NB>(urow, zc, n);
+        const long long i = t0 + rr;
+        int cell;
+        double f;
+        bool rare;
+        locate_fast(x, h, inv_h, nx, mask, inv_nx, cell, f, rare);
+        if (rare) {
+          if (!isfinite(x)) {
+            record_bad(a.status, 0, i, c, a.p);
+            continue;
+          }
+          locate(x, h, inv_h, nx, inv_nx, cell, f);
         }
-        a.lam[(size_t)i * a.ldo + c] = lv;
+        double pv[D + 1];
+#pragma unroll
+        for (int m = 0; m <= D; ++m) {
+          int nd = cell + Spline<D>::OFF + m;
+          nd = nd < 0 ? nd + nx : (nd >= nx ? nd - nx : nd);
+          pv[m] = phs[nd * P + jl];
+        }
+        double E;
+        if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
+          E = __dmul_rn(cf, __dadd_rn(__dmul_rn(-g, pv[0]), __dmul_rn(g, pv[1])));
+        } else {
+          double dw[D + 1];
+          Spline<D>::dweights(f, g, dw);
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m <= D; ++m) s = fma(dw[m], pv[m], s);
+          E = cf * s;
+        }
+        const double2* u2 = reinterpret_cast<const double2*>(urow);
+#pragma unroll
+        for (int k = 0; k < NB / 2; ++k) {
+          if (2 * k < n) {
+            const double2 uv = u2[k];
+            acc[2 * k] = fma(uv.x, E, acc[2 * k]);
+            acc[2 * k + 1] = fma(uv.y, E, acc[2 * k + 1]);
+          }
+        }
+        if (a.eout) a.eout[(size_t)i * a.ldo + c] = E;
+        if (a.lam) {
+          double lv;
+          if constexpr (D == 1) {
+            lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
+          } else {
+            double w[D + 1];
+            Spline<D>::weights(f, w);
+            lv = 0.0;
+#pragma unroll
+            for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
+          }
+          a.lam[(size_t)i * a.ldo + c] = lv;
+        }
       }
     }
+    __syncthreads();
   }
   // row-group partials -> smem -> fixed-order sum -> seg[b][c][k]
 #pragma unroll
-  for (int k = 0; k < NMAX; ++k)
-    if (k < a.n) red[((size_t)r * P + jl) * a.n + k] = acc[k];
+  for (int k = 0; k < NB; ++k)
+    if (k < n) red[((size_t)r * P + jl) * n + k] = acc[k];
   __syncthreads();
-  for (int q = tid; q < P_used * a.n; q += blockDim.x) {
-    const int cl = q / a.n, k = q % a.n;
+  for (int q = tid; q < P_used * n; q += blockDim.x) {
+    const int cl = q / n, k = q % n;
     double s = 0.0;
-    for (int rr = 0; rr < R; ++rr) s += red[((size_t)rr * P + cl) * a.n + k];
-    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * PT + cl) * a.n + k] = s;
+    for (int rr = 0; rr < R; ++rr) s += red[((size_t)rr * P + cl) * n + k];
+    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * PT + cl) * n + k] = s;
   }
 }
 
@@ -244,19 +346,56 @@ __device__ __forceinline__ long long jrow(long long i, long long half, double& s
 constexpr int GT = 16;     // rows per smem tile
 constexpr int TB = 4;      // output sub-block per thread
 
-// out = A^T B with A = blocks [0, na), B = blocks [na, nb) (na == 0: B^T B over
-// all blocks).  Rows are staged 16 at a time in smem; each thread accumulates
-// TB x TB output sub-blocks in registers; per-CTA partials -> seg.
+// out = A^T B with A = blocks [0, na), B = blocks [na, nb) (na == 0: W^T W over
+// all blocks).  Rows stream through a double-buffered smem tile filled with
+// 8-byte cp.async (J-swapped blocks read the partner row; the sign of their
+// lower half is applied in smem); each thread accumulates TB x TB output
+// sub-blocks in registers; per-CTA partials -> seg (fixed-order reduce).
+constexpr int GTR = 32;          // rows per tile
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+
 __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N, double* seg) {
-  extern __shared__ double tile[];             // [GT][W]
+  extern __shared__ __align__(16) double gsm[];
   const int W = b.off[b.nb];
-  const int a0 = 0, a1 = na > 0 ? b.off[na] : W;        // A columns [a0, a1)
-  const int b0 = na > 0 ? b.off[na] : 0, b1 = W;        // B columns [b0, b1)
+  double* tile = gsm;                                  // [2][GTR][W]
+  const double** cbase = reinterpret_cast<const double**>(tile + 2 * GTR * W);   // [W]
+  int* cld = reinterpret_cast<int*>(cbase + W);        // [W]
+  int* cjs = cld + W;                                  // [W]
+  const int a0 = 0, a1 = na > 0 ? b.off[na] : W;       // A columns [a0, a1)
+  const int b0 = na > 0 ? b.off[na] : 0, b1 = W;       // B columns [b0, b1)
   const int wa = a1 - a0, wb = b1 - b0;
   const int nbA = (wa + TB - 1) / TB, nbB = (wb + TB - 1) / TB;
   const int ntiles = nbA * nbB;
+  const long long half = N / 2;
+  bool any_js = false;
+  for (int i = 0; i < b.nb; ++i) any_js |= b.jswap[i] != 0;
+  for (int col = threadIdx.x; col < W; col += blockDim.x) {
+    int bi = 0;
+    while (col >= b.off[bi + 1]) ++bi;
+    cbase[col] = b.ptr[bi] + (col - b.off[bi]);
+    cld[col] = b.ld[bi];
+    cjs[col] = b.jswap[bi];
+  }
+  __syncthreads();
   const long long lo = row_start(blockIdx.x, N, gridDim.x);
   const long long hi = row_start(blockIdx.x + 1, N, gridDim.x);
+  const int nt = (int)((hi - lo + GTR - 1) / GTR);
+  auto stage = [&](int t) {
+    const long long r0 = lo + (long long)t * GTR;
+    const int rows = (int)min((long long)GTR, hi - r0);
+    double* dst = tile + (t & 1) * GTR * W;
+    for (int q = threadIdx.x; q < rows * W; q += blockDim.x) {
+      const int rr = q / W, col = q - rr * W;
+      long long row = r0 + rr;
+      if (cjs[col]) row = row < half ? row + half : row - half;
+      cp_async8(dst + q, cbase[col] + (size_t)row * cld[col]);
+    }
+    cp_async_commit();
+  };
   constexpr int MAXT = 4;
   double acc[MAXT][TB][TB];
 #pragma unroll
@@ -265,35 +404,32 @@ __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N
     for (int i = 0; i < TB; ++i)
 #pragma unroll
       for (int j = 0; j < TB; ++j) acc[s][i][j] = 0.0;
-  for (long long r0 = lo; r0 < hi; r0 += GT) {
-    const int rows = (int)min((long long)GT, hi - r0);
+  if (nt > 0) stage(0);
+  for (int t = 0; t < nt; ++t) {
+    const long long r0 = lo + (long long)t * GTR;
+    const int rows = (int)min((long long)GTR, hi - r0);
+    if (t + 1 < nt) { stage(t + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
     __syncthreads();
-    for (int q = threadIdx.x; q < GT * W; q += blockDim.x) {
-      const int rr = q / W, col = q % W;
-      double v = 0.0;
-      if (rr < rows) {
-        int bi = 0;
-        while (col >= b.off[bi + 1]) ++bi;
-        long long row = r0 + rr;
-        double sgn = 1.0;
-        if (b.jswap[bi]) row = jrow(row, N / 2, sgn);
-        v = sgn * __ldg(b.ptr[bi] + (size_t)row * b.ld[bi] + (col - b.off[bi]));
+    double* cur = tile + (t & 1) * GTR * W;
+    if (any_js && r0 + rows > half) {      // J: negate the (new) lower half of swapped blocks
+      for (int q = threadIdx.x; q < rows * W; q += blockDim.x) {
+        const int rr = q / W, col = q - rr * W;
+        if (cjs[col] && r0 + rr >= half) cur[q] = -cur[q];
       }
-      tile[rr * W + col] = v;
+      __syncthreads();
     }
-    __syncthreads();
 #pragma unroll
     for (int s = 0; s < MAXT; ++s) {
-      const int t = threadIdx.x + s * blockDim.x;
-      if (t >= ntiles) break;
-      const int bi = t / nbB, bj = t % nbB;
+      const int tt = threadIdx.x + s * blockDim.x;
+      if (tt >= ntiles) break;
+      const int bi = tt / nbB, bj = tt % nbB;
       for (int rr = 0; rr < rows; ++rr) {
         double av[TB], bv[TB];
 #pragma unroll
         for (int i = 0; i < TB; ++i) {
           const int ci = bi * TB + i, cj = bj * TB + i;
-          av[i] = ci < wa ? tile[rr * W + a0 + ci] : 0.0;
-          bv[i] = cj < wb ? tile[rr * W + b0 + cj] : 0.0;
+          av[i] = ci < wa ? cur[rr * W + a0 + ci] : 0.0;
+          bv[i] = cj < wb ? cur[rr * W + b0 + cj] : 0.0;
         }
 #pragma unroll
         for (int i = 0; i < TB; ++i)
@@ -301,13 +437,14 @@ __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N
           for (int j = 0; j < TB; ++j) acc[s][i][j] = fma(av[i], bv[j], acc[s][i][j]);
       }
     }
+    __syncthreads();
   }
   double* out = seg + (size_t)blockIdx.x * wa * wb;
 #pragma unroll
   for (int s = 0; s < MAXT; ++s) {
-    const int t = threadIdx.x + s * blockDim.x;
-    if (t >= ntiles) break;
-    const int bi = t / nbB, bj = t % nbB;
+    const int tt = threadIdx.x + s * blockDim.x;
+    if (tt >= ntiles) break;
+    const int bi = tt / nbB, bj = tt % nbB;
 #pragma unroll
     for (int i = 0; i < TB; ++i)
 #pragma unroll
@@ -491,6 +628,11 @@ __global__ void deim_gather_kernel(const double* uxd, const double* z, int ldz, 
   }
 }
 
+int gram_grid(long long N) {
+  long long g = std::min<long long>(2LL * picrom_num_sms(), std::max<long long>(1, N / 256));
+  return (int)g;
+}
+
 int rom_grid(long long N) {
   long long g = std::min<long long>((long long)picrom_num_sms(), std::max<long long>(1, N / 64));
   return (int)g;
@@ -504,54 +646,66 @@ extern "C" size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx) 
   const size_t G = (size_t)rom_grid(N);
   const size_t dep = G * p * nx;
   const size_t gat = G * p * n;
-  const size_t gram = G * 256 * 256;
+  const size_t gram = (size_t)gram_grid(N) * 256 * 256;
   return std::max(std::max(dep, gat), gram) * sizeof(double) + 256;
 }
 
-template <int D>
-static int launch_rom_deposit(const RomArgs& a, int G, cudaStream_t s) {
+template <int D, int NB>
+static int launch_rom_deposit_nb(const RomArgs& a, int G, cudaStream_t s) {
   const int tiles = (a.p + PT - 1) / PT;
   const int P = std::min(PT, ((std::min(a.p, PT) + 31) / 32) * 32);
   int R = std::max(1, std::min(256 / P, 2));
-  size_t sm = (size_t)(a.nx + D) * (R * P) * sizeof(double);
-  while (R > 1 && sm > 200 * 1024) { --R; sm = (size_t)(a.nx + D) * (R * P) * sizeof(double); }
-  if (sm > 227 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "rom deposit: nx too large");
+  auto smem = [&](int rr) {
+    return (size_t)2 * TR * a.n * sizeof(double) + (size_t)(a.nx + D) * (rr * P) * sizeof(double);
+  };
+  while (R > 1 && smem(R) > 200 * 1024) --R;
+  if (smem(R) > 227 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "rom deposit: nx too large");
   dim3 grid(G, tiles);
   if (R == 2) {
-    cudaFuncSetAttribute(rom_deposit_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    rom_deposit_kernel<D, 2><<<grid, 2 * P, sm, s>>>(a);
+    rom_allow_smem(rom_deposit_kernel<D, NB, 2>);
+    rom_deposit_kernel<D, NB, 2><<<grid, 2 * P, smem(2), s>>>(a);
   } else {
-    cudaFuncSetAttribute(rom_deposit_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    rom_deposit_kernel<D, 1><<<grid, P, sm, s>>>(a);
+    rom_allow_smem(rom_deposit_kernel<D, NB, 1>);
+    rom_deposit_kernel<D, NB, 1><<<grid, P, smem(1), s>>>(a);
   }
   return picrom_check_launch("rom_deposit_kernel");
 }
 
-template <int D>
-static int launch_rom_gather(const RomArgs& a, int G, cudaStream_t s) {
+template <int D, int NB>
+static int launch_rom_gather_nb(const RomArgs& a, int G, cudaStream_t s) {
   const int tiles = (a.p + PT - 1) / PT;
   const int P = std::min(PT, ((std::min(a.p, PT) + 31) / 32) * 32);
   const int R = std::max(1, std::min(256 / P, 4));
-  const size_t sm = ((size_t)a.nx * P + (size_t)R * P * a.n) * sizeof(double);
+  const size_t sm = ((size_t)2 * TR * a.n + (size_t)a.nx * P + (size_t)R * P * a.n) * sizeof(double);
   if (sm > 227 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "rom gather: nx too large");
   dim3 grid(G, tiles);
   switch (R) {
-    case 1:
-      cudaFuncSetAttribute(rom_gather_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      rom_gather_kernel<D, 1><<<grid, P, sm, s>>>(a); break;
-    case 2:
-      cudaFuncSetAttribute(rom_gather_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      rom_gather_kernel<D, 2><<<grid, 2 * P, sm, s>>>(a); break;
-    default:
-      cudaFuncSetAttribute(rom_gather_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      rom_gather_kernel<D, 4><<<grid, 4 * P, sm, s>>>(a); break;
+    case 1: rom_allow_smem(rom_gather_kernel<D, NB, 1>); rom_gather_kernel<D, NB, 1><<<grid, P, sm, s>>>(a); break;
+    case 2: rom_allow_smem(rom_gather_kernel<D, NB, 2>); rom_gather_kernel<D, NB, 2><<<grid, 2 * P, sm, s>>>(a); break;
+    default: rom_allow_smem(rom_gather_kernel<D, NB, 4>); rom_gather_kernel<D, NB, 4><<<grid, 4 * P, sm, s>>>(a); break;
   }
   return picrom_check_launch("rom_gather_kernel");
 }
 
+// basis dimension -> register block size (n <= NB, even)
+#define ROM_NB_DISPATCH(FN, D, A, G, S)                       \
+  (A.n <= 4 ? FN<D, 4>(A, G, S) : A.n <= 8 ? FN<D, 8>(A, G, S) :  \
+   A.n <= 12 ? FN<D, 12>(A, G, S) : A.n <= 16 ? FN<D, 16>(A, G, S) : \
+   A.n <= 20 ? FN<D, 20>(A, G, S) : A.n <= 24 ? FN<D, 24>(A, G, S) : FN<D, 32>(A, G, S))
+
+template <int D>
+static int launch_rom_deposit(const RomArgs& a, int G, cudaStream_t s) {
+  return ROM_NB_DISPATCH(launch_rom_deposit_nb, D, a, G, s);
+}
+
+template <int D>
+static int launch_rom_gather(const RomArgs& a, int G, cudaStream_t s) {
+  return ROM_NB_DISPATCH(launch_rom_gather_nb, D, a, G, s);
+}
+
 static int rom_check(long long N, int n, int p, int nx, int degree) {
   if (N < 1 || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "need N >= 1 and p >= 1");
-  if (n < 1 || n > NMAX) return picrom_set_error(PICROM_ERR_CONFIG, "basis dimension must be in [1, 32]");
+  if (n < 2 || n > NMAX || (n & 1)) return picrom_set_error(PICROM_ERR_CONFIG, "basis dimension must be even, in [2, 32]");
   if (degree < 1 || degree > 3) return picrom_set_error(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
   if (nx < 2) return picrom_set_error(PICROM_ERR_CONFIG, "need nx >= 2");
   return PICROM_OK;
@@ -627,9 +781,10 @@ static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* 
   const int nbA = (wa + TB - 1) / TB, nbB = (wb + TB - 1) / TB;
   if (W > 256 || nbA * nbB > 4 * 256)
     return picrom_set_error(PICROM_ERR_CONFIG, "Gram: total width <= 256 and wa*wb <= 16384");
-  const int G = rom_grid(N);
+  const int G = gram_grid(N);
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t sm = (size_t)GT * W * sizeof(double);
+  const size_t sm = (size_t)2 * GTR * W * sizeof(double) + (size_t)W * (sizeof(void*) + 2 * sizeof(int));
+  rom_allow_smem(gram_kernel);
   gram_kernel<<<G, 256, sm, s>>>(b, na, N, (double*)ws);
   int rc = picrom_check_launch("gram_kernel");
   if (rc) return rc;
