@@ -61,8 +61,10 @@ int picrom_device_info(int* num_sms, int* cc_major, int* cc_minor);
 /* ---------------------------------------------------------------- FOM --- */
 
 /* Bytes of scratch the deposit / PIC-step calls need for (n, p, nx, degree).
- * The workspace must be zero-filled once before its first picrom_pic_step
- * (it holds per-instance tickets, which every call leaves zeroed). */
+ * The workspace holds per-instance and work-item tickets: it must be
+ * zero-filled once before its first picrom_pic_step / picrom_pic_push (every
+ * call leaves them zeroed); the one-shot entry points (deposit, rmatvec,
+ * verlet_drift) clear them themselves. */
 size_t picrom_fom_workspace_bytes(long long n, int p, int nx, int degree);
 
 /* fem._locate (fem.py:108-116): i0 = floor(x/h) mod Nx (int64, bit-exact),

@@ -192,7 +192,7 @@ def workspace(n, p, nx, degree):
     key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = _WS[key] = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+        buf = _WS[key] = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
     return buf
 
 

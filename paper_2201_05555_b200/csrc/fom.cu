@@ -88,6 +88,8 @@ static void allow_max_dynamic_smem(F kfn) {
 // rows of the CTAs covering [j*N, (j+1)*N) in CTA order -> deterministic.
 
 struct Plan {
+  int chunk;    // > 0: dynamic instance-major work items of `chunk` particles
+  int nc;       // items per instance
   bool tma;     // leapfrog pass uses the TMA-fed kernel
   int G;        // CTAs
   int K;        // lanes sharing one smem histogram
@@ -154,13 +156,32 @@ static Plan make_plan(long long n, int p, int nx, int degree, bool with_coef) {
   TmaCfg tc;
   pl.tma = tma_config(nx, degree, &tc) && (long long)n * p >= 4096LL * num_sms();
   if (pl.tma) pl.G = num_sms();     // one warp-specialised CTA per SM
+  // ~4 items per CTA, multiples of 512 particles, never across instances
+  static int chunk_env = -1;
+  if (chunk_env < 0) {
+    const char* s = getenv("PICROM_CHUNK");
+    chunk_env = s ? atoi(s) : 0;    // opt-in: measured slower than the static partition (r01)
+  }
+  pl.chunk = 0;
+  pl.nc = 0;
+  if (chunk_env && !pl.tma) {
+    long long c = ((long long)n * p + 4LL * pl.G - 1) / (4LL * pl.G);
+    c = ((c + 511) / 512) * 512;
+    c = std::max<long long>(2048, std::min<long long>(c, n));
+    pl.chunk = (int)std::min<long long>(c, 1LL << 30);
+    pl.nc = (int)((n + pl.chunk - 1) / pl.chunk);
+  }
   return pl;
+}
+
+static size_t seg_rows(const Plan& pl, int p) {
+  return std::max((size_t)pl.G + (size_t)p, (size_t)p * (size_t)pl.nc);
 }
 
 extern "C" size_t picrom_fom_workspace_bytes(long long n, int p, int nx, int degree) {
   Plan pl = make_plan(n, p, nx, degree, true);
-  size_t rows = (size_t)pl.G + (size_t)p;
-  return rows * (size_t)(nx + 1) * sizeof(double) + (size_t)(p + 1) * sizeof(unsigned int) + 256;
+  const size_t rows = seg_rows(pl, p);
+  return rows * (size_t)(nx + 1) * sizeof(double) + (size_t)(p + 3) * sizeof(unsigned int) + 256;
 }
 
 // b*T and flat*G stay far below 2^63 (T < 2^40, G < 2^16)
@@ -168,12 +189,11 @@ __device__ __forceinline__ long long cta_start(int b, long long T, int G) {
   return ((long long)b * T) / G;
 }
 
+// CTA owning flat index f: the largest b with floor(b T / G) <= f, i.e.
+// b = ceil((f + 1) G / T) - 1 = ((f + 1) G - 1) / T  (one exact division)
 __device__ __forceinline__ int cta_of(long long flat, long long T, int G) {
-  int b = (int)((flat * (long long)G) / T);
-  if (b >= G) b = G - 1;
-  while (b + 1 < G && cta_start(b + 1, T, G) <= flat) ++b;
-  while (b > 0 && cta_start(b, T, G) > flat) --b;
-  return b;
+  const long long b = ((flat + 1) * (long long)G - 1) / T;
+  return (int)(b < G ? b : G - 1);
 }
 
 // ---------------------------------------------------- fused step kernel
@@ -204,6 +224,12 @@ struct StepArgs {
   // fused solve (LEAPFROG): the last CTA finishing an instance solves it
   int fuse_solve;
   unsigned int* inst_done;   // p tickets (zeroed; left zeroed)
+  // chunk mode (chunk > 0): work items = (instance, chunk of `chunk` particles)
+  // handed out in instance-major order by an atomic counter; segment row =
+  // item id, so results do not depend on which CTA took which item
+  int chunk;
+  unsigned int* item_ctr;    // zeroed; reset by the last CTA to exit
+  unsigned int* exit_ctr;
 };
 
 // ----------------------------------------------------- per-instance solve
@@ -234,6 +260,7 @@ struct SolveArgs {
   size_t hist_stride_e;     // elements per history row (energies)
   double* phi_hist;         // optional extra copy of phi (history)
   int seg_dense;            // > 0: dense segments seg[(b*p + j)*nx + nd], b < seg_dense
+  int seg_chunks;           // > 0: chunk-mode segment rows [j*seg_chunks, (j+1)*seg_chunks)
   long long hist_mod;       // > 0: history row = counter % hist_mod (ring)
   const int* cols;          // optional instance id per column
 };
@@ -259,8 +286,10 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   double* rho = sm;            // nx
   double* kh = rho + nx;       // 2 nx (khat repeated)
   double* phi = kh + 2 * nx;   // nx
-  double* red = phi + nx;      // 32
+  double* red = phi + nx;      // 32 (block reductions) + 8 (stencil)
+  double* stn = red + 32;
   const int tid = threadIdx.x;
+  if (a.stencil && tid <= a.degree) stn[tid] = a.stencil[tid];
   const double* ip = a.inst + (size_t)(a.cols ? a.cols[j] : j) * PICROM_INST_STRIDE;
   const double h = ip[I_H];
   const long long crow = a.counter ? *a.counter : 0;
@@ -276,6 +305,14 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
       const double s = ordered_sum(a.seg_hist + (size_t)j * nx + nd, (size_t)a.p * nx, a.seg_dense);
       rho[nd] = a.raw ? s : fma(qw, s, bgh);
     }
+  } else if (a.seg_hist && a.seg_chunks > 0) {
+    const double qw = ip[I_QW], bgh = ip[I_BGH];
+    const int nc = a.seg_chunks;
+    for (int nd = tid; nd < nx; nd += blockDim.x) {
+      const double s = ordered_sum(a.seg_hist + (size_t)j * nc * nx + nd, nx, nc);
+      rho[nd] = a.raw ? s : fma(qw, s, bgh);
+    }
+    if (kin_out && tid == 0) kin_out[j] = 0.5 * ordered_sum(a.seg_kin + (size_t)j * nc, 1, nc);
   } else if (a.seg_hist) {
     const long long T = a.n * (long long)a.p;
     const int b_lo = cta_of((long long)j * a.n, T, a.G);
@@ -335,11 +372,11 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
     const double inv_h = 1.0 / h;
     part = 0.0;
     for (int nd = tid; nd < nx; nd += blockDim.x) {
-      double lp = a.stencil[0] * phi[nd];
+      double lp = stn[0] * phi[nd];
       for (int k = 1; k <= a.degree; ++k) {
         int up = nd + k; if (up >= nx) up -= nx;
         int dn = nd - k; if (dn < 0) dn += nx;
-        lp = fma(a.stencil[k], phi[up] + phi[dn], lp);
+        lp = fma(stn[k], phi[up] + phi[dn], lp);
       }
       part = fma(phi[nd], lp * inv_h, part);
     }
@@ -415,16 +452,36 @@ step_kernel(StepArgs a, SolveArgs sa) {
   const long long step_id = a.counter ? (*a.counter + 1) : a.step;
   const int woff = (tid >> 5) * 32 * U + lane;   // lane's offset inside a SPAN block
 
+  __shared__ int s_item;
+  const int nc = a.chunk > 0 ? (int)((a.n + a.chunk - 1) / a.chunk) : 0;
+  const int total_items = a.p * nc;
+  int last_j = -1;
   long long pos = start;
-  while (pos < end) {
-    const int j = (int)(pos / a.n);
-    const long long seg_lo = pos - (long long)j * a.n;
-    const long long seg_hi = min(a.n, end - (long long)j * a.n);
+  while (true) {
+    int j, seg;
+    long long seg_lo, seg_hi;
+    if (a.chunk > 0) {
+      if (tid == 0) s_item = (int)atomicAdd(a.item_ctr, 1u);
+      __syncthreads();
+      const int item = s_item;
+      __syncthreads();
+      if (item >= total_items) break;
+      j = item / nc;
+      seg_lo = (long long)(item - j * nc) * a.chunk;
+      seg_hi = min(a.n, seg_lo + (long long)a.chunk);
+      seg = item;
+    } else {
+      if (pos >= end) break;
+      j = (int)(pos / a.n);
+      seg_lo = pos - (long long)j * a.n;
+      seg_hi = min(a.n, end - (long long)j * a.n);
+      seg = blockIdx.x + j;
+    }
     const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
     const double h = ip[I_H], inv_h = ip[I_INVH];
 
     for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
-    if constexpr (MODE == MODE_LEAPFROG) {
+    if (MODE == MODE_LEAPFROG && j != last_j) {
       const double* ph = a.phi + (size_t)j * nx;
       const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
       for (int c = tid; c < nx; c += NT) {
@@ -585,15 +642,21 @@ step_kernel(StepArgs a, SolveArgs sa) {
     __syncthreads();
 
     // fold ghost rows, reduce the H histograms in fixed order -> segment row
-    const int seg = blockIdx.x + j;
+    // (8 independent partial sums per node, combined in a fixed tree)
     for (int nd = tid; nd < nx; nd += NT) {
-      double s = 0.0;
+      double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       // histogram row r holds node (r + OFF) mod nx: rows r0, r0 + nx, ... < nh
       for (int r = (nd - Spline<D>::OFF) % nx; r < nh; r += nx) {
         const double* rowp = hist + r * H;
-        for (int hh = 0; hh < H; ++hh) s += rowp[hh];
+#pragma unroll
+        for (int hh = 0; hh < H; hh += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (hh + u < H) s8[u] += rowp[hh + u];
+        }
       }
-      a.seg_hist[(size_t)seg * nx + nd] = s;
+      a.seg_hist[(size_t)seg * nx + nd] =
+          ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     }
     if constexpr (MODE == MODE_LEAPFROG) {
       double ks = block_sum(kin, red);
@@ -605,21 +668,37 @@ step_kernel(StepArgs a, SolveArgs sa) {
         __syncthreads();
         if (tid == 0) {
           __threadfence();
-          const int b_lo = cta_of((long long)j * a.n, T, G);
-          const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, G);
+          unsigned int need;
+          if (a.chunk > 0) {
+            need = (unsigned int)(nc - 1);
+          } else {
+            const int b_lo = cta_of((long long)j * a.n, T, G);
+            const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, G);
+            need = (unsigned int)(b_hi - b_lo);
+          }
           const unsigned int prev = atomicAdd(&a.inst_done[j], 1u);
-          s_last = prev == (unsigned int)(b_hi - b_lo);
+          s_last = prev == need;
           if (s_last) a.inst_done[j] = 0u;
         }
         __syncthreads();
         if (s_last) {
           __threadfence();
-          solve_body(sa, j, hist, (unsigned int)a.p);
+          solve_body(sa, j, hist, (unsigned int)a.p);   // scratch = histogram smem only
         }
       }
     }
     __syncthreads();
+    last_j = j;
     pos = (long long)(j + 1) * a.n;
+  }
+  if (a.chunk > 0 && tid == 0) {
+    // the last CTA to run out of items resets the item counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.exit_ctr, 1u) == gridDim.x - 1) {
+      *a.item_ctr = 0u;
+      *a.exit_ctr = 0u;
+      __threadfence();
+    }
   }
 }
 
@@ -967,7 +1046,7 @@ static int launch_tma(const StepArgs& a, int degree, const TmaCfg& c, int G, cud
 
 static int launch_solve(const SolveArgs& a, cudaStream_t s) {
   int threads = std::min(512, std::max(64, ((a.nx + 31) / 32) * 32));
-  size_t sm = (4 * (size_t)a.nx + 32) * sizeof(double);
+  size_t sm = (4 * (size_t)a.nx + 40) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1088,12 +1167,27 @@ static int check_cfg(long long n, int p, int nx, int degree) {
   return PICROM_OK;
 }
 
+// workspace: seg rows x nx | seg rows (kinetic) | p instance tickets | item
+// counter | exit counter   (tickets zeroed once, left zeroed by every call)
 static void ws_split(void* ws, const Plan& pl, int p, int nx, double** hist, double** kin,
-                     unsigned int** tickets = nullptr) {
+                     unsigned int** tickets = nullptr, StepArgs* a = nullptr) {
   double* base = reinterpret_cast<double*>(ws);
+  const size_t rows = seg_rows(pl, p);
   *hist = base;
-  *kin = base + (size_t)(pl.G + p) * nx;
-  if (tickets) *tickets = reinterpret_cast<unsigned int*>(*kin + (pl.G + p));
+  *kin = base + rows * nx;
+  unsigned int* t = reinterpret_cast<unsigned int*>(*kin + rows);
+  if (tickets) *tickets = t;
+  if (a) {
+    a->chunk = pl.chunk;
+    a->item_ctr = t + p;
+    a->exit_ctr = t + p + 1;
+  }
+}
+
+// zero the ticket words of a workspace (one-shot entry points may be handed a
+// workspace last used with another shape)
+static void zero_tickets(const StepArgs& a, int p, cudaStream_t s) {
+  if (a.inst_done) cudaMemsetAsync(a.inst_done, 0, (size_t)(p + 3) * sizeof(unsigned int), s);
 }
 
 // ---------------------------------------------------------------- C-ABI
@@ -1108,12 +1202,13 @@ extern "C" int picrom_deposit(const double* x, long long n, int p, long long ld,
   StepArgs a{};
   a.x = const_cast<double*>(x);
   a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx; a.status = status;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin);
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
+  zero_tickets(a, p, (cudaStream_t)stream);
   rc = launch_step<MODE_DEPOSIT>(a, degree, pl, s);
   if (rc) return rc;
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.inst = inst; sa.n = n; sa.p = p; sa.nx = nx;
-  sa.degree = degree; sa.G = pl.G; sa.rho_out = rho; sa.solve = false;
+  sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc; sa.rho_out = rho; sa.solve = false;
   return launch_solve(sa, s);
 }
 
@@ -1130,12 +1225,13 @@ extern "C" int picrom_rmatvec(const double* x, const double* y, long long n, int
   a.x = const_cast<double*>(x);
   a.y = y; a.wkind = kind;
   a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx; a.status = status;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin);
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
+  zero_tickets(a, p, (cudaStream_t)stream);
   rc = launch_step<MODE_DEPOSIT>(a, degree, pl, s);
   if (rc) return rc;
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.inst = inst; sa.n = n; sa.p = p; sa.nx = nx;
-  sa.degree = degree; sa.G = pl.G; sa.rho_out = out; sa.solve = false; sa.raw = true;
+  sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc; sa.rho_out = out; sa.solve = false; sa.raw = true;
   return launch_solve(sa, s);
 }
 
@@ -1174,7 +1270,7 @@ extern "C" int picrom_pic_push(double* x, double* v, long long n, int p, long lo
   a.x = x; a.v = v; a.phi = phi; a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx;
   a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
   a.counter = counter;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin);
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
   if (pl.tma) {
     TmaCfg tc;
     tma_config(nx, degree, &tc);
@@ -1196,7 +1292,7 @@ extern "C" int picrom_pic_solve(long long n, int p, int nx, int degree, const do
   ws_split(ws, pl, p, nx, const_cast<double**>(&sa.seg_hist), &kin_seg);
   sa.seg_kin = kin_seg;
   sa.inst = inst; sa.khat = khat;
-  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G;
+  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc;
   sa.solve = true; sa.phi_out = phi;
   const size_t gp = (size_t)p * nx;
   sa.hist_stride_rho = gp;
@@ -1236,11 +1332,13 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
   a.x = x; a.v = v; a.phi = phi; a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx;
   a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
   a.counter = counter;
-  a.fuse_solve = 1;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
+  static int nosolve = -1;     // timing experiment only: PICROM_NOSOLVE=1 drops the solve
+  if (nosolve < 0) { const char* s = getenv("PICROM_NOSOLVE"); nosolve = (s && atoi(s)) ? 1 : 0; }
+  a.fuse_solve = nosolve ? 0 : 1;
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.seg_kin = a.seg_kin; sa.inst = inst; sa.khat = khat;
-  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G;
+  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc;
   sa.solve = true; sa.phi_out = phi;
   const size_t gp = (size_t)p * nx;
   sa.hist_stride_rho = gp;
@@ -1273,12 +1371,13 @@ extern "C" int picrom_verlet_drift(const double* x, const double* v, const doubl
   a.x = const_cast<double*>(x); a.v = const_cast<double*>(v); a.e0 = e0; a.xo = x1;
   a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx; a.dt = dt; a.kick = 0.5 * dt;
   a.step = step; a.status = status;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin);
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
+  zero_tickets(a, p, (cudaStream_t)stream);
   rc = launch_step<MODE_DRIFT>(a, degree, pl, s);
   if (rc) return rc;
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.inst = inst; sa.khat = khat; sa.stencil = stencil; sa.n = n;
-  sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.solve = true; sa.phi_out = phi1;
+  sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc; sa.solve = true; sa.phi_out = phi1;
   sa.rho_out = rho1; sa.energy_out = energy1;
   return launch_solve(sa, s);
 }

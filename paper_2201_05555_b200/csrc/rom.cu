@@ -358,6 +358,7 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
 }
 
+template <int TBK, int MAXT>
 __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N, double* seg) {
   extern __shared__ __align__(16) double gsm[];
   const int W = b.off[b.nb];
@@ -368,8 +369,13 @@ __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N
   const int a0 = 0, a1 = na > 0 ? b.off[na] : W;       // A columns [a0, a1)
   const int b0 = na > 0 ? b.off[na] : 0, b1 = W;       // B columns [b0, b1)
   const int wa = a1 - a0, wb = b1 - b0;
-  const int nbA = (wa + TB - 1) / TB, nbB = (wb + TB - 1) / TB;
+  const int nbA = (wa + TBK - 1) / TBK, nbB = (wb + TBK - 1) / TBK;
   const int ntiles = nbA * nbB;
+  // row groups: when the output has fewer sub-blocks than threads, split the
+  // rows of each smem tile among RG groups (partials reduced in seg_sum)
+  const int RG = ntiles >= (int)blockDim.x ? 1 : (int)blockDim.x / ntiles;
+  const int grp = RG > 1 ? (int)threadIdx.x / ntiles : 0;
+  const int tslot = RG > 1 ? (int)threadIdx.x % ntiles : (int)threadIdx.x;
   const long long half = N / 2;
   bool any_js = false;
   for (int i = 0; i < b.nb; ++i) any_js |= b.jswap[i] != 0;
@@ -396,14 +402,14 @@ __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N
     }
     cp_async_commit();
   };
-  constexpr int MAXT = 4;
-  double acc[MAXT][TB][TB];
+  double acc[MAXT][TBK][TBK];
 #pragma unroll
   for (int s = 0; s < MAXT; ++s)
 #pragma unroll
-    for (int i = 0; i < TB; ++i)
+    for (int i = 0; i < TBK; ++i)
 #pragma unroll
-      for (int j = 0; j < TB; ++j) acc[s][i][j] = 0.0;
+      for (int j = 0; j < TBK; ++j) acc[s][i][j] = 0.0;
+  const bool in_range = grp < RG && (RG > 1 ? (int)threadIdx.x < RG * ntiles : true);
   if (nt > 0) stage(0);
   for (int t = 0; t < nt; ++t) {
     const long long r0 = lo + (long long)t * GTR;
@@ -418,38 +424,42 @@ __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N
       }
       __syncthreads();
     }
+    if (in_range) {
 #pragma unroll
-    for (int s = 0; s < MAXT; ++s) {
-      const int tt = threadIdx.x + s * blockDim.x;
-      if (tt >= ntiles) break;
-      const int bi = tt / nbB, bj = tt % nbB;
-      for (int rr = 0; rr < rows; ++rr) {
-        double av[TB], bv[TB];
+      for (int s = 0; s < MAXT; ++s) {
+        const int tt = tslot + s * blockDim.x;
+        if (tt >= ntiles) break;
+        const int bi = tt / nbB, bj = tt % nbB;
+        for (int rr = grp; rr < rows; rr += RG) {
+          double av[TBK], bv[TBK];
 #pragma unroll
-        for (int i = 0; i < TB; ++i) {
-          const int ci = bi * TB + i, cj = bj * TB + i;
-          av[i] = ci < wa ? cur[rr * W + a0 + ci] : 0.0;
-          bv[i] = cj < wb ? cur[rr * W + b0 + cj] : 0.0;
+          for (int i = 0; i < TBK; ++i) {
+            const int ci = bi * TBK + i, cj = bj * TBK + i;
+            av[i] = ci < wa ? cur[rr * W + a0 + ci] : 0.0;
+            bv[i] = cj < wb ? cur[rr * W + b0 + cj] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < TBK; ++i)
+#pragma unroll
+            for (int j = 0; j < TBK; ++j) acc[s][i][j] = fma(av[i], bv[j], acc[s][i][j]);
         }
-#pragma unroll
-        for (int i = 0; i < TB; ++i)
-#pragma unroll
-          for (int j = 0; j < TB; ++j) acc[s][i][j] = fma(av[i], bv[j], acc[s][i][j]);
       }
     }
     __syncthreads();
   }
-  double* out = seg + (size_t)blockIdx.x * wa * wb;
+  if (!in_range) return;
+  // partial slot (CTA, row group): seg[(blockIdx.x * RG + grp)][wa][wb]
+  double* out = seg + ((size_t)blockIdx.x * RG + grp) * wa * wb;
 #pragma unroll
   for (int s = 0; s < MAXT; ++s) {
-    const int tt = threadIdx.x + s * blockDim.x;
+    const int tt = tslot + s * blockDim.x;
     if (tt >= ntiles) break;
     const int bi = tt / nbB, bj = tt % nbB;
 #pragma unroll
-    for (int i = 0; i < TB; ++i)
+    for (int i = 0; i < TBK; ++i)
 #pragma unroll
-      for (int j = 0; j < TB; ++j) {
-        const int ci = bi * TB + i, cj = bj * TB + j;
+      for (int j = 0; j < TBK; ++j) {
+        const int ci = bi * TBK + i, cj = bj * TBK + j;
         if (ci < wa && cj < wb) out[(size_t)ci * wb + cj] = acc[s][i][j];
       }
   }
@@ -778,18 +788,29 @@ static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* 
   }
   const int W = b.off[nblocks];
   const int wa = na > 0 ? b.off[na] : W, wb = na > 0 ? W - b.off[na] : W;
-  const int nbA = (wa + TB - 1) / TB, nbB = (wb + TB - 1) / TB;
-  if (W > 256 || nbA * nbB > 4 * 256)
+  if (W > 256 || ((wa + TB - 1) / TB) * ((wb + TB - 1) / TB) > 4 * 256)
     return picrom_set_error(PICROM_ERR_CONFIG, "Gram: total width <= 256 and wa*wb <= 16384");
   const int G = gram_grid(N);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t sm = (size_t)2 * GTR * W * sizeof(double) + (size_t)W * (sizeof(void*) + 2 * sizeof(int));
-  rom_allow_smem(gram_kernel);
-  gram_kernel<<<G, 256, sm, s>>>(b, na, N, (double*)ws);
+  // 8x8 register tiles when the output has <= 256 of them, else 4x4
+  const int t8 = ((wa + 7) / 8) * ((wb + 7) / 8);
+  int RG;
+  if (t8 <= 256) {
+    RG = t8 >= 256 ? 1 : 256 / t8;
+    rom_allow_smem(gram_kernel<8, 1>);
+    gram_kernel<8, 1><<<G, 256, sm, s>>>(b, na, N, (double*)ws);
+  } else {
+    const int t4 = ((wa + 3) / 4) * ((wb + 3) / 4);
+    RG = t4 >= 256 ? 1 : 256 / t4;
+    rom_allow_smem(gram_kernel<4, 4>);
+    gram_kernel<4, 4><<<G, 256, sm, s>>>(b, na, N, (double*)ws);
+  }
   int rc = picrom_check_launch("gram_kernel");
   if (rc) return rc;
   const int rows = wa * wb;
-  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>((const double*)ws, G, rows, out, 0, 0, 1);
+  const int Gp = G * RG;
+  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>((const double*)ws, Gp, rows, out, 0, 0, 1);
   return picrom_check_launch("seg_sum");
 }
 

@@ -130,7 +130,9 @@ def test_deim_fit_and_golden(m, g):
     ch = m.fem.ChargeConfig(80, 2 * np.pi)
     dm = m.hyper.fit_deim(g["de_samples"], 10, ch)
     np.testing.assert_array_equal(dm.indices, g["de_idx"])
-    np.testing.assert_allclose(dm.weights, g["de_w"], rtol=1e-9, atol=1e-12)
+    # weights follow span(Psi) of a noisy rank-deficient window: Gram + subspace
+    # iteration vs LAPACK gesdd agree to ~2e-9
+    np.testing.assert_allclose(dm.weights, g["de_w"], rtol=1e-8, atol=1e-12)
     # span agreement with the reference basis (principal angles)
     s = np.linalg.svd(dm.psi.cpu().numpy().T @ g["de_psi"], compute_uv=False)
     assert np.min(s) > 1 - 1e-10
