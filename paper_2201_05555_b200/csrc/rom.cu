@@ -20,6 +20,8 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -465,6 +467,139 @@ __global__ void __launch_bounds__(256) gram_kernel(Blocks b, int na, long long N
   }
 }
 
+// TMA variant of the Gram (all blocks row-contiguous, 16-B aligned): each
+// tile of GT2 rows of every block lands in smem with ONE cp.async.bulk per
+// block (two for a J-swapped block straddling N/2), double-buffered on
+// mbarriers; the LSU issues nothing for the staging.
+constexpr int GT2 = 64;
+
+template <int TBK, int MAXT>
+__global__ void __launch_bounds__(256) gram_tma_kernel(Blocks b, int na, long long N, double* seg) {
+  extern __shared__ __align__(128) double gsm2[];
+  const int W = b.off[b.nb];
+  const int SZ = GT2 * W;                                   // doubles per stage
+  double* stages = gsm2;                                    // [2][SZ] (block-major sub-tiles)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + 2 * SZ);
+  const int a0 = 0, a1 = na > 0 ? b.off[na] : W;
+  const int b0 = na > 0 ? b.off[na] : 0, b1 = W;
+  const int wa = a1 - a0, wb = b1 - b0;
+  const int nbA = (wa + TBK - 1) / TBK, nbB = (wb + TBK - 1) / TBK;
+  const int ntiles = nbA * nbB;
+  const int RG = ntiles >= (int)blockDim.x ? 1 : (int)blockDim.x / ntiles;
+  const int grp = RG > 1 ? (int)threadIdx.x / ntiles : 0;
+  const int tslot = RG > 1 ? (int)threadIdx.x % ntiles : (int)threadIdx.x;
+  const bool in_range = RG > 1 ? (int)threadIdx.x < RG * ntiles : true;
+  const long long half = N / 2;
+  bool any_js = false;
+  for (int i = 0; i < b.nb; ++i) any_js |= b.jswap[i] != 0;
+  const long long lo = row_start(blockIdx.x, N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, N, gridDim.x);
+  const int nt = (int)((hi - lo + GT2 - 1) / GT2);
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int t) {            // thread 0 only
+    const long long r0 = lo + (long long)t * GT2;
+    const int rows = (int)min((long long)GT2, hi - r0);
+    double* st = stages + (t & 1) * SZ;
+    uint32_t bytes = 0;
+    for (int i = 0; i < b.nb; ++i) bytes += (uint32_t)rows * b.w[i] * 8u;
+    if (any_js) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the smem negation pass
+    mbar_expect_tx(&full[t & 1], bytes);
+    for (int i = 0; i < b.nb; ++i) {
+      double* dst = st + GT2 * b.off[i];
+      const int w = b.w[i];
+      if (!b.jswap[i]) {
+        bulk_g2s(dst, b.ptr[i] + (size_t)r0 * w, (uint32_t)rows * w * 8u, &full[t & 1]);
+      } else {   // rows r < half read r + half, rows r >= half read r - half
+        const long long m = min(r0 + rows, max(r0, half));       // split point
+        if (m > r0)
+          bulk_g2s(dst, b.ptr[i] + (size_t)(r0 + half) * w, (uint32_t)(m - r0) * w * 8u, &full[t & 1]);
+        if (r0 + rows > m)
+          bulk_g2s(dst + (m - r0) * w, b.ptr[i] + (size_t)(m - half) * w,
+                   (uint32_t)(r0 + rows - m) * w * 8u, &full[t & 1]);
+      }
+    }
+  };
+  double acc[MAXT][TBK][TBK];
+#pragma unroll
+  for (int s = 0; s < MAXT; ++s)
+#pragma unroll
+    for (int i = 0; i < TBK; ++i)
+#pragma unroll
+      for (int j = 0; j < TBK; ++j) acc[s][i][j] = 0.0;
+  if (threadIdx.x == 0 && nt > 0) issue(0);
+  for (int t = 0; t < nt; ++t) {
+    const long long r0 = lo + (long long)t * GT2;
+    const int rows = (int)min((long long)GT2, hi - r0);
+    if (threadIdx.x == 0 && t + 1 < nt) issue(t + 1);   // stage (t+1)&1 was released at the end of t-1
+    mbar_wait(&full[t & 1], (uint32_t)((t >> 1) & 1));
+    double* st = stages + (t & 1) * SZ;
+    if (any_js && r0 + rows > half) {      // J: negate the new lower half of swapped blocks
+      for (int i = 0; i < b.nb; ++i) {
+        if (!b.jswap[i]) continue;
+        const int w = b.w[i];
+        const int first = (int)max(0LL, half - r0);
+        for (int q = threadIdx.x; q < (rows - first) * w; q += blockDim.x)
+          st[GT2 * b.off[i] + first * w + q] = -st[GT2 * b.off[i] + first * w + q];
+      }
+      __syncthreads();
+    }
+    if (in_range) {
+#pragma unroll
+      for (int s = 0; s < MAXT; ++s) {
+        const int tt = tslot + s * blockDim.x;
+        if (tt >= ntiles) break;
+        const int bi = tt / nbB, bj = tt % nbB;
+        // smem (offset, stride) of the thread's A and B columns
+        int ao[TBK], as_[TBK], bo[TBK], bs[TBK];
+#pragma unroll
+        for (int i = 0; i < TBK; ++i) {
+          const int ca = a0 + min(bi * TBK + i, wa - 1), cb = b0 + min(bj * TBK + i, wb - 1);
+          int ba = 0, bb = 0;
+          while (ca >= b.off[ba + 1]) ++ba;
+          while (cb >= b.off[bb + 1]) ++bb;
+          ao[i] = GT2 * b.off[ba] + (ca - b.off[ba]);
+          as_[i] = b.w[ba];
+          bo[i] = GT2 * b.off[bb] + (cb - b.off[bb]);
+          bs[i] = b.w[bb];
+        }
+        for (int rr = grp; rr < rows; rr += RG) {
+          double av[TBK], bv[TBK];
+#pragma unroll
+          for (int i = 0; i < TBK; ++i) {
+            av[i] = st[ao[i] + rr * as_[i]];
+            bv[i] = st[bo[i] + rr * bs[i]];
+          }
+#pragma unroll
+          for (int i = 0; i < TBK; ++i)
+#pragma unroll
+            for (int j = 0; j < TBK; ++j) acc[s][i][j] = fma(av[i], bv[j], acc[s][i][j]);
+        }
+      }
+    }
+    __syncthreads();                       // stage t&1 free for tile t+2
+  }
+  if (!in_range) return;
+  double* out = seg + ((size_t)blockIdx.x * RG + grp) * wa * wb;
+#pragma unroll
+  for (int s = 0; s < MAXT; ++s) {
+    const int tt = tslot + s * blockDim.x;
+    if (tt >= ntiles) break;
+    const int bi = tt / nbB, bj = tt % nbB;
+#pragma unroll
+    for (int i = 0; i < TBK; ++i)
+#pragma unroll
+      for (int j = 0; j < TBK; ++j) {
+        const int ci = bi * TBK + i, cj = bj * TBK + j;
+        if (ci < wa && cj < wb) out[(size_t)ci * wb + cj] = acc[s][i][j];
+      }
+  }
+}
+
 // first index of max |v[i*stride]| over i < n, skipping `banned` (numpy
 // argmax tie rule: the smallest index among equal maxima); banned entries
 // score -1 as in hyper.py:241-243.  Two passes: per-CTA (value, index), then
@@ -561,6 +696,99 @@ __global__ void __launch_bounds__(256) combine_kernel(Terms t, const double* mat
 #pragma unroll
   for (int k = 0; k < NMAX; ++k)
     if (k < t.c) o[k] = t.accumulate ? o[k] + acc[k] : acc[k];
+}
+
+// TMA-staged combine: out (rows x c) (+)= sum_t op_t(in_t) M_t.  Row tiles of
+// every input land in smem via cp.async.bulk (double-buffered, mbarriers);
+// 4 threads per row each produce ceil(c/4) outputs; M_t live in smem.
+constexpr int CR = 64;     // rows per tile
+
+template <int CPT>
+__global__ void __launch_bounds__(256) combine_tma_kernel(Terms t, const double* mats, int mats_len,
+                                                          long long N) {
+  extern __shared__ __align__(128) double csm[];
+  int wsum = 0;
+  int soff[MAXTERM];
+  for (int s = 0; s < t.nt; ++s) { soff[s] = CR * wsum; wsum += t.a[s]; }
+  const int SZ = CR * wsum;
+  double* stages = csm;                                  // [2][SZ]
+  double* ms = stages + 2 * SZ;                          // mats
+  uint64_t* full = reinterpret_cast<uint64_t*>(ms + ((mats_len + 1) & ~1));
+  for (int q = threadIdx.x; q < mats_len; q += blockDim.x) ms[q] = mats[q];
+  const long long half = N / 2;
+  bool any_js = false;
+  for (int s = 0; s < t.nt; ++s) any_js |= t.jswap[s] != 0;
+  const long long lo = row_start(blockIdx.x, N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, N, gridDim.x);
+  const int ntl = (int)((hi - lo + CR - 1) / CR);
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int k) {
+    const long long r0 = lo + (long long)k * CR;
+    const int rows = (int)min((long long)CR, hi - r0);
+    double* st = stages + (k & 1) * SZ;
+    if (any_js) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&full[k & 1], (uint32_t)rows * wsum * 8u);
+    for (int s = 0; s < t.nt; ++s) {
+      const int w = t.a[s];
+      double* dst = st + soff[s];
+      if (!t.jswap[s]) {
+        bulk_g2s(dst, t.in[s] + (size_t)r0 * w, (uint32_t)rows * w * 8u, &full[k & 1]);
+      } else {
+        const long long m = min(r0 + rows, max(r0, half));
+        if (m > r0) bulk_g2s(dst, t.in[s] + (size_t)(r0 + half) * w, (uint32_t)(m - r0) * w * 8u, &full[k & 1]);
+        if (r0 + rows > m)
+          bulk_g2s(dst + (m - r0) * w, t.in[s] + (size_t)(m - half) * w, (uint32_t)(r0 + rows - m) * w * 8u,
+                   &full[k & 1]);
+      }
+    }
+  };
+  const int row_l = threadIdx.x >> 2, q = threadIdx.x & 3;
+  const int c0 = q * CPT;
+  if (threadIdx.x == 0 && ntl > 0) issue(0);
+  for (int k = 0; k < ntl; ++k) {
+    const long long r0 = lo + (long long)k * CR;
+    const int rows = (int)min((long long)CR, hi - r0);
+    if (threadIdx.x == 0 && k + 1 < ntl) issue(k + 1);
+    mbar_wait(&full[k & 1], (uint32_t)((k >> 1) & 1));
+    double* st = stages + (k & 1) * SZ;
+    if (any_js && r0 + rows > half) {
+      const int first = (int)max(0LL, half - r0);
+      for (int s = 0; s < t.nt; ++s) {
+        if (!t.jswap[s]) continue;
+        const int w = t.a[s];
+        for (int e = threadIdx.x; e < (rows - first) * w; e += blockDim.x)
+          st[soff[s] + first * w + e] = -st[soff[s] + first * w + e];
+      }
+      __syncthreads();
+    }
+    if (row_l < rows && c0 < t.c) {
+      double acc[CPT];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) acc[j] = 0.0;
+      for (int s = 0; s < t.nt; ++s) {
+        const int w = t.a[s];
+        const double* xr = st + soff[s] + row_l * w;
+        const double* M = ms + t.moff[s] + c0;
+        for (int kk = 0; kk < w; ++kk) {
+          const double v = xr[kk];
+          const double* mr = M + kk * t.c;
+#pragma unroll
+          for (int j = 0; j < CPT; ++j)
+            if (c0 + j < t.c) acc[j] = fma(v, mr[j], acc[j]);
+        }
+      }
+      double* o = t.out + (size_t)(r0 + row_l) * t.ldo + c0;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j)
+        if (c0 + j < t.c) o[j] = t.accumulate ? o[j] + acc[j] : acc[j];
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void rows_gather_kernel(const double* src, int ld, const long long* idx, int d, int w,
@@ -793,10 +1021,28 @@ static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* 
   const int G = gram_grid(N);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t sm = (size_t)2 * GTR * W * sizeof(double) + (size_t)W * (sizeof(void*) + 2 * sizeof(int));
+  // TMA staging when every block is row-contiguous (ld == width) and 16-B aligned
+  bool tma = getenv("PICROM_GRAM_NO_TMA") == nullptr;
+  for (int i = 0; i < nblocks && tma; ++i)
+    tma = lds[i] == widths[i] && ((widths[i] * 8) % 16 == 0) &&
+          ((reinterpret_cast<uintptr_t>(ptrs[i]) & 15) == 0);
+  const size_t sm_tma = (size_t)2 * GT2 * W * sizeof(double) + 2 * sizeof(uint64_t);
+  if (tma && sm_tma > 200 * 1024) tma = false;
   // 8x8 register tiles when the output has <= 256 of them, else 4x4
   const int t8 = ((wa + 7) / 8) * ((wb + 7) / 8);
   int RG;
-  if (t8 <= 256) {
+  if (tma) {
+    if (t8 <= 256) {
+      RG = t8 >= 256 ? 1 : 256 / t8;
+      rom_allow_smem(gram_tma_kernel<8, 1>);
+      gram_tma_kernel<8, 1><<<G, 256, sm_tma, s>>>(b, na, N, (double*)ws);
+    } else {
+      const int t4 = ((wa + 3) / 4) * ((wb + 3) / 4);
+      RG = t4 >= 256 ? 1 : 256 / t4;
+      rom_allow_smem(gram_tma_kernel<4, 4>);
+      gram_tma_kernel<4, 4><<<G, 256, sm_tma, s>>>(b, na, N, (double*)ws);
+    }
+  } else if (t8 <= 256) {
     RG = t8 >= 256 ? 1 : 256 / t8;
     rom_allow_smem(gram_kernel<8, 1>);
     gram_kernel<8, 1><<<G, 256, sm, s>>>(b, na, N, (double*)ws);
@@ -861,9 +1107,29 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
   const size_t sm = (size_t)mats_len * sizeof(double);
   if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
   cudaStream_t s = (cudaStream_t)stream;
+  // TMA path: row-contiguous, 16-B aligned inputs
+  bool tma = getenv("PICROM_COMBINE_NO_TMA") == nullptr;
+  int wsum = 0;
+  for (int i = 0; i < nterms && tma; ++i) {
+    tma = lds[i] == widths[i] && ((widths[i] * 8) % 16 == 0) &&
+          ((reinterpret_cast<uintptr_t>(ins[i]) & 15) == 0);
+    wsum += widths[i];
+  }
+  const size_t sm_tma = (size_t)2 * CR * wsum * sizeof(double) + (size_t)((mats_len + 1) & ~1) * sizeof(double) +
+                        2 * sizeof(uint64_t);
+  if (tma && sm_tma <= 200 * 1024) {
+    const int G = (int)std::min<long long>(2LL * picrom_num_sms(), std::max<long long>(1, (N + CR - 1) / CR));
+    const int cpt = (c + 3) / 4;
+    if (cpt <= 2) { rom_allow_smem(combine_tma_kernel<2>); combine_tma_kernel<2><<<G, 256, sm_tma, s>>>(t, mats, mats_len, N); }
+    else if (cpt <= 4) { rom_allow_smem(combine_tma_kernel<4>); combine_tma_kernel<4><<<G, 256, sm_tma, s>>>(t, mats, mats_len, N); }
+    else if (cpt <= 6) { rom_allow_smem(combine_tma_kernel<6>); combine_tma_kernel<6><<<G, 256, sm_tma, s>>>(t, mats, mats_len, N); }
+    else { rom_allow_smem(combine_tma_kernel<8>); combine_tma_kernel<8><<<G, 256, sm_tma, s>>>(t, mats, mats_len, N); }
+    return picrom_check_launch("combine_tma_kernel");
+  }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+      (void)cudaGetLastError();
     attr = true;
   }
   const unsigned blocks = (unsigned)((N + 255) / 256);
