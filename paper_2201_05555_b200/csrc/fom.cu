@@ -263,11 +263,21 @@ struct SolveArgs {
   int seg_chunks;           // > 0: chunk-mode segment rows [j*seg_chunks, (j+1)*seg_chunks)
   long long hist_mod;       // > 0: history row = counter % hist_mod (ring)
   const int* cols;          // optional instance id per column
+  size_t scratch;           // solve_kernel: dynamic smem in doubles
 };
 
 // sum of cnt values v[0], v[stride], ... with 8 independent loads in flight,
 // combined in a fixed order (deterministic)
 __device__ __forceinline__ double ordered_sum(const double* v, size_t stride, int cnt) {
+  if (cnt <= 16) {   // common case: every load in flight at once, same sum order
+    double t[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) t[u] = u < cnt ? v[(size_t)u * stride] : 0.0;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = t[u] + t[u + 8];
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  }
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int b = 0;
   for (; b + 8 <= cnt; b += 8) {
@@ -278,16 +288,34 @@ __device__ __forceinline__ double ordered_sum(const double* v, size_t stride, in
   return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 }
 
-// One instance's assembly + solve by a whole CTA; `sm` holds 4 nx + 32
-// doubles; `ntickets` = how many instance solves make up this step (the last
-// one to finish advances the step counter).
-__device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int ntickets) {
+// smem (doubles) the solve needs with mp partial rows; khat is stored with
+// one pad slot per 4 entries so the circulant's strided window loads are
+// bank-conflict free
+__host__ __device__ inline int solve_kh_len(int nx) { return nx + nx / 4 + 4; }
+__host__ __device__ inline size_t solve_scratch(int nx, int mp) {
+  return (size_t)nx + solve_kh_len(nx) + 40 + (size_t)mp * nx;
+}
+__host__ __device__ inline int solve_mp(int nx, int threads, size_t avail) {
+  const int og = (nx + 127) / 128;
+  int mp = (threads / 32) / og;
+  while (mp > 1 && solve_scratch(nx, mp) > avail) --mp;
+  return mp < 1 ? 1 : mp;
+}
+__device__ __forceinline__ int kh_pad(int r) { return r + (r >> 2); }
+
+// One instance's assembly + solve by a whole CTA; `sm` holds `avail`
+// doubles (>= solve_scratch(nx, 1)); `ntickets` = how many instance solves
+// make up this step (the last one to finish advances the step counter).
+__device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int ntickets,
+                           size_t avail) {
   const int nx = a.nx;
-  double* rho = sm;            // nx
-  double* kh = rho + nx;       // 2 nx (khat repeated)
-  double* phi = kh + 2 * nx;   // nx
-  double* red = phi + nx;      // 32 (block reductions) + 8 (stencil)
+  double* rho = sm;                      // nx (phi overwrites it after the circulant)
+  double* kh = rho + nx;                 // khat, padded (kh_pad)
+  double* red = kh + solve_kh_len(nx);   // 32 (block reductions) + 8 (stencil)
   double* stn = red + 32;
+  double* prow = red + 40;               // mp x nx circulant partial rows
+  double* phi = rho;
+  const int mp = solve_mp(nx, blockDim.x, avail);
   const int tid = threadIdx.x;
   if (a.stencil && tid <= a.degree) stn[tid] = a.stencil[tid];
   const double* ip = a.inst + (size_t)(a.cols ? a.cols[j] : j) * PICROM_INST_STRIDE;
@@ -329,7 +357,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
     for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] = a.rho_in[(size_t)j * nx + nd];
   }
   if (a.solve)
-    for (int r = tid; r < 2 * nx; r += blockDim.x) kh[r] = a.khat[r < nx ? r : r - nx];
+    for (int r = tid; r < nx; r += blockDim.x) kh[kh_pad(r)] = a.khat[r];
   __syncthreads();
   if (rho_out)
     for (int nd = tid; nd < nx; nd += blockDim.x) rho_out[(size_t)j * nx + nd] = rho[nd];
@@ -341,22 +369,61 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   const double mean_rho = block_sum(part, red) / (double)nx;
   for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] -= mean_rho;
   __syncthreads();
-  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m; kh holds khat
-  // twice (kh[r] = khat[r mod nx], r < 2 nx) so the inner loop has no modulo,
-  // and 4 independent partial sums keep the FMA pipe busy (fixed order)
+  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m.  A lane owns
+  // 4 consecutive outputs and keeps khat[(n0 + i - m) mod nx], i < 4, in a
+  // register window that slides by one smem load per step of m (1 load per
+  // 4 FMAs); warps split the m range into mp parts, summed in fixed order.
+  {
+    const int nw = blockDim.x >> 5, warp = tid >> 5, lane = tid & 31;
+    const int og = (nx + 127) >> 7;
+    const int mlen = (nx + mp - 1) / mp;
+    for (int t = warp; t < og * mp; t += nw) {
+      const int q = t / og;
+      const int n0 = (t - q * og) * 128 + lane * 4;
+      const int mlo = q * mlen, mhi = min(nx, mlo + mlen);
+      if (n0 >= nx || mlo >= mhi) continue;
+      int idx = n0 - mlo;                     // (n0 - m) mod nx at m = mlo
+      if (idx < 0) idx += nx;
+      auto up = [nx](int r) { r += 1; return r >= nx ? r - nx : r; };
+      auto dn = [nx](int r) { r -= 1; return r < 0 ? r + nx : r; };
+      const int i1 = up(idx), i2 = up(i1), i3 = up(i2);
+      double w0 = kh[kh_pad(idx)], w1 = kh[kh_pad(i1)], w2 = kh[kh_pad(i2)], w3 = kh[kh_pad(i3)];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int m = mlo;
+      for (; m + 4 <= mhi; m += 4) {
+        const double b0 = rho[m], b1 = rho[m + 1], b2 = rho[m + 2], b3 = rho[m + 3];
+        a0 = fma(w0, b0, a0); a1 = fma(w1, b0, a1); a2 = fma(w2, b0, a2); a3 = fma(w3, b0, a3);
+        idx = dn(idx);
+        const double x = kh[kh_pad(idx)];
+        a0 = fma(x, b1, a0); a1 = fma(w0, b1, a1); a2 = fma(w1, b1, a2); a3 = fma(w2, b1, a3);
+        idx = dn(idx);
+        const double y = kh[kh_pad(idx)];
+        a0 = fma(y, b2, a0); a1 = fma(x, b2, a1); a2 = fma(w0, b2, a2); a3 = fma(w1, b2, a3);
+        idx = dn(idx);
+        const double z = kh[kh_pad(idx)];
+        a0 = fma(z, b3, a0); a1 = fma(y, b3, a1); a2 = fma(x, b3, a2); a3 = fma(w0, b3, a3);
+        idx = dn(idx);
+        w3 = x; w2 = y; w1 = z; w0 = kh[kh_pad(idx)];
+      }
+      for (; m < mhi; ++m) {
+        const double b0 = rho[m];
+        a0 = fma(w0, b0, a0); a1 = fma(w1, b0, a1); a2 = fma(w2, b0, a2); a3 = fma(w3, b0, a3);
+        idx = dn(idx);
+        w3 = w2; w2 = w1; w1 = w0; w0 = kh[kh_pad(idx)];
+      }
+      double* pr = prow + (size_t)q * nx + n0;
+      pr[0] = a0;
+      if (n0 + 1 < nx) pr[1] = a1;
+      if (n0 + 2 < nx) pr[2] = a2;
+      if (n0 + 3 < nx) pr[3] = a3;
+    }
+  }
+  __syncthreads();
   part = 0.0;
   for (int nd = tid; nd < nx; nd += blockDim.x) {
-    const double* kr = kh + nd + nx;     // kr[-m] = khat[(nd - m) mod nx]
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int m = 0;
-    for (; m + 4 <= nx; m += 4) {
-      s0 = fma(kr[-m], rho[m], s0);
-      s1 = fma(kr[-m - 1], rho[m + 1], s1);
-      s2 = fma(kr[-m - 2], rho[m + 2], s2);
-      s3 = fma(kr[-m - 3], rho[m + 3], s3);
-    }
-    for (; m < nx; ++m) s0 = fma(kr[-m], rho[m], s0);
-    phi[nd] = h * ((s0 + s1) + (s2 + s3));
+    double sum = prow[nd];
+    for (int q = 1; q < mp; ++q) sum += prow[(size_t)q * nx + nd];
+    phi[nd] = h * sum;
     part += phi[nd];
   }
   const double mean_phi = block_sum(part, red) / (double)nx;
@@ -400,7 +467,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
 
 __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   extern __shared__ double sm[];
-  solve_body(a, blockIdx.x, sm, gridDim.x);
+  solve_body(a, blockIdx.x, sm, gridDim.x, a.scratch);
 }
 
 #ifndef PICROM_STEP_U
@@ -613,15 +680,15 @@ step_kernel(StepArgs a, SolveArgs sa) {
         } else {
           Spline<D>::weights(fr[u], w);
         }
-        const int row = cl[u] * H + myh;
 #pragma unroll
         for (int q = 0; q < K; ++q) {
           if (ok[u] && klane == q) {
+            double* hp = hist + cl[u] * H + myh;
             double cur[NW];
 #pragma unroll
-            for (int m = 0; m < NW; ++m) cur[m] = hist[row + m * H];
+            for (int m = 0; m < NW; ++m) cur[m] = hp[m * H];
 #pragma unroll
-            for (int m = 0; m < NW; ++m) hist[row + m * H] = cur[m] + w[m];
+            for (int m = 0; m < NW; ++m) hp[m * H] = cur[m] + w[m];
           }
           if constexpr (K > 1) __syncwarp();
         }
@@ -681,9 +748,11 @@ step_kernel(StepArgs a, SolveArgs sa) {
           if (s_last) a.inst_done[j] = 0u;
         }
         __syncthreads();
-        if (s_last) {
+        if (s_last && a.fuse_solve == 1) {
           __threadfence();
-          solve_body(sa, j, hist, (unsigned int)a.p);   // scratch = histogram smem only
+          // scratch = the histogram, coefficient and reduction smem (free now)
+          solve_body(sa, j, hist, (unsigned int)a.p,
+                     (size_t)nh * H + (MODE == MODE_LEAPFROG ? (size_t)nx * D : 0) + 64);
         }
       }
     }
@@ -1020,12 +1089,15 @@ static int launch_tma(const StepArgs& a, int degree, const TmaCfg& c, int G, cud
   }
 }
 
-static int launch_solve(const SolveArgs& a, cudaStream_t s) {
+static int launch_solve(const SolveArgs& a_in, cudaStream_t s) {
+  SolveArgs a = a_in;
   int threads = std::min(512, std::max(64, ((a.nx + 31) / 32) * 32));
-  size_t sm = (4 * (size_t)a.nx + 40) * sizeof(double);
+  const int mp = solve_mp(a.nx, threads, (size_t)1 << 40);
+  a.scratch = solve_scratch(a.nx, mp);
+  size_t sm = a.scratch * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    allow_max_dynamic_smem(solve_kernel);
     attr = true;
   }
   solve_kernel<<<a.p, threads, sm, s>>>(a);
@@ -1308,14 +1380,16 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
   a.x = x; a.v = v; a.phi = phi; a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx;
   a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
   a.counter = counter;
-  static int nosolve = -1;     // timing experiment only: PICROM_NOSOLVE=1 drops the solve
-  if (nosolve < 0) { const char* s = getenv("PICROM_NOSOLVE"); nosolve = (s && atoi(s)) ? 1 : 0; }
-  a.fuse_solve = nosolve ? 0 : 1;
+  // timing experiments only: PICROM_NOSOLVE=1 drops the solve, =2 keeps the
+  // tickets but not the solve, =3 solves without the circulant/energy
+  static int nosolve = -1;
+  if (nosolve < 0) { const char* s = getenv("PICROM_NOSOLVE"); nosolve = s ? atoi(s) : 0; }
+  a.fuse_solve = nosolve == 1 ? 0 : (nosolve == 2 ? 2 : 1);
   ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.seg_kin = a.seg_kin; sa.inst = inst; sa.khat = khat;
   sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc;
-  sa.solve = true; sa.phi_out = phi;
+  sa.solve = nosolve != 3; sa.phi_out = phi;
   const size_t gp = (size_t)p * nx;
   sa.hist_stride_rho = gp;
   sa.hist_stride_e = (size_t)p;

@@ -60,7 +60,10 @@ __device__ __forceinline__ long long row_start(int b, long long N, int G) {
 
 template <typename F>
 static void rom_allow_smem(F kfn) {
-  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+  cudaFuncAttributes at{};
+  cudaFuncGetAttributes(&at, kfn);
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024 - (int)at.sharedSizeBytes) != cudaSuccess)
     (void)cudaGetLastError();
 }
 
@@ -107,7 +110,7 @@ __device__ __forceinline__ double row_dot(const double* urow, const double* zc, 
 // private histogram [row][tid] (conflict-free); U_X rows stream through a
 // double-buffered smem tile shared by all columns of the CTA.
 template <int D, int NB, int R>
-__global__ void __launch_bounds__(256) rom_deposit_kernel(RomArgs a) {
+__global__ void __launch_bounds__(384) rom_deposit_kernel(RomArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int P = blockDim.x / R;               // columns per row group (mult of 32)
   const int H = blockDim.x;
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(256) rom_deposit_kernel(RomArgs a) {
 // Reconstruct + field gather + projection U_X^T E (+ optional DEIM harvest
 // lam and E output), same tiling; phi of the CTA's columns in smem [node][col].
 template <int D, int NB, int R>
-__global__ void __launch_bounds__(256) rom_gather_kernel(RomArgs a) {
+__global__ void __launch_bounds__(384) rom_gather_kernel(RomArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int P = blockDim.x / R;
   const int tid = threadIdx.x;
@@ -345,7 +348,6 @@ __device__ __forceinline__ long long jrow(long long i, long long half, double& s
   return i - half;
 }
 
-constexpr int GT = 16;     // rows per smem tile
 constexpr int TB = 4;      // output sub-block per thread
 
 // out = A^T B with A = blocks [0, na), B = blocks [na, nb) (na == 0: W^T W over
@@ -888,23 +890,25 @@ extern "C" size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx) 
   return std::max(std::max(dep, gat), gram) * sizeof(double) + 256;
 }
 
+// Row groups R (threads = R x P): as many as the per-column histograms
+// (deposit) or phi + partials (gather) leave room for, up to 384 threads
+// (one CTA per SM, 12 warps at C3); measured latency-bound, so warps matter.
 template <int D, int NB>
 static int launch_rom_deposit_nb(const RomArgs& a, int G, cudaStream_t s) {
   const int tiles = (a.p + PT - 1) / PT;
   const int P = std::min(PT, ((std::min(a.p, PT) + 31) / 32) * 32);
-  int R = std::max(1, std::min(256 / P, 2));
+  int R = std::max(1, std::min(384 / P, 4));
   auto smem = [&](int rr) {
     return (size_t)2 * TR * a.n * sizeof(double) + (size_t)(a.nx + D) * (rr * P) * sizeof(double);
   };
-  while (R > 1 && smem(R) > 200 * 1024) --R;
+  while (R > 1 && smem(R) > 220 * 1024) --R;
   if (smem(R) > 227 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "rom deposit: nx too large");
   dim3 grid(G, tiles);
-  if (R == 2) {
-    rom_allow_smem(rom_deposit_kernel<D, NB, 2>);
-    rom_deposit_kernel<D, NB, 2><<<grid, 2 * P, smem(2), s>>>(a);
-  } else {
-    rom_allow_smem(rom_deposit_kernel<D, NB, 1>);
-    rom_deposit_kernel<D, NB, 1><<<grid, P, smem(1), s>>>(a);
+  switch (R) {
+    case 1: rom_allow_smem(rom_deposit_kernel<D, NB, 1>); rom_deposit_kernel<D, NB, 1><<<grid, P, smem(1), s>>>(a); break;
+    case 2: rom_allow_smem(rom_deposit_kernel<D, NB, 2>); rom_deposit_kernel<D, NB, 2><<<grid, 2 * P, smem(2), s>>>(a); break;
+    case 3: rom_allow_smem(rom_deposit_kernel<D, NB, 3>); rom_deposit_kernel<D, NB, 3><<<grid, 3 * P, smem(3), s>>>(a); break;
+    default: rom_allow_smem(rom_deposit_kernel<D, NB, 4>); rom_deposit_kernel<D, NB, 4><<<grid, 4 * P, smem(4), s>>>(a); break;
   }
   return picrom_check_launch("rom_deposit_kernel");
 }
@@ -913,13 +917,18 @@ template <int D, int NB>
 static int launch_rom_gather_nb(const RomArgs& a, int G, cudaStream_t s) {
   const int tiles = (a.p + PT - 1) / PT;
   const int P = std::min(PT, ((std::min(a.p, PT) + 31) / 32) * 32);
-  const int R = std::max(1, std::min(256 / P, 4));
-  const size_t sm = ((size_t)2 * TR * a.n + (size_t)a.nx * P + (size_t)R * P * a.n) * sizeof(double);
+  int R = std::max(1, std::min(384 / P, 4));
+  auto smem = [&](int rr) {
+    return ((size_t)2 * TR * a.n + (size_t)a.nx * P + (size_t)rr * P * a.n) * sizeof(double);
+  };
+  while (R > 1 && smem(R) > 220 * 1024) --R;
+  const size_t sm = smem(R);
   if (sm > 227 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "rom gather: nx too large");
   dim3 grid(G, tiles);
   switch (R) {
     case 1: rom_allow_smem(rom_gather_kernel<D, NB, 1>); rom_gather_kernel<D, NB, 1><<<grid, P, sm, s>>>(a); break;
     case 2: rom_allow_smem(rom_gather_kernel<D, NB, 2>); rom_gather_kernel<D, NB, 2><<<grid, 2 * P, sm, s>>>(a); break;
+    case 3: rom_allow_smem(rom_gather_kernel<D, NB, 3>); rom_gather_kernel<D, NB, 3><<<grid, 3 * P, sm, s>>>(a); break;
     default: rom_allow_smem(rom_gather_kernel<D, NB, 4>); rom_gather_kernel<D, NB, 4><<<grid, 4 * P, sm, s>>>(a); break;
   }
   return picrom_check_launch("rom_gather_kernel");
