@@ -602,6 +602,172 @@ __global__ void __launch_bounds__(256) gram_tma_kernel(Blocks b, int na, long lo
   }
 }
 
+// ---- FP64 tensor-core (DMMA) Gram: mma.sync.m8n8k4 f64 ----
+//
+// D (8x8) += A (8x4) B (4x8), one f64 per lane for A and B, two for D:
+// A[l>>2][l&3], B[l&3][l>>2], D[l>>2][2(l&3) + e].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+constexpr int MAXTASK = 64;
+struct GramTasks {             // block pairs (bi, bj) of the output, TPC per CTA group
+  int ntask;
+  unsigned char bi[MAXTASK], bj[MAXTASK];
+};
+
+// All blocks wdt (<= 32) wide, row-contiguous, 16-B aligned.  Grid: x = task
+// group (TPC block pairs), y = row chunk.  A CTA stages only the blocks its
+// tasks read (TMA bulk copies, 2 stages of GT rows, mbarriers); its 8 warps
+// split the 4-row k-steps and each accumulates every task's TB x TB tiles of
+// 8x8 in DMMA fragments; warps are summed in a fixed order in smem and the
+// CTA writes its entries of row-chunk slot y (seg[y][wa][wb]).
+template <int TB, int TPC>
+__global__ void __launch_bounds__(256, 2)
+gram_mma_kernel(Blocks b, GramTasks tk, int na, long long N, int GT, int wn, double* seg) {
+  extern __shared__ __align__(128) double msm[];
+  __shared__ int s_loc[MAXB];
+  const int wdt = b.w[0];
+  const int W = b.off[b.nb];
+  const int b0 = na > 0 ? b.off[na] : 0;
+  const int wa = na > 0 ? b.off[na] : W, wb = na > 0 ? W - b0 : W;
+  const int t_lo = blockIdx.x * TPC;
+  const int t_n = min(TPC, tk.ntask - t_lo);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    unsigned need = 0;
+    for (int t = 0; t < t_n; ++t) need |= (1u << tk.bi[t_lo + t]) | (1u << tk.bj[t_lo + t]);
+    int loc = 0;
+    for (int i = 0; i < b.nb; ++i) {
+      s_loc[i] = (need >> i) & 1u ? loc : -1;
+      if ((need >> i) & 1u) loc += wdt;
+    }
+  }
+  const int SZ = GT * wn;
+  double* stages = msm;                                      // [2][GT][wn] block-major
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + 2 * SZ);
+  double* red = reinterpret_cast<double*>(full + 2);         // [TPC][TB][TB][64]
+  const long long half = N / 2;
+  const long long lo = row_start(blockIdx.y, N, gridDim.y);
+  const long long hi = row_start(blockIdx.y + 1, N, gridDim.y);
+  const int nt = (int)((hi - lo + GT - 1) / GT);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  bool any_js = false;
+  for (int i = 0; i < b.nb; ++i) any_js |= (b.jswap[i] != 0 && s_loc[i] >= 0);
+  auto issue = [&](int t) {            // thread 0 only
+    const long long r0 = lo + (long long)t * GT;
+    const int rows = (int)min((long long)GT, hi - r0);
+    double* st = stages + (t & 1) * SZ;
+    uint32_t bytes = 0;
+    for (int i = 0; i < b.nb; ++i)
+      if (s_loc[i] >= 0) bytes += (uint32_t)rows * wdt * 8u;
+    if (any_js) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&full[t & 1], bytes);
+    for (int i = 0; i < b.nb; ++i) {
+      if (s_loc[i] < 0) continue;
+      double* dst = st + GT * s_loc[i];
+      if (!b.jswap[i]) {
+        bulk_g2s(dst, b.ptr[i] + (size_t)r0 * wdt, (uint32_t)rows * wdt * 8u, &full[t & 1]);
+      } else {
+        const long long m = min(r0 + rows, max(r0, half));
+        if (m > r0)
+          bulk_g2s(dst, b.ptr[i] + (size_t)(r0 + half) * wdt, (uint32_t)(m - r0) * wdt * 8u, &full[t & 1]);
+        if (r0 + rows > m)
+          bulk_g2s(dst + (m - r0) * wdt, b.ptr[i] + (size_t)(m - half) * wdt,
+                   (uint32_t)(r0 + rows - m) * wdt * 8u, &full[t & 1]);
+      }
+    }
+  };
+  double acc[TPC][TB][TB][2];
+#pragma unroll
+  for (int t = 0; t < TPC; ++t)
+#pragma unroll
+    for (int i = 0; i < TB; ++i)
+#pragma unroll
+      for (int j = 0; j < TB; ++j) acc[t][i][j][0] = acc[t][i][j][1] = 0.0;
+  // the lane's column inside an 8-wide tile, and its row inside a k-step
+  const int lc = lane >> 2, lr = lane & 3;
+  if (tid == 0 && nt > 0) issue(0);
+  for (int t = 0; t < nt; ++t) {
+    const long long r0 = lo + (long long)t * GT;
+    const int rows = (int)min((long long)GT, hi - r0);
+    if (tid == 0 && t + 1 < nt) issue(t + 1);
+    mbar_wait(&full[t & 1], (uint32_t)((t >> 1) & 1));
+    double* st = stages + (t & 1) * SZ;
+    if (any_js && r0 + rows > half) {      // J: negate the new lower half of swapped blocks
+      for (int i = 0; i < b.nb; ++i) {
+        if (!b.jswap[i] || s_loc[i] < 0) continue;
+        const int first = (int)max(0LL, half - r0);
+        double* bl = st + GT * s_loc[i];
+        for (int q = tid; q < (rows - first) * wdt; q += blockDim.x)
+          bl[first * wdt + q] = -bl[first * wdt + q];
+      }
+      __syncthreads();
+    }
+    const int ksteps = (rows + 3) >> 2;
+    for (int kk = warp; kk < ksteps; kk += 8) {
+      const int r = kk * 4 + lr;
+      const bool rv = r < rows;
+#pragma unroll
+      for (int tt = 0; tt < TPC; ++tt) {
+        if (tt < t_n) {
+          const int bi = tk.bi[t_lo + tt], bj = tk.bj[t_lo + tt];
+          const double* pa = st + GT * s_loc[bi] + r * wdt;
+          const double* pb = st + GT * s_loc[bj] + r * wdt;
+          double fa[TB], fb[TB];
+#pragma unroll
+          for (int i = 0; i < TB; ++i) {
+            const int c = 8 * i + lc;
+            fa[i] = (rv && c < wdt) ? pa[c] : 0.0;
+            fb[i] = (rv && c < wdt) ? pb[c] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < TB; ++i)
+#pragma unroll
+            for (int j = 0; j < TB; ++j) dmma(acc[tt][i][j][0], acc[tt][i][j][1], fa[i], fb[j]);
+        }
+      }
+    }
+    __syncthreads();                       // stage t&1 free for tile t+2
+  }
+  // warps summed in a fixed order (warp 0 first)
+  constexpr int NACC = TPC * TB * TB * 64;
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int tt = 0; tt < TPC; ++tt)
+#pragma unroll
+        for (int i = 0; i < TB; ++i)
+#pragma unroll
+          for (int j = 0; j < TB; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double* q = red + ((tt * TB + i) * TB + j) * 64 + lane * 2 + e;
+              *q = (w == 0) ? acc[tt][i][j][e] : *q + acc[tt][i][j][e];
+            }
+    }
+    __syncthreads();
+  }
+  double* out = seg + (size_t)blockIdx.y * wa * wb;
+  for (int q = tid; q < t_n * TB * TB * 64; q += blockDim.x) {
+    const int e = q & 1, ln = (q >> 1) & 31, tile = q >> 6;
+    const int j = tile % TB, i = (tile / TB) % TB, tt = tile / (TB * TB);
+    const int bi = tk.bi[t_lo + tt], bj = tk.bj[t_lo + tt];
+    const int ri = 8 * i + (ln >> 2), cj = 8 * j + 2 * (ln & 3) + e;
+    if (ri >= wdt || cj >= wdt) continue;
+    const int row = b.off[bi] + ri, col = b.off[bj] - b0 + cj;
+    out[(size_t)row * wb + col] = red[q];
+    if (na == 0 && bi != bj) out[(size_t)col * wb + row] = red[q];
+  }
+  (void)NACC;
+}
+
 // first index of max |v[i*stride]| over i < n, skipping `banned` (numpy
 // argmax tie rule: the smallest index among equal maxima); banned entries
 // score -1 as in hyper.py:241-243.  Two passes: per-CTA (value, index), then
@@ -882,6 +1048,110 @@ int rom_grid(long long N) {
 
 // ------------------------------------------------------------------ C-ABI
 
+// ---- DMMA combine: out (N x c) (+)= sum_t op(in_t) M_t ----
+//
+// K = sum a_t (the terms' columns back to back) is the GEMM depth.  M (K x c)
+// sits in smem with pitch cp; the inputs stream through two cp.async stages
+// of 64 rows, term t at pitch pa_t (pa_t = 4 or 12 mod 16 doubles: the 8 x 4
+// A fragments then hit two wavefronts).  Warp w owns the 8-row tile w of a
+// stage; the J sign of a swapped term is applied at the fragment load.
+constexpr int CMR = 64;   // rows per stage
+
+struct MmaTerms {
+  int koff[MAXTERM + 1];  // first GEMM row of term t in M
+  int soff[MAXTERM + 1];  // offset of term t in a stage (doubles per row of the stage)
+  int pa[MAXTERM];        // smem pitch of term t
+  int cp;                 // smem pitch of M
+};
+
+__device__ __forceinline__ void cp_async16z(void* smem_dst, const void* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+
+template <int TBO>
+__global__ void __launch_bounds__(256, 2)
+combine_mma_kernel(Terms t, MmaTerms mt, const double* mats, long long N) {
+  extern __shared__ __align__(16) double csm[];
+  const int K = mt.koff[t.nt];
+  const int cp = mt.cp;
+  double* ms = csm;                                   // [K + 4][cp] (+ 8 pad)
+  double* stg = ms + (size_t)(K + 4) * cp + 8;        // [2][CMR * soff[nt]]
+  const int SZ = CMR * mt.soff[t.nt];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = t.c;
+  for (int q = tid; q < (K + 4) * cp + 8; q += blockDim.x) {
+    const int k = q / cp, j = q - k * cp;
+    double v = 0.0;
+    if (k < K && j < c) {
+      int ti = 0;
+      while (k >= mt.koff[ti + 1]) ++ti;
+      v = mats[t.moff[ti] + (k - mt.koff[ti]) * c + j];
+    }
+    ms[q] = v;
+  }
+  const long long half = N / 2;
+  const long long lo = row_start(blockIdx.x, N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, N, gridDim.x);
+  const int nst = (int)((hi - lo + CMR - 1) / CMR);
+  auto stage = [&](int st) {
+    const long long r0 = lo + (long long)st * CMR;
+    const int rows = (int)min((long long)CMR, hi - r0);
+    double* dst = stg + (st & 1) * SZ;
+    for (int ti = 0; ti < t.nt; ++ti) {
+      const int ch = t.a[ti] >> 1;                    // 16-B chunks per row
+      double* d = dst + CMR * mt.soff[ti];
+      for (int q = tid; q < rows * ch; q += blockDim.x) {
+        const int rr = q / ch, k2 = q - rr * ch;
+        long long row = r0 + rr;
+        if (t.jswap[ti]) row = row < half ? row + half : row - half;
+        cp_async16z(d + rr * mt.pa[ti] + 2 * k2, t.in[ti] + (size_t)row * t.ld[ti] + 2 * k2);
+      }
+    }
+    cp_async_commit();
+  };
+  const int lr = lane >> 2, lk = lane & 3;
+  if (nst > 0) stage(0);
+  for (int st = 0; st < nst; ++st) {
+    const long long r0 = lo + (long long)st * CMR;
+    const int rows = (int)min((long long)CMR, hi - r0);
+    if (st + 1 < nst) { stage(st + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
+    __syncthreads();
+    const double* cur = stg + (st & 1) * SZ;
+    const int r = warp * 8 + lr;                      // A-fragment row of this lane
+    if (warp * 8 < rows) {
+      double acc[TBO][2];
+#pragma unroll
+      for (int j = 0; j < TBO; ++j) acc[j][0] = acc[j][1] = 0.0;
+      const bool rv = r < rows;
+      for (int ti = 0; ti < t.nt; ++ti) {
+        const double sg = (t.jswap[ti] && r0 + r >= half) ? -1.0 : 1.0;
+        const double* arow = cur + CMR * mt.soff[ti] + r * mt.pa[ti];
+        const double* mrow = ms + (size_t)mt.koff[ti] * cp + lr;
+        const int a = t.a[ti];
+        for (int k0 = 0; k0 < a; k0 += 4) {
+          const int kk = k0 + lk;
+          const double av = (rv && kk < a) ? sg * arow[kk] : 0.0;
+          const double* mk = mrow + (size_t)kk * cp;
+#pragma unroll
+          for (int j = 0; j < TBO; ++j) dmma(acc[j][0], acc[j][1], av, mk[8 * j]);
+        }
+      }
+      if (rv) {
+        double* orow = t.out + (size_t)(r0 + r) * t.ldo;
+#pragma unroll
+        for (int j = 0; j < TBO; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * j + 2 * lk + e;
+            if (col < c) orow[col] = t.accumulate ? orow[col] + acc[j][e] : acc[j][e];
+          }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 extern "C" size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx) {
   const size_t G = (size_t)rom_grid(N);
   const size_t dep = G * p * nx;
@@ -1011,6 +1281,62 @@ extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const dou
 }
 
 // Gram of the row-concatenation W = [B_0 | B_1 | ...] (N rows): out (w x w).
+// DMMA fast path of gram_impl: equal block widths <= 32, row-contiguous,
+// 16-B aligned, at least 1024 rows.  Returns -1 when not applicable.
+template <int TB, int TPC>
+static int launch_gram_mma(const Blocks& b, const GramTasks& tk, int na, long long N, int wdt,
+                           void* ws, cudaStream_t s, int* gy_out) {
+  const int ngroups = (tk.ntask + TPC - 1) / TPC;
+  int wn = 0;                       // widest needed set over the groups
+  for (int g = 0; g < ngroups; ++g) {
+    unsigned need = 0;
+    for (int t = g * TPC; t < std::min(tk.ntask, (g + 1) * TPC); ++t)
+      need |= (1u << tk.bi[t]) | (1u << tk.bj[t]);
+    wn = std::max(wn, __builtin_popcount(need) * wdt);
+  }
+  int GT = (40 * 1024 / (wn * 8)) / 32 * 32;
+  GT = std::max(32, std::min(256, GT));
+  const size_t sm = (size_t)2 * GT * wn * sizeof(double) + 2 * sizeof(uint64_t) +
+                    (size_t)TPC * TB * TB * 64 * sizeof(double);
+  const int gy = std::max(1, std::min(gram_grid(N), (4 * picrom_num_sms()) / ngroups));
+  static bool attr = false;
+  if (!attr) { rom_allow_smem(gram_mma_kernel<TB, TPC>); attr = true; }
+  gram_mma_kernel<TB, TPC><<<dim3(ngroups, gy), 256, sm, s>>>(b, tk, na, N, GT, wn, (double*)ws);
+  *gy_out = gy;
+  return picrom_check_launch("gram_mma_kernel");
+}
+
+static int gram_mma_try(const Blocks& b, int na, long long N, void* ws, cudaStream_t s,
+                        double* out) {
+  if (getenv("PICROM_GRAM_NO_MMA") || N < 1024) return -1;
+  const int wdt = b.w[0];
+  if (wdt > 32 || wdt < 2 || (wdt & 1)) return -1;
+  for (int i = 0; i < b.nb; ++i)
+    if (b.w[i] != wdt || b.ld[i] != wdt || (reinterpret_cast<uintptr_t>(b.ptr[i]) & 15)) return -1;
+  GramTasks tk{};
+  if (na == 0) {
+    for (int i = 0; i < b.nb; ++i)
+      for (int j = i; j < b.nb; ++j) { tk.bi[tk.ntask] = (unsigned char)i; tk.bj[tk.ntask] = (unsigned char)j; ++tk.ntask; }
+  } else {
+    for (int i = 0; i < na; ++i)
+      for (int j = na; j < b.nb; ++j) { tk.bi[tk.ntask] = (unsigned char)i; tk.bj[tk.ntask] = (unsigned char)j; ++tk.ntask; }
+  }
+  const int TBv = (wdt + 7) / 8;
+  int gy = 0, rc;
+  switch (TBv) {
+    case 1: rc = launch_gram_mma<1, 8>(b, tk, na, N, wdt, ws, s, &gy); break;
+    case 2: rc = launch_gram_mma<2, 4>(b, tk, na, N, wdt, ws, s, &gy); break;
+    case 3: rc = launch_gram_mma<3, 2>(b, tk, na, N, wdt, ws, s, &gy); break;
+    default: rc = launch_gram_mma<4, 1>(b, tk, na, N, wdt, ws, s, &gy); break;
+  }
+  if (rc) return rc;
+  const int W = b.off[b.nb];
+  const int wa = na > 0 ? b.off[na] : W, wb = na > 0 ? W - b.off[na] : W;
+  const int rows = wa * wb;
+  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>((const double*)ws, gy, rows, out, 0, 0, 1);
+  return picrom_check_launch("seg_sum");
+}
+
 static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* lds,
                      const int* widths, const int* jswap, long long N, double* out, void* ws,
                      void* stream) {
@@ -1025,10 +1351,14 @@ static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* 
   }
   const int W = b.off[nblocks];
   const int wa = na > 0 ? b.off[na] : W, wb = na > 0 ? W - b.off[na] : W;
-  if (W > 256 || ((wa + TB - 1) / TB) * ((wb + TB - 1) / TB) > 4 * 256)
-    return picrom_set_error(PICROM_ERR_CONFIG, "Gram: total width <= 256 and wa*wb <= 16384");
   const int G = gram_grid(N);
   cudaStream_t s = (cudaStream_t)stream;
+  {
+    int rc = gram_mma_try(b, na, N, ws, s, out);
+    if (rc != -1) return rc;
+  }
+  if (W > 256 || ((wa + TB - 1) / TB) * ((wb + TB - 1) / TB) > 4 * 256)
+    return picrom_set_error(PICROM_ERR_CONFIG, "Gram: total width <= 256 and wa*wb <= 16384");
   const size_t sm = (size_t)2 * GTR * W * sizeof(double) + (size_t)W * (sizeof(void*) + 2 * sizeof(int));
   // TMA staging when every block is row-contiguous (ld == width) and 16-B aligned
   bool tma = getenv("PICROM_GRAM_NO_TMA") == nullptr;
@@ -1116,6 +1446,37 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
   const size_t sm = (size_t)mats_len * sizeof(double);
   if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
   cudaStream_t s = (cudaStream_t)stream;
+  // DMMA path: even widths, rows 16-B aligned (ld even, 16-B aligned base)
+  bool mma = getenv("PICROM_COMBINE_NO_MMA") == nullptr && N >= 1024;
+  MmaTerms mt{};
+  for (int i = 0; i < nterms && mma; ++i)
+    mma = (widths[i] % 2 == 0) && (lds[i] % 2 == 0) && ((reinterpret_cast<uintptr_t>(ins[i]) & 15) == 0);
+  if (mma) {
+    mt.koff[0] = 0;
+    mt.soff[0] = 0;
+    for (int i = 0; i < nterms; ++i) {
+      int pa = widths[i];
+      while (pa % 16 != 4 && pa % 16 != 12) pa += 2;
+      mt.pa[i] = pa;
+      mt.koff[i + 1] = mt.koff[i] + widths[i];
+      mt.soff[i + 1] = mt.soff[i] + pa;
+    }
+    int cp = c;                       // M pitch = 4 or 12 mod 16: conflict-free B fragments
+    while (cp % 16 != 4 && cp % 16 != 12) ++cp;
+    mt.cp = cp;
+    const size_t smm = ((size_t)(mt.koff[nterms] + 4) * cp + 8 + (size_t)2 * CMR * mt.soff[nterms]) * sizeof(double);
+    if (smm <= 200 * 1024) {
+      const int G = (int)std::min<long long>(2LL * picrom_num_sms(), std::max<long long>(1, (N + CMR - 1) / CMR));
+      const int tbo = (c + 7) / 8;
+      switch (tbo) {
+        case 1: rom_allow_smem(combine_mma_kernel<1>); combine_mma_kernel<1><<<G, 256, smm, s>>>(t, mt, mats, N); break;
+        case 2: rom_allow_smem(combine_mma_kernel<2>); combine_mma_kernel<2><<<G, 256, smm, s>>>(t, mt, mats, N); break;
+        case 3: rom_allow_smem(combine_mma_kernel<3>); combine_mma_kernel<3><<<G, 256, smm, s>>>(t, mt, mats, N); break;
+        default: rom_allow_smem(combine_mma_kernel<4>); combine_mma_kernel<4><<<G, 256, smm, s>>>(t, mt, mats, N); break;
+      }
+      return picrom_check_launch("combine_mma_kernel");
+    }
+  }
   // TMA path: row-contiguous, 16-B aligned inputs
   bool tma = getenv("PICROM_COMBINE_NO_TMA") == nullptr;
   int wsum = 0;

@@ -1,0 +1,105 @@
+"""Tall-skinny Gram / combine kernels (the manifold building blocks of
+reduction.py:143-182) against numpy on the same inputs: the DMMA and TMA fast
+paths (equal block widths <= 32, >= 1024 rows) and the generic fallback."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _j(b):
+    """J applied to a (2h x w) block: [X; V] -> [V; -X] (reduction.py:44-47)."""
+    h = b.shape[0] // 2
+    return np.concatenate([b[h:], -b[:h]])
+
+
+def _cross(lib_built, blocks, na, rows):
+    import torch
+    from paper_2201_05555_b200 import _lib, _tall
+    from paper_2201_05555_b200 import _device as dev
+    widths = [int(t.shape[1]) for t, _ in blocks]
+    wa, wb = sum(widths[:na]), sum(widths[na:])
+    out = torch.empty((wa, wb), dtype=torch.float64, device="cuda")
+    arr = _tall._arr
+    _lib.call("picrom_cross_gram", len(blocks), na, arr(C.c_void_p, [t.data_ptr() for t, _ in blocks]),
+              arr(C.c_int, [int(t.stride(0)) for t, _ in blocks]), arr(C.c_int, widths),
+              arr(C.c_int, [int(j) for _, j in blocks]), rows, out.data_ptr(),
+              _tall._ws(rows, wa + wb).data_ptr(), dev.stream_handle())
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("w", [8, 16, 20, 32])
+@pytest.mark.parametrize("rows", [1024, 2 * 25013])
+def test_gram_equal_widths(lib_built, w, rows):
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(w * 7 + rows)
+    hs = [rng.standard_normal((rows, w)) for _ in range(3)]
+    blocks = [(torch.from_numpy(hs[0]).cuda(), False), (torch.from_numpy(hs[1]).cuda(), False),
+              (torch.from_numpy(hs[1]).cuda(), True), (torch.from_numpy(hs[2]).cuda(), False)]
+    W = np.concatenate([hs[0], hs[1], _j(hs[1]), hs[2]], axis=1)
+    ref = W.T @ W
+    got = _tall.gram(blocks)
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert np.array_equal(got, got.T)
+    assert np.array_equal(got, _tall.gram(blocks))       # deterministic
+
+
+def test_gram_eight_blocks_and_cross(lib_built):
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(5)
+    rows = 2 * 40001
+    hs = [rng.standard_normal((rows, 20)) for _ in range(8)]
+    js = [False, True, False, False, True, False, False, True]
+    blocks = [(torch.from_numpy(h).cuda(), j) for h, j in zip(hs, js)]
+    W = np.concatenate([_j(h) if j else h for h, j in zip(hs, js)], axis=1)
+    ref = W.T @ W
+    got = _tall.gram(blocks)
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    for na in (1, 3):
+        cg = _cross(lib_built, blocks, na, rows)
+        cref = W[:, :20 * na].T @ W[:, 20 * na:]
+        assert np.abs(cg - cref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_gram_fallback_paths(lib_built):
+    """Unequal widths / strided blocks take the generic kernels; same answers."""
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(9)
+    rows = 4096
+    a = rng.standard_normal((rows, 20))
+    b = rng.standard_normal((rows, 12))
+    big = torch.from_numpy(rng.standard_normal((rows, 40))).cuda()
+    blocks = [(torch.from_numpy(a).cuda(), False), (torch.from_numpy(b).cuda(), True), (big[:, :20], False)]
+    W = np.concatenate([a, _j(b), big[:, :20].cpu().numpy()], axis=1)
+    ref = W.T @ W
+    got = _tall.gram(blocks)
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("rows", [1024, 2 * 25013])
+def test_combine_terms(lib_built, rows):
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(rows)
+    x = rng.standard_normal((rows, 20))
+    y = rng.standard_normal((rows, 20))
+    e = rng.standard_normal((rows, 128))
+    m1, m2, m3 = (rng.standard_normal((20, 20)), rng.standard_normal((20, 20)),
+                  rng.standard_normal((128, 20)))
+    got = _tall.combine([(torch.from_numpy(x).cuda(), m1, False),
+                         (torch.from_numpy(y).cuda(), m2, True)]).cpu().numpy()
+    ref = x @ m1 + _j(y) @ m2
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    got = _tall.combine([(torch.from_numpy(e).cuda(), m3, False)]).cpu().numpy()
+    ref = e @ m3
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    out = torch.from_numpy(ref.copy()).cuda()
+    _tall.combine([(torch.from_numpy(x).cuda(), m1, False)], out=out, accumulate=True)
+    ref2 = ref + x @ m1
+    assert np.abs(out.cpu().numpy() - ref2).max() <= 1e-12 * np.abs(ref2).max()
