@@ -20,7 +20,7 @@ LIB_PATH = PKG_DIR / LIB_NAME
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
 ]
 
@@ -45,14 +45,32 @@ def build(force=False, verbose=False):
     if not Path(nvcc).exists():
         nvcc = "nvcc"
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", str(tmp), *map(str, sources())]
+    # one nvcc per translation unit, in parallel, then a host link
+    objs, procs = [], []
+    for src in sources():
+        obj = PKG_DIR / f"build_{src.stem}.o"
+        cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", str(obj), str(src)]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
+        objs.append(obj)
+    log = []
+    for cmd, pr in procs:
+        out, err = pr.communicate()
+        log.append(err)
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError(f"nvcc failed ({pr.returncode}): {' '.join(cmd)}")
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
+           *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode}): {' '.join(cmd)}")
+        raise RuntimeError(f"nvcc link failed ({res.returncode}): {' '.join(cmd)}")
+    for o in objs:
+        o.unlink(missing_ok=True)
     if verbose:
-        sys.stderr.write(res.stderr)
-    (PKG_DIR / "build_ptxas.log").write_text(res.stderr)
+        sys.stderr.write("".join(log))
+    (PKG_DIR / "build_ptxas.log").write_text("".join(log))
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

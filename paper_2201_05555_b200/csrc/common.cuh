@@ -62,15 +62,23 @@ __device__ __forceinline__ void locate(double x, double h, double inv_h, int nx,
 // (then cvt is exact and the Markstein residual exact); `rare` flags the
 // other inputs (tiny/huge/non-finite), which callers re-run through locate()
 // in a warp-uniform fix-up pass.  mask = nx-1 for power-of-two nx, else -1.
+//
+// floor() without the XU pipe: F2I.F64 / FRND.F64 issue on the conversion
+// unit, which ncu showed at 83% busy in the step kernel (profiles/r01).  For
+// |s| < 2^31, t = RD(s + 1.5*2^52) = 1.5*2^52 + floor(s) exactly (the ulp of
+// t is 1), so c = t - 1.5*2^52 = floor(s) (exact) and the low word of t is
+// floor(s) as a two's-complement int: three FP64-pipe adds, no conversion.
 __device__ __forceinline__ void locate_fast(double x, double h, double inv_h, int nx, int mask,
                                             double inv_nx, int& i0, double& frac, bool& rare) {
+  constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52
   const double q0 = __dmul_rn(x, inv_h);
   const double r = fma(-h, q0, x);
   const double s = fma(r, inv_h, q0);
-  const double c = floor(s);
+  const double t = __dadd_rd(s, kMagic);
+  const double c = __dsub_rn(t, kMagic);
   frac = __dsub_rn(s, c);
-  rare = !(fabs(q0) > 1e-280 && fabs(c) < 2147483647.0);
-  const int ci = __double2int_rz(c);
+  rare = !(fabs(q0) > 1e-280 && fabs(s) < 2147483647.0);
+  const int ci = __double2loint(t);
   if (mask >= 0) {
     i0 = ci & mask;
   } else {
@@ -225,6 +233,27 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // ---- TMA bulk copies + mbarriers (Hopper/Blackwell async proxy) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+
+// predicated shared-memory f64 load / store (no branch: @p ld/st.shared)
+__device__ __forceinline__ double lds_f64_if(uint32_t addr, bool p) {
+  double v = 0.0;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}\n"
+      : "+d"(v) : "r"(addr), "r"((uint32_t)p));
+  return v;
+}
+__device__ __forceinline__ void sts_f64_if(uint32_t addr, double v, bool p) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}\n"
+      ::"r"(addr), "d"(v), "r"((uint32_t)p) : "memory");
+}
+
+// histogram id of thread tid when K lanes share one histogram (step kernels)
+template <int K>
+__device__ __forceinline__ int myh_of(int tid) {
+  constexpr int KG = 32 / K;
+  return (tid >> 5) * KG + ((tid & 31) % KG);
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

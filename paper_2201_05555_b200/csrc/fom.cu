@@ -106,14 +106,8 @@ static int hist_budget_bytes() {
   return b;
 }
 
-static int step_nt() {
-  static int nt = 0;
-  if (!nt) {
-    const char* s = getenv("PICROM_STEP_NT");
-    nt = (s && atoi(s) == 256) ? 256 : 128;      // 128 measured best (profiles/r01)
-  }
-  return nt;
-}
+// 128 threads per CTA measured best (profiles/r01; 256 was slower at every K)
+static int step_nt() { return 128; }
 
 static int choose_k(int nx, int degree) {
   int budget = hist_budget_bytes();
@@ -505,11 +499,16 @@ step_kernel(StepArgs a, SolveArgs sa) {
   double* hist = smem;                         // [nh][H]
   double* coef = hist + nh * H;                // [D][nx] field polynomials
   double* red = coef + (MODE == MODE_LEAPFROG ? nx * D : 0);
+  const unsigned int hist_base = smem_u32(hist + myh_of<K>(threadIdx.x));
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int myh = tid / K;
-  const int klane = lane % K;
+  // lanes l, l + 32/K, l + 2*32/K, ... share histogram (warp, l mod 32/K) and
+  // take turns by lane range: the active lanes of a phase are one contiguous
+  // 32/K-lane group with distinct banks (histogram id mod 16), so each
+  // 8-byte access of a phase is a single conflict-free wavefront
+  constexpr int KG = 32 / K;
+  const int klane = lane / KG;     // histogram: myh_of<K>(tid)
   const int G = gridDim.x;
   const long long T = a.n * (long long)a.p;
   const long long start = cta_start(blockIdx.x, T, G);
@@ -666,32 +665,38 @@ step_kernel(StepArgs a, SolveArgs sa) {
         }
       }
 
-      // pass 3: deposit (K lanes per histogram take turns)
+      // pass 3: deposit.  Weights of all U particles first, then K phases; in
+      // phase q the lanes of group q read-modify-write their U particles'
+      // rows with predicated shared loads/stores (no branches, so the block
+      // stays one scheduling region), one warp barrier between phases.
+      double w[U][NW];
+      unsigned int hrow[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        double w[NW];
         if constexpr (MODE == MODE_DEPOSIT) {
-          if (a.wkind == 1) Spline<D>::dweights(fr[u], ip[I_INVH], w);
-          else Spline<D>::weights(fr[u], w);
+          if (a.wkind == 1) Spline<D>::dweights(fr[u], ip[I_INVH], w[u]);
+          else Spline<D>::weights(fr[u], w[u]);
           if (Y) {
 #pragma unroll
-            for (int m = 0; m < NW; ++m) w[m] *= cv[u];
+            for (int m = 0; m < NW; ++m) w[u][m] *= cv[u];
           }
         } else {
-          Spline<D>::weights(fr[u], w);
+          Spline<D>::weights(fr[u], w[u]);
         }
+        hrow[u] = hist_base + (unsigned int)(cl[u] * H) * 8u;
+      }
 #pragma unroll
-        for (int q = 0; q < K; ++q) {
-          if (ok[u] && klane == q) {
-            double* hp = hist + cl[u] * H + myh;
-            double cur[NW];
+      for (int q = 0; q < K; ++q) {
 #pragma unroll
-            for (int m = 0; m < NW; ++m) cur[m] = hp[m * H];
+        for (int u = 0; u < U; ++u) {
+          const bool act = ok[u] && klane == q;
+          double cur[NW];
 #pragma unroll
-            for (int m = 0; m < NW; ++m) hp[m * H] = cur[m] + w[m];
-          }
-          if constexpr (K > 1) __syncwarp();
+          for (int m = 0; m < NW; ++m) cur[m] = lds_f64_if(hrow[u] + m * H * 8u, act);
+#pragma unroll
+          for (int m = 0; m < NW; ++m) sts_f64_if(hrow[u] + m * H * 8u, cur[m] + w[u][m], act);
         }
+        if constexpr (K > 1) __syncwarp();
       }
     };
 
@@ -1120,23 +1125,13 @@ int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, cons
 
 template <int D, int K, int MODE>
 static int launch_step_t(const StepArgs& a, const SolveArgs& sa, const Plan& pl, cudaStream_t s) {
-  if (step_nt() == 128) {
-    auto kfn = step_kernel<D, K, MODE, 128>;
-    static bool attr = false;
-    if (!attr) {
-      allow_max_dynamic_smem(kfn);
-      attr = true;
-    }
-    kfn<<<pl.G, 128, pl.smem, s>>>(a, sa);
-  } else {
-    auto kfn = step_kernel<D, K, MODE, 256>;
-    static bool attr = false;
-    if (!attr) {
-      allow_max_dynamic_smem(kfn);
-      attr = true;
-    }
-    kfn<<<pl.G, 256, pl.smem, s>>>(a, sa);
+  auto kfn = step_kernel<D, K, MODE, 128>;
+  static bool attr = false;
+  if (!attr) {
+    allow_max_dynamic_smem(kfn);
+    attr = true;
   }
+  kfn<<<pl.G, 128, pl.smem, s>>>(a, sa);
   return check_launch("step_kernel");
 }
 
@@ -1168,15 +1163,9 @@ static int launch_step(const StepArgs& a, int degree, const Plan& pl, cudaStream
 template <int D, int K>
 static int occ_of(size_t smem) {
   int occ = 0;
-  if (step_nt() == 128) {
-    auto kfn = step_kernel<D, K, MODE_LEAPFROG, 128>;
-    allow_max_dynamic_smem(kfn);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, smem) != cudaSuccess) occ = 1;
-  } else {
-    auto kfn = step_kernel<D, K, MODE_LEAPFROG, 256>;
-    allow_max_dynamic_smem(kfn);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, smem) != cudaSuccess) occ = 1;
-  }
+  auto kfn = step_kernel<D, K, MODE_LEAPFROG, 128>;
+  allow_max_dynamic_smem(kfn);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, smem) != cudaSuccess) occ = 1;
   return occ;
 }
 
@@ -1571,9 +1560,13 @@ __global__ void __launch_bounds__(kThreads) table_kernel(const double* x, long l
       record_bad(status, 0, i, j, p);
       continue;
     }
+    // the step kernels' branch-free locate (rare inputs: exact locate), so
+    // picrom_locate's bit-exactness tests cover the production path
     int c;
     double f;
-    locate(xv, ip[I_H], ip[I_INVH], nx, inv_nx, c, f);
+    bool rare;
+    locate_fast(xv, ip[I_H], ip[I_INVH], nx, (nx & (nx - 1)) == 0 ? nx - 1 : -1, inv_nx, c, f, rare);
+    if (rare) locate(xv, ip[I_H], ip[I_INVH], nx, inv_nx, c, f);
     const size_t o = (size_t)j * ldo + i;
     if (i0) i0[o] = c;
     if (!w) continue;

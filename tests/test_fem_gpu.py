@@ -72,7 +72,11 @@ def test_locate_division_is_ieee(lib_built):
                  rng.integers(-10 * nx, 10 * nx, 200_000) * h,
                  np.nextafter(rng.integers(-10 * nx, 10 * nx, 200_000) * h, np.inf),
                  np.nextafter(rng.integers(-10 * nx, 10 * nx, 200_000) * h, -np.inf),
-                 rng.uniform(-1e6, 1e6, 200_000), rng.standard_normal(200_000) * 1e-300]
+                 rng.uniform(-1e6, 1e6, 200_000), rng.standard_normal(200_000) * 1e-300,
+                 # around the fast path's |x/h| < 2^31 - 1 limit and the +-0 / tiny edges
+                 np.array([2.0**31 - 1, 2.0**31 - 1.5, 2.0**31, 2.0**31 + 7, -(2.0**31),
+                           -(2.0**31) + 1, -(2.0**31) - 3, 0.5, -0.5]) * h,
+                 np.array([0.0, -0.0, 5e-324, -5e-324, 1e-280, -1e-280])]
         x = np.concatenate(parts)
         xd = torch.from_numpy(x).cuda().reshape(1, -1)
         n = x.size
