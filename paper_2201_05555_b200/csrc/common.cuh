@@ -58,16 +58,23 @@ __device__ __forceinline__ void locate(double x, double h, double inv_h, int nx,
   i0 = cell_mod(c, nx, inv_nx);
 }
 
-// Branch-free common path of locate(): valid when |x/h| is in (1e-280, 2^31)
-// (then cvt is exact and the Markstein residual exact); `rare` flags the
-// other inputs (tiny/huge/non-finite), which callers re-run through locate()
-// in a warp-uniform fix-up pass.  mask = nx-1 for power-of-two nx, else -1.
+// Branch-free common path of locate() for power-of-two nx.  `mask` comes from
+// fast_mask(): nx - 1, or -1 when nx is not a power of two or h is outside
+// [2^-100, 2^100].  `rare` flags the inputs the fast path does not cover --
+// |x/h| >= 2^51, |x/h| <= 2^-900 (incl. 0), non-finite x, or mask < 0 -- which
+// callers re-run through locate() in a warp-uniform fix-up pass.
 //
-// floor() without the XU pipe: F2I.F64 / FRND.F64 issue on the conversion
-// unit, which ncu showed at 83% busy in the step kernel (profiles/r01).  For
-// |s| < 2^31, t = RD(s + 1.5*2^52) = 1.5*2^52 + floor(s) exactly (the ulp of
-// t is 1), so c = t - 1.5*2^52 = floor(s) (exact) and the low word of t is
-// floor(s) as a two's-complement int: three FP64-pipe adds, no conversion.
+// x/h: Markstein's correction of q0 = RN(x * RN(1/h)) gives RN(x/h) (IEEE
+// division) whenever q0 is far from under/overflow (|q0| > 2^-900 here).
+// floor() without the XU pipe (F2I.F64 / FRND.F64 run on the conversion unit,
+// which ncu showed at 83% busy in the step kernel, profiles/r01): for
+// |s| < 2^51, t = RD(s + 1.5*2^52) = 1.5*2^52 + floor(s) exactly (the ulp of
+// t is 1), so c = t - 1.5*2^52 = floor(s), and the low word of t is
+// floor(s) mod 2^32, hence floor(s) mod nx = lo(t) & (nx - 1).
+__device__ __forceinline__ int fast_mask(int nx, double h) {
+  return ((nx & (nx - 1)) == 0 && h > 0x1p-100 && h < 0x1p100) ? nx - 1 : -1;
+}
+
 __device__ __forceinline__ void locate_fast(double x, double h, double inv_h, int nx, int mask,
                                             double inv_nx, int& i0, double& frac, bool& rare) {
   constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52
@@ -77,17 +84,8 @@ __device__ __forceinline__ void locate_fast(double x, double h, double inv_h, in
   const double t = __dadd_rd(s, kMagic);
   const double c = __dsub_rn(t, kMagic);
   frac = __dsub_rn(s, c);
-  rare = !(fabs(q0) > 1e-280 && fabs(s) < 2147483647.0);
-  const int ci = __double2loint(t);
-  if (mask >= 0) {
-    i0 = ci & mask;
-  } else {
-    const int q = __double2int_rd(static_cast<double>(ci) * inv_nx);
-    int rr = ci - q * nx;
-    rr += (rr < 0) ? nx : 0;
-    rr -= (rr >= nx) ? nx : 0;
-    i0 = rr;
-  }
+  rare = !(fabs(q0) > 0x1p-900 && fabs(s) < 0x1p51) || mask < 0;
+  i0 = __double2loint(t) & mask;
 }
 
 template <int D> struct Spline;
@@ -127,12 +125,12 @@ template <> struct Spline<3> {
   static constexpr int OFF = -1;
   __device__ static __forceinline__ void weights(double f, double* w) {
     const double s6 = 1.0 / 6.0;
-    double g = 1.0 - f;
-    double f2 = f * f;
-    w[0] = g * g * g * s6;
-    w[1] = (2.0 / 3.0) - f2 + 0.5 * f2 * f;
-    w[2] = s6 + 0.5 * (f + f2 - f2 * f);
-    w[3] = f2 * f * s6;
+    const double g = 1.0 - f;
+    const double f2 = f * f, f3 = f2 * f;
+    w[0] = (g * g) * (g * s6);
+    w[1] = fma(0.5, f3, (2.0 / 3.0) - f2);
+    w[2] = fma(0.5, (f + f2) - f3, s6);
+    w[3] = f3 * s6;
   }
   __device__ static __forceinline__ void dweights(double f, double g, double* w) {
     const double e = 1.0 - f;

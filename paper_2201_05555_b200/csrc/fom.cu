@@ -514,7 +514,6 @@ step_kernel(StepArgs a, SolveArgs sa) {
   const long long start = cta_start(blockIdx.x, T, G);
   const long long end = cta_start(blockIdx.x + 1, T, G);
   const double inv_nx = 1.0 / (double)nx;
-  const int mask = (nx & (nx - 1)) == 0 ? nx - 1 : -1;
   const long long step_id = a.counter ? (*a.counter + 1) : a.step;
   const int woff = (tid >> 5) * 32 * U + lane;   // lane's offset inside a SPAN block
 
@@ -545,6 +544,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
     }
     const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
     const double h = ip[I_H], inv_h = ip[I_INVH];
+    const int mask = fast_mask(nx, h);
 
     for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
     if (MODE == MODE_LEAPFROG && j != last_j) {
@@ -614,12 +614,16 @@ step_kernel(StepArgs a, SolveArgs sa) {
         for (int u = 0; u < U; ++u) {
           double C[D];
 #pragma unroll
+#ifdef PICROM_EXP_NOGATHER
+          for (int k = 0; k < D; ++k) C[k] = f0[u] * (k + 1);      // timing experiment only
+#else
           for (int k = 0; k < D; ++k) C[k] = coef[k * nx + c0[u]];
+#endif
           const double E = horner<D>(C, f0[u]);
           const double vn = cv[u] + a.kfull * E;
           kin = valid[u] ? fma(vn, vn, kin) : kin;
-          const double vh = __dadd_rn(cv[u], __dmul_rn(a.kick, E));
-          xn[u] = __dadd_rn(cx[u], __dmul_rn(a.dt, vh));
+          const double vh = fma(a.kick, E, cv[u]);      // leapfrog kick + drift
+          xn[u] = fma(a.dt, vh, cx[u]);
           const int i = b0 + woff + u * 32;
           if (valid[u]) {
             __stcs(X + i, xn[u]);
@@ -689,7 +693,11 @@ step_kernel(StepArgs a, SolveArgs sa) {
       for (int q = 0; q < K; ++q) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+#ifdef PICROM_EXP_NODEP
+          const bool act = ok[u] && klane == q && fr[u] < -1.0;   // timing experiment only
+#else
           const bool act = ok[u] && klane == q;
+#endif
           double cur[NW];
 #pragma unroll
           for (int m = 0; m < NW; ++m) cur[m] = lds_f64_if(hrow[u] + m * H * 8u, act);
@@ -879,7 +887,6 @@ __global__ void __launch_bounds__(NCW * 32 + 32, 1) step_tma_kernel(StepArgs a, 
   const int myh = tid / K;
   const int klane = lane % K;
   const double inv_nx = 1.0 / (double)nx;
-  const int mask = (nx & (nx - 1)) == 0 ? nx - 1 : -1;
   const long long step_id = a.counter ? (*a.counter + 1) : a.step;
   int stage = 0;
   uint32_t phase = 0;
@@ -890,6 +897,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, 1) step_tma_kernel(StepArgs a, 
     const long long hi = min(a.n, end - (long long)j * a.n);
     const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
     const double h = ip[I_H], inv_h = ip[I_INVH];
+    const int mask = fast_mask(nx, h);
     for (int q = tid; q < nh * H; q += NC) hist[q] = 0.0;
     {
       const double* ph = a.phi + (size_t)j * nx;
@@ -1565,7 +1573,7 @@ __global__ void __launch_bounds__(kThreads) table_kernel(const double* x, long l
     int c;
     double f;
     bool rare;
-    locate_fast(xv, ip[I_H], ip[I_INVH], nx, (nx & (nx - 1)) == 0 ? nx - 1 : -1, inv_nx, c, f, rare);
+    locate_fast(xv, ip[I_H], ip[I_INVH], nx, fast_mask(nx, ip[I_H]), inv_nx, c, f, rare);
     if (rare) locate(xv, ip[I_H], ip[I_INVH], nx, inv_nx, c, f);
     const size_t o = (size_t)j * ldo + i;
     if (i0) i0[o] = c;

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(384) rom_deposit_kernel(RomArgs a) {
   const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
   const double h = ip[I_H], inv_h = ip[I_INVH];
   const double inv_nx = 1.0 / (double)a.nx;
-  const int mask = (a.nx & (a.nx - 1)) == 0 ? a.nx - 1 : -1;
+  const int mask = fast_mask(a.nx, h);
   double zc[NB];
 #pragma unroll
   for (int k = 0; k < NB; ++k) zc[k] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(384) rom_gather_kernel(RomArgs a) {
   const double h = ip[I_H], g = ip[I_INVH], inv_h = g;
   const double cf = a.coef_kind == 0 ? ip[I_GCOEF] : 1.0;
   const double inv_nx = 1.0 / (double)nx;
-  const int mask = (nx & (nx - 1)) == 0 ? nx - 1 : -1;
+  const int mask = fast_mask(nx, h);
   double zc[NB], acc[NB];
 #pragma unroll
   for (int k = 0; k < NB; ++k) {

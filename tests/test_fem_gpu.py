@@ -76,7 +76,10 @@ def test_locate_division_is_ieee(lib_built):
                  # around the fast path's |x/h| < 2^31 - 1 limit and the +-0 / tiny edges
                  np.array([2.0**31 - 1, 2.0**31 - 1.5, 2.0**31, 2.0**31 + 7, -(2.0**31),
                            -(2.0**31) + 1, -(2.0**31) - 3, 0.5, -0.5]) * h,
-                 np.array([0.0, -0.0, 5e-324, -5e-324, 1e-280, -1e-280])]
+                 np.array([2.0**51 - 1, 2.0**51 - 0.5, 2.0**51, 2.0**51 + 2, -(2.0**51),
+                           -(2.0**51) + 1, -(2.0**51) - 2, 2.0**52 + 6, 2.0**60]) * h,
+                 np.array([0.0, -0.0, 5e-324, -5e-324, 1e-280, -1e-280, 2.0**-800, 2.0**-801,
+                           -(2.0**-800), 3.0 * 2.0**-801, 1e300, -1e300])]
         x = np.concatenate(parts)
         xd = torch.from_numpy(x).cuda().reshape(1, -1)
         n = x.size
