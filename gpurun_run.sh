@@ -1,25 +1,6 @@
 mkdir -p gpurun_out
-: > gpurun_out/variants.log
-for rep in 1 2; do
-for v in main dsetp; do
-  if [ "$v" = main ]; then L="X=1"; else L="PICROM_LIB=paper_2201_05555_b200/variants/libpicrom_$v.so"; fi
-  for c in C2 C5; do
-    echo "== $v $c" >> gpurun_out/variants.log
-    env $L timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 2 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value']/1e9, d['ms_per_step'], d['roofline']['frac'])" >> gpurun_out/variants.log 2>&1
-  done
-done
-done
-./tools/bin/fp64_peak > gpurun_out/fp64_peak.log 2>&1
-python - > gpurun_out/dgemm.log 2>&1 <<'PY'
-import torch, time
-for n in (4096, 8192):
-    a = torch.randn(n, n, dtype=torch.float64, device="cuda"); b = torch.randn(n, n, dtype=torch.float64, device="cuda")
-    for _ in range(3): a @ b
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-    best = 1e9
-    for _ in range(5):
-        e0.record(); a @ b; e1.record(); torch.cuda.synchronize(); best = min(best, e0.elapsed_time(e1))
-    print(f"dgemm {n}: {best:.3f} ms  {2*n**3/best/1e9:.1f} TF/s")
-PY
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python tools/prof_rom_step.py > gpurun_out/prof_rom.log 2>&1
+PICROM_ROM_NO_MMA=1 timeout 600 python tools/prof_rom_step.py > gpurun_out/prof_rom_nomma.log 2>&1
+timeout 1200 python tools/bench_rom.py --config C3 --steps 3 --warmup 1 > gpurun_out/rom_c3.log 2>&1; echo "rc=$?" >> gpurun_out/rom_c3.log
 echo done

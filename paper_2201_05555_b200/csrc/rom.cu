@@ -1034,6 +1034,258 @@ __global__ void deim_gather_kernel(const double* uxd, const double* z, int ldz, 
   }
 }
 
+// ---- DMMA (mma.sync m8n8k4 f64) reduced-basis F-evaluation kernels ----
+//
+// Same contract as rom_deposit_kernel / rom_gather_kernel, with the two
+// tall-skinny products of the reduced F-evaluation on the FP64 tensor pipe:
+// the reconstruct X_r = U_X Z (driver.py:69) as X^T (8 cols x 8 rows) =
+// Z^T (8 x n) . U_blk^T (n x 8), and the projection U_X^T E (driver.py:85) as
+// (n x 8 cols) += U_blk^T (n x 8 rows) . E (8 rows x 8 cols).  Warp w owns 8
+// columns; in the X^T fragment lane (g = lane/4, t = lane%4) holds column g at
+// rows 2t, 2t+1 of each 8-row block, so per-lane deposit histograms (4 copies
+// per column) stay private and conflict-free.  DMMA and DFMA share the FP64
+// pipe on B200 (profiles/r01b/fp64_peak.log: 37.2 vs 36.4 TF/s, 30.8 mixed):
+// the gain is issue slots -- 5 DMMA per 64 units instead of 1280 DFMA.
+constexpr int MW = 8;            // warps per CTA
+constexpr int MC = MW * 8;       // z columns per CTA
+
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// X^T block: x0, x1 = X[rb + 2t (+1)][column g] from the staged U tile
+template <int NK>
+__device__ __forceinline__ void recon_block(const double* tile, int rb, int rows, int n,
+                                            const double* za, int g, int t, double& x0,
+                                            double& x1) {
+  x0 = 0.0;
+  x1 = 0.0;
+  const int ur = rb + g;
+#pragma unroll
+  for (int ks = 0; ks < NK; ++ks) {
+    const int k = ks * 4 + t;
+    const double b = (ur < rows && k < n) ? tile[ur * n + k] : 0.0;
+    dmma_f64(x0, x1, za[ks], b);
+  }
+}
+
+template <int D, int NK>
+__global__ void __launch_bounds__(MW * 32, 1) rom_deposit_mma_kernel(RomArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int NT = MW * 32;
+  const int n = a.n, nx = a.nx, nh = nx + D;
+  double* ut = smem;                          // [2][TR * n]
+  double* hist = ut + 2 * TR * n;             // [nh][NT] private per lane
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int c = blockIdx.y * MC + warp * 8 + g;
+  const bool active = c < a.p;
+  const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
+  const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
+  const double h = ip[I_H], inv_h = ip[I_INVH];
+  const double inv_nx = 1.0 / (double)nx;
+  const int mask = fast_mask(nx, h);
+  double za[NK];
+#pragma unroll
+  for (int ks = 0; ks < NK; ++ks) {
+    const int k = ks * 4 + t;
+    za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+  }
+  for (int q = tid; q < nh * NT; q += NT) hist[q] = 0.0;
+  const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
+  const int ntiles = (int)((hi - lo + TR - 1) / TR);
+  if (ntiles > 0) stage_rows(ut, a.ux, lo, (int)min((long long)TR, hi - lo), n);
+  for (int tt = 0; tt < ntiles; ++tt) {
+    const long long t0 = lo + (long long)tt * TR;
+    const int rows = (int)min((long long)TR, hi - t0);
+    if (tt + 1 < ntiles) {
+      const long long t1 = t0 + TR;
+      stage_rows(ut + ((tt + 1) & 1) * TR * n, a.ux, t1, (int)min((long long)TR, hi - t1), n);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* tile = ut + (tt & 1) * TR * n;
+    for (int rb = 0; rb < rows; rb += 8) {
+      double xv[2];
+      recon_block<NK>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = rb + 2 * t + e;
+        if (!active || row >= rows) continue;
+        const double x = xv[e];
+        int cell;
+        double f;
+        bool rare;
+        locate_fast(x, h, inv_h, nx, mask, inv_nx, cell, f, rare);
+        if (rare) {
+          if (!isfinite(x)) {
+            record_bad(a.status, 0, t0 + row, c, a.p);
+            continue;
+          }
+          locate(x, h, inv_h, nx, inv_nx, cell, f);
+        }
+        double w[D + 1];
+        Spline<D>::weights(f, w);
+        double* hp = hist + cell * NT + tid;
+        double cur[D + 1];
+#pragma unroll
+        for (int m = 0; m <= D; ++m) cur[m] = hp[m * NT];
+#pragma unroll
+        for (int m = 0; m <= D; ++m) hp[m * NT] = cur[m] + w[m];
+      }
+    }
+    __syncthreads();
+  }
+  // fold ghost rows and the 4 copies per column (fixed order) -> seg[b][c][nd]
+  const int P_used = min(MC, a.p - blockIdx.y * MC);
+  for (int q = tid; q < P_used * nx; q += NT) {
+    const int cl = q / nx, nd = q % nx;
+    const int t_base = (cl >> 3) * 32 + (cl & 7) * 4;
+    double s = 0.0;
+    for (int rr = (nd - Spline<D>::OFF) % nx; rr < nh; rr += nx)
+      for (int cp = 0; cp < 4; ++cp) s += hist[rr * NT + t_base + cp];
+    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * MC + cl) * nx + nd] = s;
+  }
+}
+
+template <int D, int NK>
+__global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int NT = MW * 32;
+  constexpr int NM = (4 * NK + 7) / 8;        // 8-row tiles of the projection (n <= 8 NM)
+  constexpr int PS = MC + 1;                  // padded phi row (bank spread)
+  const int n = a.n, nx = a.nx;
+  double* ut = smem;                          // [2][TR * n]
+  double* phs = ut + 2 * TR * n;              // [nx][PS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int cl = warp * 8 + g;
+  const int c = blockIdx.y * MC + cl;
+  const bool active = c < a.p;
+  const int P_used = min(MC, a.p - blockIdx.y * MC);
+  for (int q = tid; q < nx * MC; q += NT) {
+    const int nd = q / MC, cc = q % MC;
+    phs[nd * PS + cc] = cc < P_used ? a.phi[(size_t)(blockIdx.y * MC + cc) * nx + nd] : 0.0;
+  }
+  const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
+  const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
+  const double h = ip[I_H], gi = ip[I_INVH], inv_h = gi;
+  const double cf = a.coef_kind == 0 ? ip[I_GCOEF] : 1.0;
+  const double inv_nx = 1.0 / (double)nx;
+  const int mask = fast_mask(nx, h);
+  double za[NK], acc[NM][2];
+#pragma unroll
+  for (int ks = 0; ks < NK; ++ks) {
+    const int k = ks * 4 + t;
+    za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+  }
+#pragma unroll
+  for (int mt = 0; mt < NM; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+  const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
+  const int ntiles = (int)((hi - lo + TR - 1) / TR);
+  if (ntiles > 0) stage_rows(ut, a.ux, lo, (int)min((long long)TR, hi - lo), n);
+  for (int tt = 0; tt < ntiles; ++tt) {
+    const long long t0 = lo + (long long)tt * TR;
+    const int rows = (int)min((long long)TR, hi - t0);
+    if (tt + 1 < ntiles) {
+      const long long t1 = t0 + TR;
+      stage_rows(ut + ((tt + 1) & 1) * TR * n, a.ux, t1, (int)min((long long)TR, hi - t1), n);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* tile = ut + (tt & 1) * TR * n;
+    for (int rb = 0; rb < rows; rb += 8) {
+      double xv[2], ev[2];
+      recon_block<NK>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ev[e] = 0.0;
+        const int row = rb + 2 * t + e;
+        if (!active || row >= rows) continue;
+        const double x = xv[e];
+        const long long i = t0 + row;
+        int cell;
+        double f;
+        bool rare;
+        locate_fast(x, h, inv_h, nx, mask, inv_nx, cell, f, rare);
+        if (rare) {
+          if (!isfinite(x)) {
+            record_bad(a.status, 0, i, c, a.p);
+            continue;
+          }
+          locate(x, h, inv_h, nx, inv_nx, cell, f);
+        }
+        double pv[D + 1];
+#pragma unroll
+        for (int m = 0; m <= D; ++m) {
+          int nd = cell + Spline<D>::OFF + m;
+          nd = nd < 0 ? nd + nx : (nd >= nx ? nd - nx : nd);
+          pv[m] = phs[nd * PS + cl];
+        }
+        double E;
+        if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
+          E = __dmul_rn(cf, __dadd_rn(__dmul_rn(-gi, pv[0]), __dmul_rn(gi, pv[1])));
+        } else {
+          double dw[D + 1];
+          Spline<D>::dweights(f, gi, dw);
+          double sacc = 0.0;
+#pragma unroll
+          for (int m = 0; m <= D; ++m) sacc = fma(dw[m], pv[m], sacc);
+          E = cf * sacc;
+        }
+        ev[e] = E;
+        if (a.eout) a.eout[(size_t)i * a.ldo + c] = E;
+        if (a.lam) {
+          double lv;
+          if constexpr (D == 1) {
+            lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
+          } else {
+            double w[D + 1];
+            Spline<D>::weights(f, w);
+            lv = 0.0;
+#pragma unroll
+            for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
+          }
+          a.lam[(size_t)i * a.ldo + c] = lv;
+        }
+      }
+      // projection: acc (basis m = 8 mt + g, columns 2t, 2t+1) += U_blk^T E_blk;
+      // B fragment E[rb + 4 ks + t][column g] lives in lane 4 g + 2 ks + t/2
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int src = g * 4 + 2 * ks + (t >> 1);
+        const double s0 = __shfl_sync(0xffffffffu, ev[0], src);
+        const double s1 = __shfl_sync(0xffffffffu, ev[1], src);
+        const double b = (t & 1) ? s1 : s0;
+        const int ur = rb + 4 * ks + t;
+#pragma unroll
+        for (int mt = 0; mt < NM; ++mt) {
+          const int m = mt * 8 + g;
+          const double av = (ur < rows && m < n) ? tile[ur * n + m] : 0.0;
+          dmma_f64(acc[mt][0], acc[mt][1], av, b);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // per-CTA partials seg[b][c][k]: lane holds basis m = 8 mt + g at columns 2t, 2t+1
+#pragma unroll
+  for (int mt = 0; mt < NM; ++mt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int m = mt * 8 + g;
+      const int col = blockIdx.y * MC + warp * 8 + 2 * t + e;
+      if (m < n && col < a.p) a.seg[((size_t)blockIdx.x * a.p + col) * n + m] = acc[mt][e];
+    }
+}
+
 int gram_grid(long long N) {
   long long g = std::min<long long>(2LL * picrom_num_sms(), std::max<long long>(1, N / 256));
   return (int)g;
@@ -1042,6 +1294,20 @@ int gram_grid(long long N) {
 int rom_grid(long long N) {
   long long g = std::min<long long>((long long)picrom_num_sms(), std::max<long long>(1, N / 64));
   return (int)g;
+}
+
+// DMMA path row blocks: one wave of `per_sm` CTAs per SM over the column tiles
+int rom_grid_mma(long long N, int p, int per_sm) {
+  const int tiles = (p + MC - 1) / MC;
+  long long g = std::max(1LL, (long long)picrom_num_sms() * per_sm / tiles);
+  return (int)std::min<long long>(g, std::max<long long>(1, N / 64));
+}
+constexpr int kGatherMmaPerSm = 3;   // 79 registers x 256 threads: 3 CTAs per SM
+
+bool rom_use_mma() {
+  static int use = -1;
+  if (use < 0) use = getenv("PICROM_ROM_NO_MMA") == nullptr;
+  return use == 1;
 }
 
 }  // namespace
@@ -1153,7 +1419,7 @@ combine_mma_kernel(Terms t, MmaTerms mt, const double* mats, long long N) {
 }
 
 extern "C" size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx) {
-  const size_t G = (size_t)rom_grid(N);
+  const size_t G = (size_t)std::max(rom_grid(N), rom_grid_mma(N, p, kGatherMmaPerSm));
   const size_t dep = G * p * nx;
   const size_t gat = G * p * n;
   const size_t gram = (size_t)gram_grid(N) * 256 * 256;
@@ -1220,6 +1486,56 @@ static int launch_rom_gather(const RomArgs& a, int G, cudaStream_t s) {
   return ROM_NB_DISPATCH(launch_rom_gather_nb, D, a, G, s);
 }
 
+// DMMA path: k-steps NK = ceil(n / 4) rounded up to {2, 4, 5, 8}
+static int mma_nk(int n) { return n <= 8 ? 2 : n <= 16 ? 4 : n <= 20 ? 5 : 8; }
+static size_t mma_dep_smem(int n, int nx, int D) {
+  return ((size_t)2 * TR * n + (size_t)(nx + D) * MW * 32) * sizeof(double);
+}
+static size_t mma_gat_smem(int n, int nx) {
+  return ((size_t)2 * TR * n + (size_t)nx * (MC + 1)) * sizeof(double);
+}
+
+template <int D, int NK>
+static int launch_dep_mma_t(const RomArgs& a, int G, cudaStream_t s) {
+  auto kfn = rom_deposit_mma_kernel<D, NK>;
+  static bool attr = false;
+  if (!attr) { rom_allow_smem(kfn); attr = true; }
+  kfn<<<dim3(G, (a.p + MC - 1) / MC), MW * 32, mma_dep_smem(a.n, a.nx, D), s>>>(a);
+  return picrom_check_launch("rom_deposit_mma_kernel");
+}
+template <int D, int NK>
+static int launch_gat_mma_t(const RomArgs& a, int G, cudaStream_t s) {
+  auto kfn = rom_gather_mma_kernel<D, NK>;
+  static bool attr = false;
+  if (!attr) { rom_allow_smem(kfn); attr = true; }
+  kfn<<<dim3(G, (a.p + MC - 1) / MC), MW * 32, mma_gat_smem(a.n, a.nx), s>>>(a);
+  return picrom_check_launch("rom_gather_mma_kernel");
+}
+#define ROM_NK_DISPATCH(FN, D, A, G, S)                                              \
+  (mma_nk(A.n) == 2 ? FN<D, 2>(A, G, S) : mma_nk(A.n) == 4 ? FN<D, 4>(A, G, S) :     \
+   mma_nk(A.n) == 5 ? FN<D, 5>(A, G, S) : FN<D, 8>(A, G, S))
+
+// row blocks of the deposit for this call (DMMA: one CTA per SM), 0 = old path
+template <int D>
+static int rom_dep_grid(const RomArgs& a) {
+  if (!rom_use_mma() || mma_dep_smem(a.n, a.nx, D) > 220 * 1024) return rom_grid(a.N);
+  return rom_grid_mma(a.N, a.p, 1);
+}
+template <int D>
+static int launch_rom_deposit_any(const RomArgs& a, int G, cudaStream_t s) {
+  if (!rom_use_mma() || mma_dep_smem(a.n, a.nx, D) > 220 * 1024) return launch_rom_deposit<D>(a, G, s);
+  return ROM_NK_DISPATCH(launch_dep_mma_t, D, a, G, s);
+}
+static int rom_gat_grid(const RomArgs& a) {
+  if (!rom_use_mma() || mma_gat_smem(a.n, a.nx) > 200 * 1024) return rom_grid(a.N);
+  return rom_grid_mma(a.N, a.p, kGatherMmaPerSm);
+}
+template <int D>
+static int launch_rom_gather_any(const RomArgs& a, int G, cudaStream_t s) {
+  if (!rom_use_mma() || mma_gat_smem(a.n, a.nx) > 200 * 1024) return launch_rom_gather<D>(a, G, s);
+  return ROM_NK_DISPATCH(launch_gat_mma_t, D, a, G, s);
+}
+
 static int rom_check(long long N, int n, int p, int nx, int degree) {
   if (N < 1 || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "need N >= 1 and p >= 1");
   if (n < 2 || n > NMAX || (n & 1)) return picrom_set_error(PICROM_ERR_CONFIG, "basis dimension must be even, in [2, 32]");
@@ -1240,12 +1556,12 @@ extern "C" int picrom_rom_field(const double* ux, long long N, int n, const doub
   RomArgs a{};
   a.ux = ux; a.z = z; a.inst = inst; a.cols = cols; a.seg = (double*)ws; a.N = N; a.n = n;
   a.p = p; a.ldz = ldz; a.nx = nx; a.status = status;
-  const int G = rom_grid(N);
+  const int G = degree == 1 ? rom_dep_grid<1>(a) : degree == 2 ? rom_dep_grid<2>(a) : rom_dep_grid<3>(a);
   cudaStream_t s = (cudaStream_t)stream;
   switch (degree) {
-    case 1: rc = launch_rom_deposit<1>(a, G, s); break;
-    case 2: rc = launch_rom_deposit<2>(a, G, s); break;
-    default: rc = launch_rom_deposit<3>(a, G, s); break;
+    case 1: rc = launch_rom_deposit_any<1>(a, G, s); break;
+    case 2: rc = launch_rom_deposit_any<2>(a, G, s); break;
+    default: rc = launch_rom_deposit_any<3>(a, G, s); break;
   }
   if (rc) return rc;
   return picrom_solve_dense(a.seg, G, p, nx, degree, cols, inst, khat, stencil, phi, rho, energy, s);
@@ -1264,12 +1580,12 @@ extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const dou
   a.ux = ux; a.z = z; a.inst = inst; a.cols = cols; a.phi = phi; a.seg = (double*)ws;
   a.lam = lam; a.eout = eout; a.N = N; a.ldo = ldo; a.n = n; a.p = p; a.ldz = ldz; a.nx = nx;
   a.coef_kind = coef_kind; a.status = status;
-  const int G = rom_grid(N);
+  const int G = rom_gat_grid(a);
   cudaStream_t s = (cudaStream_t)stream;
   switch (degree) {
-    case 1: rc = launch_rom_gather<1>(a, G, s); break;
-    case 2: rc = launch_rom_gather<2>(a, G, s); break;
-    default: rc = launch_rom_gather<3>(a, G, s); break;
+    case 1: rc = launch_rom_gather_any<1>(a, G, s); break;
+    case 2: rc = launch_rom_gather_any<2>(a, G, s); break;
+    default: rc = launch_rom_gather_any<3>(a, G, s); break;
   }
   if (rc) return rc;
   if (g_out) {
