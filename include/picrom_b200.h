@@ -215,6 +215,16 @@ int picrom_rom_gather(const double* ux, long long N, int n, const double* z, int
                       double* lam, double* eout, long long ldo, void* workspace,
                       unsigned long long* status, void* stream);
 
+/* As picrom_rom_gather with u the full (2N x n) basis [U_X; U_V] and both
+ * projections of E: g_out = U_X^T E and gv_out = U_V^T E (n x p', ld ldg).
+ * With them the basis velocity's U^T (G Z^T) and U^T J (G Z^T) blocks
+ * (reduction.py:148-153) come from n x n algebra instead of a 2N-row Gram. */
+int picrom_rom_gather_uv(const double* u, long long N, int n, const double* z, int ldz,
+                         int p, const int* cols, const double* inst, int nx, int degree,
+                         const double* phi, int coef_kind, double* g_out, double* gv_out,
+                         int ldg, double* lam, double* eout, long long ldo, void* workspace,
+                         unsigned long long* status, void* stream);
+
 /* out (w x w) = W^T W, W = [B_0 | ... | B_{k-1}] the column concatenation of k
  * tall blocks with N rows (block i: ptrs[i], row stride lds[i], widths[i]
  * columns; jswap[i] = 1 uses J B_i, the block with its row halves swapped and
@@ -224,6 +234,14 @@ int picrom_rom_gather(const double* ux, long long N, int n, const double* z, int
 int picrom_paired_gram(int nblocks, const double* const* ptrs, const int* lds,
                        const int* widths, const int* jswap, long long N, double* out,
                        void* workspace, void* stream);
+
+/* Selected blocks of the paired Gram (same block conventions): for each task
+ * t, out block (bi[t], bj[t]) = B_bi^T B_bj; other entries unspecified; at most
+ * 64 tasks.  tangent_velocity's 7 needed products of [U, xi, r, x_eval]
+ * (reduction.py:170-182) in one pass instead of the 10 of the full Gram. */
+int picrom_gram_tasks(int nblocks, const double* const* ptrs, const int* lds,
+                      const int* widths, const int* jswap, int ntask, const int* bi,
+                      const int* bj, long long N, double* out, void* workspace, void* stream);
 
 /* out (wa x wb) = A^T B with A = blocks [0, na) and B = blocks [na, nblocks)
  * (same block conventions as picrom_paired_gram; total width <= 256):

@@ -46,7 +46,10 @@ SIGNATURES = {
                               _vp, _vp, _vp, _vp]),
     "picrom_rom_gather": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _i,
                                _vp, _vp, _ll, _vp, _vp, _vp]),
+    "picrom_rom_gather_uv": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp,
+                                  _i, _vp, _vp, _ll, _vp, _vp, _vp]),
     "picrom_paired_gram": (_i, [_i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp]),
+    "picrom_gram_tasks": (_i, [_i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _ll, _vp, _vp, _vp]),
     "picrom_cross_gram": (_i, [_i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp]),
     "picrom_argmax_abs": (_i, [_vp, _ll, _ll, _vp, _i, _vp, _vp, _vp, _vp]),
     "picrom_combine": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _i, _i, _i, _vp]),

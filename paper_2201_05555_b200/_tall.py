@@ -3,6 +3,7 @@ operation of the reduced basis is built from).
 
 * ``gram(blocks)``    -> W^T W on the host (numpy), W = column concatenation of
                          tall device blocks, optionally J-applied (picrom_paired_gram)
+* ``gram_tasks``      -> only the listed block products of that Gram (picrom_gram_tasks)
 * ``combine(terms)``  -> sum_t op_t(B_t) @ M_t on the device (picrom_combine)
 
 Tall blocks are row-major float64 CUDA tensors with a common row count; the
@@ -55,6 +56,24 @@ def gram(blocks):
               _arr(C.c_void_p, [t.data_ptr() for t, _ in blocks]),
               _arr(C.c_int, [int(t.stride(0)) for t, _ in blocks]),
               _arr(C.c_int, widths), _arr(C.c_int, [int(bool(j)) for _, j in blocks]),
+              rows, out.data_ptr(), _ws(rows, W).data_ptr(), dev.stream_handle())
+    return out.cpu().numpy()
+
+
+def gram_tasks(blocks, tasks):
+    """Selected block products of gram(blocks): tasks = [(i, j), ...] -> numpy (W x W)
+    with block (i, j) = B_i^T B_j for each task (other entries unspecified)."""
+    rows = blocks[0][0].shape[0]
+    blocks = [(t if t.is_contiguous() else t.contiguous(), j) for t, j in blocks]
+    widths = [int(t.shape[1]) for t, _ in blocks]
+    W = sum(widths)
+    out = torch.empty((W, W), dtype=torch.float64, device="cuda")
+    _lib.call("picrom_gram_tasks", len(blocks),
+              _arr(C.c_void_p, [t.data_ptr() for t, _ in blocks]),
+              _arr(C.c_int, [int(t.stride(0)) for t, _ in blocks]),
+              _arr(C.c_int, widths), _arr(C.c_int, [int(bool(j)) for _, j in blocks]),
+              len(tasks), _arr(C.c_int, [int(i) for i, _ in tasks]),
+              _arr(C.c_int, [int(j) for _, j in tasks]),
               rows, out.data_ptr(), _ws(rows, W).data_ptr(), dev.stream_handle())
     return out.cpu().numpy()
 

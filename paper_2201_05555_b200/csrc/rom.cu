@@ -52,6 +52,8 @@ struct RomArgs {
   int n, p, ldz, nx;
   int coef_kind;        // gather: 0 -> gcoef (exact_gradients), 1 -> raw derivative
   unsigned long long* status;
+  const double* uv;     // gather (DMMA path): optional U_V rows (N x n) -> U_V^T E
+  double* seg2;         // gather: [G][p'][n] partials of U_V^T E
 };
 
 __device__ __forceinline__ long long row_start(int b, long long N, int G) {
@@ -1109,12 +1111,16 @@ __global__ void __launch_bounds__(MW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
     }
     __syncthreads();
     const double* tile = ut + (tt & 1) * TR * n;
-    for (int rb = 0; rb < rows; rb += 8) {
-      double xv[2];
-      recon_block<NK>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
+    // RB row blocks per pass: RB independent DMMA chains, 2 RB units per lane
+    constexpr int RB = 4;
+    for (int rb0 = 0; rb0 < rows; rb0 += 8 * RB) {
+      double xv[2 * RB];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int row = rb + 2 * t + e;
+      for (int q = 0; q < RB; ++q)
+        recon_block<NK>(tile, rb0 + 8 * q, rows, n, za, g, t, xv[2 * q], xv[2 * q + 1]);
+#pragma unroll
+      for (int e = 0; e < 2 * RB; ++e) {
+        const int row = rb0 + 8 * (e >> 1) + 2 * t + (e & 1);
         if (!active || row >= rows) continue;
         const double x = xv[e];
         int cell;
@@ -1152,15 +1158,17 @@ __global__ void __launch_bounds__(MW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
   }
 }
 
-template <int D, int NK>
+template <int D, int NK, bool VPROJ>
 __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int NT = MW * 32;
   constexpr int NM = (4 * NK + 7) / 8;        // 8-row tiles of the projection (n <= 8 NM)
   constexpr int PS = MC + 1;                  // padded phi row (bank spread)
   const int n = a.n, nx = a.nx;
+  constexpr bool vproj = VPROJ;
   double* ut = smem;                          // [2][TR * n]
   double* phs = ut + 2 * TR * n;              // [nx][PS]
+  double* vt = phs + nx * PS;                 // [2][TR * n] U_V rows (vproj)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int cl = warp * 8 + g;
@@ -1177,30 +1185,40 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
   const double cf = a.coef_kind == 0 ? ip[I_GCOEF] : 1.0;
   const double inv_nx = 1.0 / (double)nx;
   const int mask = fast_mask(nx, h);
-  double za[NK], acc[NM][2];
+  double za[NK], acc[NM][2], accv[NM][2];
 #pragma unroll
   for (int ks = 0; ks < NK; ++ks) {
     const int k = ks * 4 + t;
     za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
   }
 #pragma unroll
-  for (int mt = 0; mt < NM; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+  for (int mt = 0; mt < NM; ++mt) acc[mt][0] = acc[mt][1] = accv[mt][0] = accv[mt][1] = 0.0;
   const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
   const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
   const int ntiles = (int)((hi - lo + TR - 1) / TR);
-  if (ntiles > 0) stage_rows(ut, a.ux, lo, (int)min((long long)TR, hi - lo), n);
+  // U_X (and U_V) row tiles, one cp.async group per tile
+  auto stage = [&](int buf, long long r0, int rws) {
+    const int chunks = rws * n / 2;
+    for (int q = threadIdx.x; q < chunks; q += blockDim.x) {
+      cp_async16(ut + buf * TR * n + 2 * q, a.ux + r0 * n + 2 * q);
+      if constexpr (VPROJ) cp_async16(vt + buf * TR * n + 2 * q, a.uv + r0 * n + 2 * q);
+    }
+    cp_async_commit();
+  };
+  if (ntiles > 0) stage(0, lo, (int)min((long long)TR, hi - lo));
   for (int tt = 0; tt < ntiles; ++tt) {
     const long long t0 = lo + (long long)tt * TR;
     const int rows = (int)min((long long)TR, hi - t0);
     if (tt + 1 < ntiles) {
       const long long t1 = t0 + TR;
-      stage_rows(ut + ((tt + 1) & 1) * TR * n, a.ux, t1, (int)min((long long)TR, hi - t1), n);
+      stage((tt + 1) & 1, t1, (int)min((long long)TR, hi - t1));
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
     const double* tile = ut + (tt & 1) * TR * n;
+    const double* vtile = vt + (tt & 1) * TR * n;
     for (int rb = 0; rb < rows; rb += 8) {
       double xv[2], ev[2];
       recon_block<NK>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
@@ -1271,6 +1289,14 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
           const double av = (ur < rows && m < n) ? tile[ur * n + m] : 0.0;
           dmma_f64(acc[mt][0], acc[mt][1], av, b);
         }
+        if constexpr (VPROJ) {
+#pragma unroll
+          for (int mt = 0; mt < NM; ++mt) {
+            const int m = mt * 8 + g;
+            const double av = (ur < rows && m < n) ? vtile[ur * n + m] : 0.0;
+            dmma_f64(accv[mt][0], accv[mt][1], av, b);
+          }
+        }
       }
     }
     __syncthreads();
@@ -1282,7 +1308,10 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
     for (int e = 0; e < 2; ++e) {
       const int m = mt * 8 + g;
       const int col = blockIdx.y * MC + warp * 8 + 2 * t + e;
-      if (m < n && col < a.p) a.seg[((size_t)blockIdx.x * a.p + col) * n + m] = acc[mt][e];
+      if (m < n && col < a.p) {
+        a.seg[((size_t)blockIdx.x * a.p + col) * n + m] = acc[mt][e];
+        if constexpr (VPROJ) a.seg2[((size_t)blockIdx.x * a.p + col) * n + m] = accv[mt][e];
+      }
     }
 }
 
@@ -1421,7 +1450,7 @@ combine_mma_kernel(Terms t, MmaTerms mt, const double* mats, long long N) {
 extern "C" size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx) {
   const size_t G = (size_t)std::max(rom_grid(N), rom_grid_mma(N, p, kGatherMmaPerSm));
   const size_t dep = G * p * nx;
-  const size_t gat = G * p * n;
+  const size_t gat = 2 * G * p * n;        // U_X^T E and U_V^T E partials
   const size_t gram = (size_t)gram_grid(N) * 256 * 256;
   return std::max(std::max(dep, gat), gram) * sizeof(double) + 256;
 }
@@ -1491,8 +1520,8 @@ static int mma_nk(int n) { return n <= 8 ? 2 : n <= 16 ? 4 : n <= 20 ? 5 : 8; }
 static size_t mma_dep_smem(int n, int nx, int D) {
   return ((size_t)2 * TR * n + (size_t)(nx + D) * MW * 32) * sizeof(double);
 }
-static size_t mma_gat_smem(int n, int nx) {
-  return ((size_t)2 * TR * n + (size_t)nx * (MC + 1)) * sizeof(double);
+static size_t mma_gat_smem(int n, int nx, bool vproj = false) {
+  return ((size_t)(vproj ? 4 : 2) * TR * n + (size_t)nx * (MC + 1)) * sizeof(double);
 }
 
 template <int D, int NK>
@@ -1505,10 +1534,18 @@ static int launch_dep_mma_t(const RomArgs& a, int G, cudaStream_t s) {
 }
 template <int D, int NK>
 static int launch_gat_mma_t(const RomArgs& a, int G, cudaStream_t s) {
-  auto kfn = rom_gather_mma_kernel<D, NK>;
-  static bool attr = false;
-  if (!attr) { rom_allow_smem(kfn); attr = true; }
-  kfn<<<dim3(G, (a.p + MC - 1) / MC), MW * 32, mma_gat_smem(a.n, a.nx), s>>>(a);
+  const dim3 grid(G, (a.p + MC - 1) / MC);
+  if (a.uv) {
+    auto kfn = rom_gather_mma_kernel<D, NK, true>;
+    static bool attr = false;
+    if (!attr) { rom_allow_smem(kfn); attr = true; }
+    kfn<<<grid, MW * 32, mma_gat_smem(a.n, a.nx, true), s>>>(a);
+  } else {
+    auto kfn = rom_gather_mma_kernel<D, NK, false>;
+    static bool attr = false;
+    if (!attr) { rom_allow_smem(kfn); attr = true; }
+    kfn<<<grid, MW * 32, mma_gat_smem(a.n, a.nx, false), s>>>(a);
+  }
   return picrom_check_launch("rom_gather_mma_kernel");
 }
 #define ROM_NK_DISPATCH(FN, D, A, G, S)                                              \
@@ -1527,11 +1564,17 @@ static int launch_rom_deposit_any(const RomArgs& a, int G, cudaStream_t s) {
   return ROM_NK_DISPATCH(launch_dep_mma_t, D, a, G, s);
 }
 static int rom_gat_grid(const RomArgs& a) {
+  if (a.uv) return rom_grid_mma(a.N, a.p, 2);     // 94 registers: 2 CTAs per SM
   if (!rom_use_mma() || mma_gat_smem(a.n, a.nx) > 200 * 1024) return rom_grid(a.N);
   return rom_grid_mma(a.N, a.p, kGatherMmaPerSm);
 }
 template <int D>
 static int launch_rom_gather_any(const RomArgs& a, int G, cudaStream_t s) {
+  if (a.uv) {   // the U_V projection exists only on the DMMA path
+    if (mma_gat_smem(a.n, a.nx, true) > 200 * 1024)
+      return picrom_set_error(PICROM_ERR_CONFIG, "rom gather: nx too large for the U_V projection");
+    return ROM_NK_DISPATCH(launch_gat_mma_t, D, a, G, s);
+  }
   if (!rom_use_mma() || mma_gat_smem(a.n, a.nx) > 200 * 1024) return launch_rom_gather<D>(a, G, s);
   return ROM_NK_DISPATCH(launch_gat_mma_t, D, a, G, s);
 }
@@ -1569,11 +1612,11 @@ extern "C" int picrom_rom_field(const double* ux, long long N, int n, const doub
 
 // Gather + projection: g_out (n x p', ld ldg) = U_X^T E with E = coef d/dx
 // (phi . lambda)(U_X Z); lam/eout optional (p', ldo).
-extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const double* z, int ldz,
-                                 int p, const int* cols, const double* inst, int nx, int degree,
-                                 const double* phi, int coef_kind, double* g_out, int ldg,
-                                 double* lam, double* eout, long long ldo, void* ws,
-                                 unsigned long long* status, void* stream) {
+static int rom_gather_impl(const double* ux, long long N, int n, const double* z, int ldz, int p,
+                           const int* cols, const double* inst, int nx, int degree,
+                           const double* phi, int coef_kind, double* g_out, int ldg,
+                           double* gv_out, double* lam, double* eout, long long ldo, void* ws,
+                           unsigned long long* status, void* stream) {
   int rc = rom_check(N, n, p, nx, degree);
   if (rc) return rc;
   RomArgs a{};
@@ -1581,6 +1624,10 @@ extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const dou
   a.lam = lam; a.eout = eout; a.N = N; a.ldo = ldo; a.n = n; a.p = p; a.ldz = ldz; a.nx = nx;
   a.coef_kind = coef_kind; a.status = status;
   const int G = rom_gat_grid(a);
+  if (gv_out) {
+    a.uv = ux + (size_t)N * n;
+    a.seg2 = a.seg + (size_t)G * p * n;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   switch (degree) {
     case 1: rc = launch_rom_gather_any<1>(a, G, s); break;
@@ -1588,12 +1635,40 @@ extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const dou
     default: rc = launch_rom_gather_any<3>(a, G, s); break;
   }
   if (rc) return rc;
+  const int rows = p * n;
   if (g_out) {
-    const int rows = p * n;
     seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg, G, rows, g_out, ldg, 1, n);
-    return picrom_check_launch("seg_sum");
+    rc = picrom_check_launch("seg_sum");
+    if (rc) return rc;
   }
-  return PICROM_OK;
+  if (gv_out) {
+    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg2, G, rows, gv_out, ldg, 1, n);
+    rc = picrom_check_launch("seg_sum");
+  }
+  return rc;
+}
+
+extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const double* z, int ldz,
+                                 int p, const int* cols, const double* inst, int nx, int degree,
+                                 const double* phi, int coef_kind, double* g_out, int ldg,
+                                 double* lam, double* eout, long long ldo, void* ws,
+                                 unsigned long long* status, void* stream) {
+  return rom_gather_impl(ux, N, n, z, ldz, p, cols, inst, nx, degree, phi, coef_kind, g_out, ldg,
+                         nullptr, lam, eout, ldo, ws, status, stream);
+}
+
+// Gather with both projections of E: g_out = U_X^T E and gv_out = U_V^T E
+// (n x p', ld ldg), U = ux the full (2N x n) basis; used by exact_gradients so
+// the basis velocity's U^T G Z^T products need no pass over G (reduction.py:148-153).
+extern "C" int picrom_rom_gather_uv(const double* u, long long N, int n, const double* z,
+                                    int ldz, int p, const int* cols, const double* inst, int nx,
+                                    int degree, const double* phi, int coef_kind, double* g_out,
+                                    double* gv_out, int ldg, double* lam, double* eout,
+                                    long long ldo, void* ws, unsigned long long* status,
+                                    void* stream) {
+  if (!g_out || !gv_out) return picrom_set_error(PICROM_ERR_CONFIG, "rom_gather_uv: need g_out and gv_out");
+  return rom_gather_impl(u, N, n, z, ldz, p, cols, inst, nx, degree, phi, coef_kind, g_out, ldg,
+                         gv_out, lam, eout, ldo, ws, status, stream);
 }
 
 // Gram of the row-concatenation W = [B_0 | B_1 | ...] (N rows): out (w x w).
@@ -1623,14 +1698,16 @@ static int launch_gram_mma(const Blocks& b, const GramTasks& tk, int na, long lo
 }
 
 static int gram_mma_try(const Blocks& b, int na, long long N, void* ws, cudaStream_t s,
-                        double* out) {
+                        double* out, const GramTasks* tasks = nullptr) {
   if (getenv("PICROM_GRAM_NO_MMA") || N < 1024) return -1;
   const int wdt = b.w[0];
   if (wdt > 32 || wdt < 2 || (wdt & 1)) return -1;
   for (int i = 0; i < b.nb; ++i)
     if (b.w[i] != wdt || b.ld[i] != wdt || (reinterpret_cast<uintptr_t>(b.ptr[i]) & 15)) return -1;
   GramTasks tk{};
-  if (na == 0) {
+  if (tasks) {
+    tk = *tasks;
+  } else if (na == 0) {
     for (int i = 0; i < b.nb; ++i)
       for (int j = i; j < b.nb; ++j) { tk.bi[tk.ntask] = (unsigned char)i; tk.bj[tk.ntask] = (unsigned char)j; ++tk.ntask; }
   } else {
@@ -1729,6 +1806,36 @@ extern "C" int picrom_cross_gram(int nblocks, int na, const double* const* ptrs,
   return gram_impl(nblocks, na, ptrs, lds, widths, jswap, N, out, ws, stream);
 }
 
+// Selected blocks of the Gram W^T W: out (w x w) holds B_bi[t]^T B_bj[t] at
+// block (bi[t], bj[t]) for each task t; the other entries are unspecified.
+// Only the requested products are computed (tangent_velocity needs 7 of the
+// 10 block pairs of [U, xi, r, x_eval], reduction.py:170-182).
+extern "C" int picrom_gram_tasks(int nblocks, const double* const* ptrs, const int* lds,
+                                 const int* widths, const int* jswap, int ntask, const int* bi,
+                                 const int* bj, long long N, double* out, void* ws, void* stream) {
+  if (nblocks < 1 || nblocks > MAXB) return picrom_set_error(PICROM_ERR_CONFIG, "1..8 blocks");
+  if (ntask < 1 || ntask > MAXTASK) return picrom_set_error(PICROM_ERR_CONFIG, "gram_tasks: bad task count");
+  Blocks b{};
+  b.nb = nblocks;
+  b.off[0] = 0;
+  for (int i = 0; i < nblocks; ++i) {
+    b.ptr[i] = ptrs[i]; b.ld[i] = lds[i]; b.w[i] = widths[i];
+    b.jswap[i] = jswap ? jswap[i] : 0;
+    b.off[i + 1] = b.off[i] + widths[i];
+  }
+  GramTasks tk{};
+  for (int t = 0; t < ntask; ++t) {
+    if (bi[t] < 0 || bj[t] < 0 || bi[t] >= nblocks || bj[t] >= nblocks)
+      return picrom_set_error(PICROM_ERR_CONFIG, "gram_tasks: block index out of range");
+    tk.bi[t] = (unsigned char)bi[t];
+    tk.bj[t] = (unsigned char)bj[t];
+  }
+  tk.ntask = ntask;
+  const int rc = gram_mma_try(b, 0, N, ws, (cudaStream_t)stream, out, &tk);
+  if (rc != -1) return rc;
+  return gram_impl(nblocks, 0, ptrs, lds, widths, jswap, N, out, ws, stream);   // all blocks
+}
+
 extern "C" int picrom_argmax_abs(const double* v, long long n, long long stride,
                                  const long long* banned, int nbanned, long long* out_index,
                                  double* out_value, void* ws, void* stream) {
@@ -1746,6 +1853,104 @@ extern "C" int picrom_argmax_abs(const double* v, long long n, long long stride,
 
 // out (N x c) (+)= sum_t in_t (N x a_t) @ M_t (a_t x c); mats is a device buffer
 // holding the M_t back to back (offsets moffs, in doubles).
+// Combine with a wide term (a_t > 32, e.g. the N x p' field block E times a
+// p' x n matrix in the basis velocity): A streams from global straight into
+// DMMA fragments (lane (g, t) reads row g, column 4 ks + t: every 32-byte
+// sector read once), M sits in smem with a pitch = 4 mod 16 (conflict-free B
+// fragments), and a warp owns 32 rows = 4 row blocks x TBO column tiles of
+// independent accumulators.
+constexpr int WRB = 4;          // 8-row blocks per warp chunk
+template <int TBO>
+__global__ void __launch_bounds__(256, 2) wide_combine_kernel(Terms t, const double* mats,
+                                                           long long N, int cp) {
+  extern __shared__ __align__(16) double wsm[];
+  int koff[MAXTERM + 1];
+  koff[0] = 0;
+  for (int i = 0; i < t.nt; ++i) koff[i + 1] = koff[i] + ((t.a[i] + 3) & ~3);
+  const int K = koff[t.nt];
+  const int c = t.c;
+  for (int q = threadIdx.x; q < K * cp; q += blockDim.x) {
+    const int k = q / cp, j = q - k * cp;
+    int ti = 0;
+    while (k >= koff[ti + 1]) ++ti;
+    const int kk = k - koff[ti];
+    wsm[q] = (kk < t.a[ti] && j < c) ? mats[t.moff[ti] + kk * c + j] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const long long half = N / 2;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r0 = gw * 8 * WRB; r0 < N; r0 += nw * 8 * WRB) {
+    double acc[WRB][TBO][2];
+#pragma unroll
+    for (int q = 0; q < WRB; ++q)
+#pragma unroll
+      for (int j = 0; j < TBO; ++j) acc[q][j][0] = acc[q][j][1] = 0.0;
+    for (int ti = 0; ti < t.nt; ++ti) {
+      const double* base[WRB];
+      double sg[WRB];
+      bool rv[WRB];
+#pragma unroll
+      for (int q = 0; q < WRB; ++q) {
+        long long row = r0 + 8 * q + g;
+        rv[q] = row < N;
+        sg[q] = (t.jswap[ti] && row >= half) ? -1.0 : 1.0;
+        if (t.jswap[ti]) row = row < half ? row + half : row - half;
+        base[q] = t.in[ti] + (size_t)(rv[q] ? row : 0) * t.ld[ti];
+      }
+      const int a = t.a[ti];
+      const double* mrow = wsm + (size_t)koff[ti] * cp + g;
+#pragma unroll 4
+      for (int k0 = 0; k0 < a; k0 += 4) {
+        const int k = k0 + tq;
+        double av[WRB], bv[TBO];
+#pragma unroll
+        for (int q = 0; q < WRB; ++q) av[q] = (rv[q] && k < a) ? sg[q] * __ldcs(base[q] + k) : 0.0;
+#pragma unroll
+        for (int j = 0; j < TBO; ++j) bv[j] = mrow[(size_t)k * cp + 8 * j];
+#pragma unroll
+        for (int q = 0; q < WRB; ++q)
+#pragma unroll
+          for (int j = 0; j < TBO; ++j) dmma(acc[q][j][0], acc[q][j][1], av[q], bv[j]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < WRB; ++q) {
+      const long long row = r0 + 8 * q + g;
+      if (row >= N) continue;
+      double* orow = t.out + (size_t)row * t.ldo;
+#pragma unroll
+      for (int j = 0; j < TBO; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * j + 2 * tq + e;
+          if (col < c) orow[col] = t.accumulate ? orow[col] + acc[q][j][e] : acc[q][j][e];
+        }
+    }
+  }
+}
+
+static int launch_wide_combine(const Terms& t, const double* mats, long long N, cudaStream_t s) {
+  int K = 0;
+  for (int i = 0; i < t.nt; ++i) K += (t.a[i] + 3) & ~3;
+  const int tbo = (t.c + 7) / 8;
+  int cp = 8 * tbo;
+  while (cp % 16 != 4) ++cp;
+  const size_t sm = (size_t)K * cp * sizeof(double);
+  if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
+  const long long chunks = (N + 8 * WRB - 1) / (8 * WRB);
+  const int G = (int)std::max<long long>(1, std::min<long long>(2LL * picrom_num_sms(), (chunks + 7) / 8));
+  switch (tbo) {
+    case 1: rom_allow_smem(wide_combine_kernel<1>); wide_combine_kernel<1><<<G, 256, sm, s>>>(t, mats, N, cp); break;
+    case 2: rom_allow_smem(wide_combine_kernel<2>); wide_combine_kernel<2><<<G, 256, sm, s>>>(t, mats, N, cp); break;
+    case 3: rom_allow_smem(wide_combine_kernel<3>); wide_combine_kernel<3><<<G, 256, sm, s>>>(t, mats, N, cp); break;
+    default: rom_allow_smem(wide_combine_kernel<4>); wide_combine_kernel<4><<<G, 256, sm, s>>>(t, mats, N, cp); break;
+  }
+  return picrom_check_launch("wide_combine_kernel");
+}
+
 extern "C" int picrom_combine(int nterms, const double* const* ins, const int* lds,
                               const int* widths, const int* jswap, const int* moffs,
                               const double* mats, int mats_len, long long N, double* out,
@@ -1762,6 +1967,10 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
   const size_t sm = (size_t)mats_len * sizeof(double);
   if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
   cudaStream_t s = (cudaStream_t)stream;
+  bool wide = false;
+  for (int i = 0; i < nterms; ++i) wide |= widths[i] > 32;
+  if (wide && getenv("PICROM_COMBINE_NO_WIDE") == nullptr && N >= 1024)
+    return launch_wide_combine(t, mats, N, s);
   // DMMA path: even widths, rows 16-B aligned (ld even, 16-B aligned base)
   bool mma = getenv("PICROM_COMBINE_NO_MMA") == nullptr && N >= 1024;
   MmaTerms mt{};

@@ -138,8 +138,10 @@ class DeviceGradient:
     E (N x p') on the device plus (U, z).  ``times_matrix(M)`` = G @ M as two
     combines; ``dense()`` materialises G (API / tests)."""
 
-    def __init__(self, u, z, e):
+    def __init__(self, u, z, e, ux_e=None, uv_e=None):
         self.u, self.z, self.e = u, np.asarray(z, dtype=float), e
+        # U_X^T E and U_V^T E (n x p') from the same gather pass (host arrays)
+        self.ux_e, self.uv_e = ux_e, uv_e
 
     @property
     def shape(self):
@@ -171,13 +173,15 @@ def exact_gradients_device(system, ud, z, cols=None, harvest=True):
     zd, inst, phi, _, st = _field_device(system, ud, z, colmap)
     e = torch.empty((N, p), dtype=torch.float64, device="cuda")
     lam = torch.empty((N, p), dtype=torch.float64, device="cuda") if harvest else None
+    proj = torch.empty((2, n, p), dtype=torch.float64, device="cuda")
     mesh = system.mesh
-    _lib.call("picrom_rom_gather", ud.data_ptr(), N, n, zd.data_ptr(), p, p, colmap.ptr,
-              inst.data_ptr(), mesh.num_cells, mesh.degree, phi.data_ptr(), 0, None, 0,
-              dev.ptr(lam), e.data_ptr(), p, _rom_ws(N, p, n, mesh.num_cells).data_ptr(),
-              st.data_ptr(), dev.stream_handle())
+    _lib.call("picrom_rom_gather_uv", ud.data_ptr(), N, n, zd.data_ptr(), p, p, colmap.ptr,
+              inst.data_ptr(), mesh.num_cells, mesh.degree, phi.data_ptr(), 0,
+              proj[0].data_ptr(), proj[1].data_ptr(), p, dev.ptr(lam), e.data_ptr(), p,
+              _rom_ws(N, p, n, mesh.num_cells).data_ptr(), st.data_ptr(), dev.stream_handle())
     _raise_eval(st, p)
-    return DeviceGradient(ud, z, e), phi, lam
+    ph = proj.cpu().numpy()
+    return DeviceGradient(ud, z, e, ph[0], ph[1]), phi, lam
 
 
 def exact_gradients(system, u, z):

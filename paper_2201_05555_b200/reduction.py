@@ -58,8 +58,36 @@ def jrmul(m):
     return np.concatenate([-m[:, half:], m[:, :half]], axis=1)
 
 
+class Scaled:
+    """c * a for a tall device operand, kept lazy: retraction and
+    tangent_velocity fold c into their Gram blocks and combine coefficients,
+    so the PRK step's dt/2 * xi and dt * xi2 (reduction.py:236,258) cost no pass."""
+
+    def __init__(self, a, c):
+        self.a, self.c = a, float(c)
+
+    @property
+    def shape(self):
+        return self.a.shape
+
+    def materialize(self):
+        ad, _ = _tall_in(self.a)
+        return _tall.combine([(ad, self.c * np.eye(ad.shape[1]), False)])
+
+
+def _scaled_in(a):
+    """(CUDA tensor, scale, was_numpy) of a possibly lazy-scaled tall operand."""
+    if isinstance(a, Scaled):
+        t, _ = _tall_in(a.a)
+        return t, a.c, False
+    t, was_np = _tall_in(a)
+    return t, 1.0, was_np
+
+
 def _tall_in(a):
     """(CUDA tensor, was_numpy) for a tall operand."""
+    if isinstance(a, Scaled):
+        return a.materialize(), False
     if isinstance(a, torch.Tensor):
         return a.to(device="cuda", dtype=torch.float64).contiguous(), False
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda"), True
@@ -173,14 +201,42 @@ def basis_velocity(u, z, g, s=None):
     z = np.asarray(z, dtype=float)
     s = s or SMatrix(z)
     n = ud.shape[1]
-    gzt = _times_zt(g, z)
-    G = _tall.gram([(ud, False), (gzt, False), (gzt, True)])
-    u_gzt, u_jgzt = G[:n, n:2 * n], G[:n, 2 * n:]
     s_inv = s.solve_right(np.eye(n))
     js_inv = jmul(s_inv)                         # (G Z^T J) S^-1 = G Z^T (J S^-1)
+    if getattr(g, "ux_e", None) is not None:
+        return _tall_out(_basis_velocity_device(ud, z, g, s_inv, js_inv), was_np)
+    gzt = _times_zt(g, z)
+    G = _tall.gram_tasks([(ud, False), (gzt, False), (gzt, True)], [(0, 1), (0, 2)])
+    u_gzt, u_jgzt = G[:n, n:2 * n], G[:n, 2 * n:]
     q = u_jgzt @ s_inv + u_gzt @ js_inv          # U^T m
     xi = _tall.combine([(gzt, s_inv, True), (gzt, js_inv, False), (ud, -q, False)])
     return _tall_out(xi, was_np)
+
+
+def _basis_velocity_device(ud, z, g, s_inv, js_inv):
+    """basis_velocity for an implicit device gradient G = [E; U_V Z] whose gather
+    also returned U_X^T E and U_V^T E: with H = Z Z^T and the n x n blocks
+    C_ab = U_a^T U_b of U (one Gram of its halves),
+        U^T G Z^T   = (U_X^T E) Z^T + C_VV H
+        U^T J G Z^T = C_XV H - (U_V^T E) Z^T
+    and xi = J G Z^T S^-1 + G Z^T J S^-1 - U Q splits by halves into
+        xi_X = E (Z^T J S^-1) + U_V (H S^-1) - U_X Q
+        xi_V = E (-Z^T S^-1)  + U_V (H J S^-1 - Q),
+    two combines over E and U: no G Z^T and no 2N-row Gram."""
+    N = ud.shape[0] // 2
+    n = ud.shape[1]
+    ux, uv = ud[:N], ud[N:]
+    C = _tall.gram([(ux, False), (uv, False)])
+    cxv, cvv = C[:n, n:], C[n:, n:]
+    zt = z.T
+    H = z @ zt
+    u_gzt = g.ux_e @ zt + cvv @ H
+    u_jgzt = cxv @ H - g.uv_e @ zt
+    q = u_jgzt @ s_inv + u_gzt @ js_inv
+    out = torch.empty((2 * N, n), dtype=torch.float64, device="cuda")
+    _tall.combine([(g.e, zt @ js_inv, False), (uv, H @ s_inv, False), (ux, -q, False)], out=out[:N])
+    _tall.combine([(g.e, -(zt @ s_inv), False), (uv, H @ js_inv - q, False)], out=out[N:])
+    return out
 
 
 def _retraction_coeffs(G, n):
@@ -197,25 +253,33 @@ def _retraction_coeffs(G, n):
 def retraction(u, xi):
     """Low-rank Cayley retraction cay(W U^T - U W^T) U (reduction.py:156-167):
     u + [w, -u] cap^{-1} [u, w]^T u with w = xi - U (U^T xi)/2, assembled from
-    the Gram of [U, xi] as U (I - M Y1/2 - Y2) + xi Y1."""
+    the Gram of [U, xi] as U (I - M Y1/2 - Y2) + xi Y1.  xi may be a lazy
+    Scaled(x, c): the Gram of [U, x] is rescaled on the host."""
     ud, was_np = _tall_in(u)
-    xd, _ = _tall_in(xi)
+    xd, c, _ = _scaled_in(xi)
     n = ud.shape[1]
-    cu, cx = _retraction_coeffs(_tall.gram([(ud, False), (xd, False)]), n)
-    return _tall_out(_tall.combine([(ud, cu, False), (xd, cx, False)]), was_np)
+    G = _tall.gram([(ud, False), (xd, False)])
+    G[:n, n:] *= c
+    G[n:, :n] *= c
+    G[n:, n:] *= c * c
+    cu, cx = _retraction_coeffs(G, n)
+    return _tall_out(_tall.combine([(ud, cu, False), (xd, c * cx, False)]), was_np)
 
 
 def tangent_velocity(u, xi, r_xi, x_eval):
-    """Pull a velocity at r_xi = retraction(u, xi) back to u (reduction.py:170-182)."""
+    """Pull a velocity at r_xi = retraction(u, xi) back to u (reduction.py:170-182).
+    Only the 7 needed block products of [U, xi, r, x_eval] are formed; xi and
+    x_eval may be lazy Scaled operands."""
     ud, was_np = _tall_in(u)
-    xd, _ = _tall_in(xi)
+    xd, cxi, _ = _scaled_in(xi)
     rd, _ = _tall_in(r_xi)
-    ed, _ = _tall_in(x_eval)
+    ed, cev, _ = _scaled_in(x_eval)
     n = ud.shape[1]
-    G = _tall.gram([(ud, False), (xd, False), (rd, False), (ed, False)])
+    G = _tall.gram_tasks([(ud, False), (xd, False), (rd, False), (ed, False)],
+                         [(0, 0), (0, 1), (0, 2), (0, 3), (1, 3), (2, 1), (2, 3)])
     b = _tall.split(G, [n, n, n, n])
-    P, M, R, E = b[0][0], b[0][1], b[0][2], b[0][3]
-    F, rxi, rxe = b[1][3], b[2][1], b[2][3]
+    P, M, R, E = b[0][0], cxi * b[0][1], b[0][2], cev * b[0][3]
+    F, rxi, rxe = cxi * cev * b[1][3], cxi * b[2][1], cev * b[2][3]
     eye = np.eye(n)
     t_u = 0.5 * M @ E + F - 0.5 * M.T @ E         # t = 2 x_eval - xi E + u t_u
     K = np.linalg.inv(R + eye)                     # ups = t (U^T r + I)^-1
@@ -223,14 +287,17 @@ def tangent_velocity(u, xi, r_xi, x_eval):
     rt_ups = rxe @ c_e + rxi @ c_x + R.T @ c_u
     ut_ups = E @ c_e + M @ c_x + P @ c_u
     lead = np.linalg.solve(R.T + eye, rt_ups + ut_ups)
-    out = _tall.combine([(ed, c_e, False), (xd, c_x, False), (ud, c_u - lead - ut_ups.T, False)])
+    out = _tall.combine([(ed, cev * c_e, False), (xd, cxi * c_x, False),
+                         (ud, c_u - lead - ut_ups.T, False)])
     return _tall_out(out, was_np)
 
 
 def scaled(a, c):
-    """c * a for a tall device operand (the combine kernel with c*I)."""
-    ad, was_np = _tall_in(a)
-    return _tall_out(_tall.combine([(ad, c * np.eye(ad.shape[1]), False)]), was_np)
+    """c * a: a lazy Scaled for device operands (folded into the next Gram and
+    combine), a plain product for host arrays."""
+    if isinstance(a, np.ndarray):
+        return c * a
+    return Scaled(a, c)
 
 
 def fixed_point(map_fn, z0, tol=1e-9, max_iter=100):

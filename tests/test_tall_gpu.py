@@ -103,3 +103,25 @@ def test_combine_terms(lib_built, rows):
     _tall.combine([(torch.from_numpy(x).cuda(), m1, False)], out=out, accumulate=True)
     ref2 = ref + x @ m1
     assert np.abs(out.cpu().numpy() - ref2).max() <= 1e-12 * np.abs(ref2).max()
+
+
+@pytest.mark.parametrize("rows", [1030, 2 * 25013])
+@pytest.mark.parametrize("c", [7, 20, 32])
+def test_combine_wide_term(lib_built, rows, c):
+    """The wide-term combine (a 128- or 130-wide block, as E (N x p') in the basis
+    velocity) with narrow and J-applied terms, into a strided output half."""
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(rows + c)
+    e = rng.standard_normal((rows, 130))
+    x = rng.standard_normal((rows, 20))
+    y = rng.standard_normal((rows, 20))
+    me, mx, my = (rng.standard_normal((130, c)), rng.standard_normal((20, c)),
+                  rng.standard_normal((20, c)))
+    out = torch.zeros((2 * rows, c), dtype=torch.float64, device="cuda")
+    _tall.combine([(torch.from_numpy(e).cuda(), me, False), (torch.from_numpy(x).cuda(), mx, False),
+                   (torch.from_numpy(y).cuda(), my, True)], out=out[rows:])
+    ref = e @ me + x @ mx + _j(y) @ my
+    got = out.cpu().numpy()
+    assert np.abs(got[rows:] - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert not got[:rows].any()
