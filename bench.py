@@ -301,6 +301,14 @@ def run_ours(args, w, rank, world, local_rank):
         "clocks": clk,
         "cpu_baseline": cpu,
     }
+    if world == 1 and not args.no_rom:
+        # the reduced-basis step (BASELINE configs[2], C3) on the same GPU,
+        # reported beside the headline FOM line (tools/bench_rom.py)
+        del ens, rec
+        torch.cuda.empty_cache()
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_rom
+        line["reduced_step"] = bench_rom.measure("C3", steps=5, warmup=2)
     print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
@@ -315,6 +323,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rom", action="store_true", help="skip the reduced-step (C3) section")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -1072,29 +1072,41 @@ __device__ __forceinline__ void recon_block(const double* tile, int rb, int rows
   }
 }
 
+// Deposit: DW = 16 warps x 8 columns = 128 columns per CTA (all of C3's p in
+// one column tile, so U_X is staged once).  The lanes t and t^1 of a column
+// share one histogram (2 copies per column, [nh][2 DC]) and take turns (two
+// predicated phases): half the smem per lane of private histograms, which
+// buys 16 resident warps instead of 8 (the kernel is latency-bound).
+constexpr int DW = 16;           // warps per deposit CTA
+constexpr int DC = DW * 8;       // z columns per deposit CTA
 template <int D, int NK>
-__global__ void __launch_bounds__(MW * 32, 1) rom_deposit_mma_kernel(RomArgs a) {
+__global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) {
   extern __shared__ __align__(16) double smem[];
-  constexpr int NT = MW * 32;
+  constexpr int NT = DW * 32;
+  constexpr int HS = DC * 2;                  // histograms (row stride)
   const int n = a.n, nx = a.nx, nh = nx + D;
   double* ut = smem;                          // [2][TR * n]
-  double* hist = ut + 2 * TR * n;             // [nh][NT] private per lane
+  double* hist = ut + 2 * TR * n;             // [nh][HS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int c = blockIdx.y * MC + warp * 8 + g;
+  const int cl = warp * 8 + g;
+  const int c = blockIdx.y * DC + cl;
   const bool active = c < a.p;
   const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
   const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
   const double h = ip[I_H], inv_h = ip[I_INVH];
   const double inv_nx = 1.0 / (double)nx;
   const int mask = fast_mask(nx, h);
+  // histogram of (column, t/2): bank = 2 cl + t/2 mod 16 -- distinct over the
+  // 8 lanes of one phase in each half-warp
+  const unsigned int hbase = smem_u32(hist + 2 * cl + (t >> 1));
   double za[NK];
 #pragma unroll
   for (int ks = 0; ks < NK; ++ks) {
     const int k = ks * 4 + t;
     za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
   }
-  for (int q = tid; q < nh * NT; q += NT) hist[q] = 0.0;
+  for (int q = tid; q < nh * HS; q += NT) hist[q] = 0.0;
   const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
   const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
   const int ntiles = (int)((hi - lo + TR - 1) / TR);
@@ -1112,49 +1124,62 @@ __global__ void __launch_bounds__(MW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
     __syncthreads();
     const double* tile = ut + (tt & 1) * TR * n;
     // RB row blocks per pass: RB independent DMMA chains, 2 RB units per lane
-    constexpr int RB = 4;
+    constexpr int RB = 2;
     for (int rb0 = 0; rb0 < rows; rb0 += 8 * RB) {
       double xv[2 * RB];
 #pragma unroll
       for (int q = 0; q < RB; ++q)
         recon_block<NK>(tile, rb0 + 8 * q, rows, n, za, g, t, xv[2 * q], xv[2 * q + 1]);
+      double w[2 * RB][D + 1];
+      unsigned int hrow[2 * RB];
+      bool act[2 * RB];
 #pragma unroll
       for (int e = 0; e < 2 * RB; ++e) {
         const int row = rb0 + 8 * (e >> 1) + 2 * t + (e & 1);
-        if (!active || row >= rows) continue;
+        act[e] = active && row < rows;
         const double x = xv[e];
         int cell;
         double f;
         bool rare;
         locate_fast(x, h, inv_h, nx, mask, inv_nx, cell, f, rare);
-        if (rare) {
+        if (act[e] && rare) {
           if (!isfinite(x)) {
             record_bad(a.status, 0, t0 + row, c, a.p);
-            continue;
+            act[e] = false;
+            cell = 0;
+            f = 0.0;
+          } else {
+            locate(x, h, inv_h, nx, inv_nx, cell, f);
           }
-          locate(x, h, inv_h, nx, inv_nx, cell, f);
         }
-        double w[D + 1];
-        Spline<D>::weights(f, w);
-        double* hp = hist + cell * NT + tid;
-        double cur[D + 1];
+        Spline<D>::weights(f, w[e]);
+        hrow[e] = hbase + (unsigned int)(act[e] ? cell : 0) * (unsigned int)(HS * 8);
+      }
+      // lanes t = 0, 2 then t = 1, 3 (the two lanes of a histogram)
 #pragma unroll
-        for (int m = 0; m <= D; ++m) cur[m] = hp[m * NT];
+      for (int ph = 0; ph < 2; ++ph) {
 #pragma unroll
-        for (int m = 0; m <= D; ++m) hp[m * NT] = cur[m] + w[m];
+        for (int e = 0; e < 2 * RB; ++e) {
+          const bool on = act[e] && (t & 1) == ph;
+          double cur[D + 1];
+#pragma unroll
+          for (int m = 0; m <= D; ++m) cur[m] = lds_f64_if(hrow[e] + m * HS * 8u, on);
+#pragma unroll
+          for (int m = 0; m <= D; ++m) sts_f64_if(hrow[e] + m * HS * 8u, cur[m] + w[e][m], on);
+        }
+        __syncwarp();
       }
     }
     __syncthreads();
   }
-  // fold ghost rows and the 4 copies per column (fixed order) -> seg[b][c][nd]
-  const int P_used = min(MC, a.p - blockIdx.y * MC);
+  // fold ghost rows and the 2 copies per column (fixed order) -> seg[b][c][nd]
+  const int P_used = min(DC, a.p - blockIdx.y * DC);
   for (int q = tid; q < P_used * nx; q += NT) {
-    const int cl = q / nx, nd = q % nx;
-    const int t_base = (cl >> 3) * 32 + (cl & 7) * 4;
+    const int cc = q / nx, nd = q % nx;
     double s = 0.0;
     for (int rr = (nd - Spline<D>::OFF) % nx; rr < nh; rr += nx)
-      for (int cp = 0; cp < 4; ++cp) s += hist[rr * NT + t_base + cp];
-    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * MC + cl) * nx + nd] = s;
+      s += hist[rr * HS + 2 * cc] + hist[rr * HS + 2 * cc + 1];
+    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * DC + cc) * nx + nd] = s;
   }
 }
 
@@ -1518,7 +1543,7 @@ static int launch_rom_gather(const RomArgs& a, int G, cudaStream_t s) {
 // DMMA path: k-steps NK = ceil(n / 4) rounded up to {2, 4, 5, 8}
 static int mma_nk(int n) { return n <= 8 ? 2 : n <= 16 ? 4 : n <= 20 ? 5 : 8; }
 static size_t mma_dep_smem(int n, int nx, int D) {
-  return ((size_t)2 * TR * n + (size_t)(nx + D) * MW * 32) * sizeof(double);
+  return ((size_t)2 * TR * n + (size_t)(nx + D) * DC * 2) * sizeof(double);
 }
 static size_t mma_gat_smem(int n, int nx, bool vproj = false) {
   return ((size_t)(vproj ? 4 : 2) * TR * n + (size_t)nx * (MC + 1)) * sizeof(double);
@@ -1529,7 +1554,7 @@ static int launch_dep_mma_t(const RomArgs& a, int G, cudaStream_t s) {
   auto kfn = rom_deposit_mma_kernel<D, NK>;
   static bool attr = false;
   if (!attr) { rom_allow_smem(kfn); attr = true; }
-  kfn<<<dim3(G, (a.p + MC - 1) / MC), MW * 32, mma_dep_smem(a.n, a.nx, D), s>>>(a);
+  kfn<<<dim3(G, (a.p + DC - 1) / DC), DW * 32, mma_dep_smem(a.n, a.nx, D), s>>>(a);
   return picrom_check_launch("rom_deposit_mma_kernel");
 }
 template <int D, int NK>
@@ -1556,7 +1581,8 @@ static int launch_gat_mma_t(const RomArgs& a, int G, cudaStream_t s) {
 template <int D>
 static int rom_dep_grid(const RomArgs& a) {
   if (!rom_use_mma() || mma_dep_smem(a.n, a.nx, D) > 220 * 1024) return rom_grid(a.N);
-  return rom_grid_mma(a.N, a.p, 1);
+  const int tiles = (a.p + DC - 1) / DC;
+  return (int)std::min<long long>(std::max(1, picrom_num_sms() / tiles), std::max<long long>(1, a.N / 64));
 }
 template <int D>
 static int launch_rom_deposit_any(const RomArgs& a, int G, cudaStream_t s) {
