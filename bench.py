@@ -7,7 +7,8 @@ One "step" = one fused gather-kick-drift-deposit pass over all Np x p particles
 plus the per-instance Poisson solve (picrom_pic_push + picrom_pic_solve), on
 device-resident state; the default workload is BASELINE.json configs[1] (C2:
 two-stream, p = 32 instances x 250,000 particles, Nx = 128, cubic splines).
-L2 is flushed (256 MiB write, outside the timed events) between timed steps.
+L2 is flushed between timed steps, outside the timed events: a 256 MiB write, then
+a 256 MiB read so the lines left in L2 are clean (no dirty write-back in the step).
 Multi-GPU (torchrun): every rank runs its own independent C2 batch (instance
 sharding, no collective on the data path; weak scaling); time = max over ranks.
 
@@ -195,9 +196,21 @@ def run_ours(args, w, rank, world, local_rank):
                   e.r_ee.data_ptr() if hist else None, e.r_kin.data_ptr() if hist else None,
                   e.ws.data_ptr(), e.status.data_ptr(), s)
 
+    # L2 flush between timed steps (outside the events): write a 256 MiB buffer
+    # (> 126 MB L2), then read a second one so the lines left in L2 are clean --
+    # otherwise the timed step pays the write-back of the flush buffer's dirty
+    # lines (up to 126 MB of extra HBM writes) on top of its own traffic
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    for _ in range(args.warmup):
+    flush_rd = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    flush_sink = torch.empty((), dtype=torch.float64, device="cuda")
+
+    def l2_flush():
         flush.zero_()
+        if args.flush == "writeread":
+            torch.sum(flush_rd, dim=0, out=flush_sink)
+
+    for _ in range(args.warmup):
+        l2_flush()
         step()
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
@@ -212,12 +225,12 @@ def run_ours(args, w, rank, world, local_rank):
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < 1.0:
         for _ in range(10):
-            flush.zero_()
+            l2_flush()
             step(hist=False)
         torch.cuda.synchronize()
     torch.cuda.synchronize()
     for k in range(args.steps):
-        flush.zero_()                       # L2 flush outside the timed events
+        l2_flush()                          # L2 flush outside the timed events
         evs[k][0].record()
         step()
         evs[k][1].record()
@@ -285,7 +298,8 @@ def run_ours(args, w, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded two-stream loading, SURVEY.md §8(d))",
         "config": w.describe() | {"parallelism": f"instances, {world} rank(s), no data-path collective",
-                                  "l2": "flushed between timed steps (256 MiB write outside events)",
+                                  "l2": ("flushed between timed steps outside the events: 256 MiB write"
+                                         + (" + 256 MiB read (clean lines)" if args.flush == "writeread" else "")),
                                   "state_bytes": 2 * n * p * 8},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -324,6 +338,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rom", action="store_true", help="skip the reduced-step (C3) section")
+    ap.add_argument("--flush", default="writeread", choices=["write", "writeread"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

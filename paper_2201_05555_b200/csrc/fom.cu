@@ -546,7 +546,9 @@ step_kernel(StepArgs a, SolveArgs sa) {
     const double h = ip[I_H], inv_h = ip[I_INVH];
     const int mask = fast_mask(nx, h);
 
+#ifndef PICROM_EXP_NOHIST
     for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
+#endif
     if (MODE == MODE_LEAPFROG && j != last_j) {
       const double* ph = a.phi + (size_t)j * nx;
       const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
@@ -585,6 +587,20 @@ step_kernel(StepArgs a, SolveArgs sa) {
 
     // the particle work of one SPAN block already in registers
     auto process = [&](int b0, const double* cx, const double* cv, const double* ce) {
+#ifdef PICROM_EXP_STREAM
+      // timing experiment only: the bare x, v stream (no locate/gather/deposit)
+      if constexpr (MODE == MODE_LEAPFROG) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = b0 + woff + u * 32;
+          if (i < len) {
+            __stcs(X + i, fma(a.dt, cv[u], cx[u]));
+            __stcs(V + i, cv[u] * 0.999);
+          }
+        }
+        return;
+      }
+#endif
       bool valid[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) valid[u] = b0 + woff + u * 32 < len;
@@ -723,6 +739,9 @@ step_kernel(StepArgs a, SolveArgs sa) {
 
     // fold ghost rows, reduce the H histograms in fixed order -> segment row
     // (8 independent partial sums per node, combined in a fixed tree)
+#ifdef PICROM_EXP_NOHIST
+    if (false)
+#endif
     for (int nd = tid; nd < nx; nd += NT) {
       double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       // histogram row r holds node (r + OFF) mod nx: rows r0, r0 + nx, ... < nh
@@ -761,7 +780,11 @@ step_kernel(StepArgs a, SolveArgs sa) {
           if (s_last) a.inst_done[j] = 0u;
         }
         __syncthreads();
+#ifdef PICROM_EXP_NOSOLVE
+        if (false) {     // timing experiment only
+#else
         if (s_last && a.fuse_solve == 1) {
+#endif
           __threadfence();
           // scratch = the histogram, coefficient and reduction smem (free now)
           solve_body(sa, j, hist, (unsigned int)a.p,
