@@ -737,8 +737,10 @@ step_kernel(StepArgs a, SolveArgs sa) {
     }
     __syncthreads();
 
-    // fold ghost rows, reduce the H histograms in fixed order -> segment row
-    // (8 independent partial sums per node, combined in a fixed tree)
+    // fold ghost rows, reduce the H histograms in a fixed order -> segment row.
+    // Thread per node; node nd reads the histograms rotated by nd (H is a
+    // power of two), so the 32 lanes of a load hit 32 consecutive histograms
+    // -- conflict-free (unrotated, all lanes would read one bank, rows apart).
 #ifdef PICROM_EXP_NOHIST
     if (false)
 #endif
@@ -751,7 +753,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
         for (int hh = 0; hh < H; hh += 8) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            if (hh + u < H) s8[u] += rowp[hh + u];
+            if (hh + u < H) s8[u] += rowp[(hh + u + nd) & (H - 1)];
         }
       }
       a.seg_hist[(size_t)seg * nx + nd] =

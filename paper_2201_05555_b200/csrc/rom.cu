@@ -1172,13 +1172,17 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
     }
     __syncthreads();
   }
-  // fold ghost rows and the 2 copies per column (fixed order) -> seg[b][c][nd]
+  // fold ghost rows and the 2 copies per column (fixed order) -> seg[b][c][nd];
+  // consecutive threads take consecutive columns of one node (one 16-byte
+  // load of both copies: conflict-free)
   const int P_used = min(DC, a.p - blockIdx.y * DC);
   for (int q = tid; q < P_used * nx; q += NT) {
-    const int cc = q / nx, nd = q % nx;
+    const int nd = q / P_used, cc = q % P_used;
     double s = 0.0;
-    for (int rr = (nd - Spline<D>::OFF) % nx; rr < nh; rr += nx)
-      s += hist[rr * HS + 2 * cc] + hist[rr * HS + 2 * cc + 1];
+    for (int rr = (nd - Spline<D>::OFF) % nx; rr < nh; rr += nx) {
+      const double2 v = *reinterpret_cast<const double2*>(hist + rr * HS + 2 * cc);
+      s += v.x + v.y;
+    }
     a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * DC + cc) * nx + nd] = s;
   }
 }
