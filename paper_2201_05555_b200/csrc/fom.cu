@@ -120,7 +120,9 @@ static int choose_k(int nx, int degree) {
 
 static size_t step_smem(int nx, int degree, int K, bool with_coef) {
   size_t h = (size_t)(nx + degree) * (step_nt() / K) * sizeof(double);
-  size_t c = with_coef ? (size_t)nx * degree * sizeof(double) : 0;
+  // LEAPFROG: per-cell field polynomials + the solve's khat (padded) and stencil,
+  // preloaded at CTA start so the last-CTA solve tail has no global round trip for them
+  size_t c = with_coef ? ((size_t)nx * degree + (size_t)(nx + nx / 4 + 4) + 8) * sizeof(double) : 0;
   return h + c + 64 * sizeof(double);
 }
 
@@ -300,8 +302,11 @@ __device__ __forceinline__ int kh_pad(int r) { return r + (r >> 2); }
 // One instance's assembly + solve by a whole CTA; `sm` holds `avail`
 // doubles (>= solve_scratch(nx, 1)); `ntickets` = how many instance solves
 // make up this step (the last one to finish advances the step counter).
+// kh_pre / stn_pre (nullable): khat (padded, kh_pad) and the stencil already
+// in shared memory; crow_pre >= 0: the step counter value already read.
 __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int ntickets,
-                           size_t avail) {
+                           size_t avail, const double* kh_pre = nullptr,
+                           const double* stn_pre = nullptr, long long crow_pre = -1) {
   const int nx = a.nx;
   double* rho = sm;                      // nx (phi overwrites it after the circulant)
   double* kh = rho + nx;                 // khat, padded (kh_pad)
@@ -311,10 +316,11 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   double* phi = rho;
   const int mp = solve_mp(nx, blockDim.x, avail);
   const int tid = threadIdx.x;
-  if (a.stencil && tid <= a.degree) stn[tid] = a.stencil[tid];
+  if (stn_pre) stn = const_cast<double*>(stn_pre);
+  else if (a.stencil && tid <= a.degree) stn[tid] = a.stencil[tid];
   const double* ip = a.inst + (size_t)(a.cols ? a.cols[j] : j) * PICROM_INST_STRIDE;
   const double h = ip[I_H];
-  const long long crow = a.counter ? *a.counter : 0;
+  const long long crow = crow_pre >= 0 ? crow_pre : (a.counter ? *a.counter : 0);
   const long long row = a.hist_mod > 0 ? crow % a.hist_mod : crow;
   double* rho_out = a.rho_out ? a.rho_out + row * a.hist_stride_rho : nullptr;
   double* phi_hist = a.phi_hist ? a.phi_hist + row * a.hist_stride_rho : nullptr;
@@ -350,7 +356,8 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   } else {
     for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] = a.rho_in[(size_t)j * nx + nd];
   }
-  if (a.solve)
+  if (kh_pre) kh = const_cast<double*>(kh_pre);
+  else if (a.solve)
     for (int r = tid; r < nx; r += blockDim.x) kh[kh_pad(r)] = a.khat[r];
   __syncthreads();
   if (rho_out)
@@ -363,6 +370,9 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   const double mean_rho = block_sum(part, red) / (double)nx;
   for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] -= mean_rho;
   __syncthreads();
+#ifdef PICROM_EXP_NOCIRC
+  if (false)     // timing experiment only
+#endif
   // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m.  A lane owns
   // 4 consecutive outputs and keeps khat[(n0 + i - m) mod nx], i < 4, in a
   // register window that slides by one smem load per step of m (1 load per
@@ -428,7 +438,11 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   }  // !energy_only
   if (phi_hist)
     for (int nd = tid; nd < nx; nd += blockDim.x) phi_hist[(size_t)j * nx + nd] = phi[nd];
+#ifdef PICROM_EXP_NOCIRC
+  if (false) {
+#else
   if (energy_out) {
+#endif
     // L phi with L = stencil / h (circulant, half bandwidth d)
     const double inv_h = 1.0 / h;
     part = 0.0;
@@ -499,6 +513,12 @@ step_kernel(StepArgs a, SolveArgs sa) {
   double* hist = smem;                         // [nh][H]
   double* coef = hist + nh * H;                // [D][nx] field polynomials
   double* red = coef + (MODE == MODE_LEAPFROG ? nx * D : 0);
+  double* kh_pre = red + 64;                   // LEAPFROG: khat (padded) + stencil
+  double* stn_pre = kh_pre + (nx + nx / 4 + 4);
+  if (MODE == MODE_LEAPFROG && a.fuse_solve == 1) {
+    for (int r = threadIdx.x; r < nx; r += NT) kh_pre[kh_pad(r)] = sa.khat[r];
+    if (sa.stencil && threadIdx.x <= D) stn_pre[threadIdx.x] = sa.stencil[threadIdx.x];
+  }
   const unsigned int hist_base = smem_u32(hist + myh_of<K>(threadIdx.x));
 
   const int tid = threadIdx.x;
@@ -790,7 +810,8 @@ step_kernel(StepArgs a, SolveArgs sa) {
           __threadfence();
           // scratch = the histogram, coefficient and reduction smem (free now)
           solve_body(sa, j, hist, (unsigned int)a.p,
-                     (size_t)nh * H + (MODE == MODE_LEAPFROG ? (size_t)nx * D : 0) + 64);
+                     (size_t)nh * H + (MODE == MODE_LEAPFROG ? (size_t)nx * D : 0) + 64,
+                     kh_pre, stn_pre, a.counter ? step_id - 1 : -1);
         }
       }
     }
