@@ -228,6 +228,22 @@ struct StepArgs {
   unsigned int* exit_ctr;
 };
 
+#ifdef PICROM_EXP_TIMING
+// timing experiment only: %globaltimer stamps of instance 0's tail CTA
+__device__ unsigned long long g_ts[16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TSTAMP(k, cond) do { if ((cond) && threadIdx.x == 0) g_ts[k] = gtimer(); } while (0)
+extern "C" int picrom_debug_timestamps(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_ts, sizeof(g_ts)) == cudaSuccess ? 0 : -1;
+}
+#else
+#define TSTAMP(k, cond) do { } while (0)
+#endif
+
 // ----------------------------------------------------- per-instance solve
 //
 // One CTA per instance.  rho = qw * (sum of segment rows) + bg*h   (or rho_in)
@@ -345,12 +361,40 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
     const long long T = a.n * (long long)a.p;
     const int b_lo = cta_of((long long)j * a.n, T, a.G);
     const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, a.G);
+    const int cnt = b_hi - b_lo + 1;
     const double qw = ip[I_QW], bgh = ip[I_BGH];
-    for (int nd = tid; nd < nx; nd += blockDim.x) {
-      const double s = ordered_sum(a.seg_hist + (size_t)(b_lo + j) * nx + nd, nx, b_hi - b_lo + 1);
-      rho[nd] = a.raw ? s : fma(qw, s, bgh);
+    const double* base = a.seg_hist + (size_t)(b_lo + j) * nx;
+    const int nparts = max(1, min(min((int)(blockDim.x / nx), mp), (cnt + 15) / 16));
+    if (nparts == 1) {
+      for (int nd = tid; nd < nx; nd += blockDim.x) {
+        const double s = ordered_sum(base + nd, nx, cnt);
+        rho[nd] = a.raw ? s : fma(qw, s, bgh);
+      }
+    } else {
+      // many segment rows (one instance over many CTAs, e.g. C1): nparts
+      // threads per node sum consecutive row ranges in parallel (one round of
+      // loads each), then the parts are added in order
+      double* part_s = red + 40;                 // nparts x nx (solve scratch)
+      const int per = (cnt + nparts - 1) / nparts;
+      const int nd = tid % nx, q = tid / nx;
+      if (q < nparts) {
+        const int r0 = q * per, r1 = min(cnt, r0 + per);
+        part_s[q * nx + nd] = r1 > r0 ? ordered_sum(base + (size_t)r0 * nx + nd, nx, r1 - r0) : 0.0;
+      }
+      __syncthreads();
+      for (int m = tid; m < nx; m += blockDim.x) {
+        double s = part_s[m];
+        for (int qq = 1; qq < nparts; ++qq) s += part_s[qq * nx + m];
+        rho[m] = a.raw ? s : fma(qw, s, bgh);
+      }
+      __syncthreads();
     }
-    if (kin_out && tid == 0) kin_out[j] = 0.5 * ordered_sum(a.seg_kin + b_lo + j, 1, b_hi - b_lo + 1);
+    if (kin_out && tid < 32) {                   // warp-parallel, fixed lane tree
+      double k = 0.0;
+      for (int b = tid; b < cnt; b += 32) k += a.seg_kin[b_lo + j + b];
+      k = warp_sum(k);
+      if (tid == 0) kin_out[j] = 0.5 * k;
+    }
   } else if (a.energy_only) {
     for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] = a.rho_in[(size_t)j * nx + nd];
   } else {
@@ -360,6 +404,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   else if (a.solve)
     for (int r = tid; r < nx; r += blockDim.x) kh[kh_pad(r)] = a.khat[r];
   __syncthreads();
+  TSTAMP(4, j == 0);
   if (rho_out)
     for (int nd = tid; nd < nx; nd += blockDim.x) rho_out[(size_t)j * nx + nd] = rho[nd];
   if (!a.solve && !a.energy_only) return;
@@ -368,6 +413,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   if (!a.energy_only) {
   for (int nd = tid; nd < nx; nd += blockDim.x) part += rho[nd];
   const double mean_rho = block_sum(part, red) / (double)nx;
+  TSTAMP(5, j == 0);
   for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] -= mean_rho;
   __syncthreads();
 #ifdef PICROM_EXP_NOCIRC
@@ -430,6 +476,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
     phi[nd] = h * sum;
     part += phi[nd];
   }
+  TSTAMP(6, j == 0);
   const double mean_phi = block_sum(part, red) / (double)nx;
   for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] -= mean_phi;
   __syncthreads();
@@ -455,9 +502,11 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
       }
       part = fma(phi[nd], lp * inv_h, part);
     }
+    TSTAMP(7, j == 0);
     double e = block_sum(part, red);
     if (tid == 0) energy_out[j] = ip[I_HALFINVMP] * e;
   }
+  TSTAMP(8, j == 0);
   if (a.counter) {
     // last CTA to finish advances the step counter (all CTAs read it above)
     __syncthreads();
@@ -513,6 +562,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
   double* hist = smem;                         // [nh][H]
   double* coef = hist + nh * H;                // [D][nx] field polynomials
   double* red = coef + (MODE == MODE_LEAPFROG ? nx * D : 0);
+  TSTAMP(0, MODE == MODE_LEAPFROG && blockIdx.x == 0);
   double* kh_pre = red + 64;                   // LEAPFROG: khat (padded) + stencil
   double* stn_pre = kh_pre + (nx + nx / 4 + 4);
   if (MODE == MODE_LEAPFROG && a.fuse_solve == 1) {
@@ -755,6 +805,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
       if (b0 + 2 * SPAN < len) load(b0 + 2 * SPAN, ax, av, ae);
       process(b0 + SPAN, bx, bv, be);
     }
+    TSTAMP(1, MODE == MODE_LEAPFROG && j == 0 && seg_hi == a.n);
     __syncthreads();
 
     // fold ghost rows, reduce the H histograms in a fixed order -> segment row.
@@ -779,6 +830,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
       a.seg_hist[(size_t)seg * nx + nd] =
           ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     }
+    TSTAMP(2, MODE == MODE_LEAPFROG && j == 0 && seg_hi == a.n);
     if constexpr (MODE == MODE_LEAPFROG) {
       double ks = block_sum(kin, red);
       if (tid == 0) a.seg_kin[seg] = ks;
@@ -808,6 +860,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
         if (s_last && a.fuse_solve == 1) {
 #endif
           __threadfence();
+          TSTAMP(3, j == 0);
           // scratch = the histogram, coefficient and reduction smem (free now)
           solve_body(sa, j, hist, (unsigned int)a.p,
                      (size_t)nh * H + (MODE == MODE_LEAPFROG ? (size_t)nx * D : 0) + 64,
