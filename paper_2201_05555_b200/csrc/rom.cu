@@ -782,14 +782,19 @@ __global__ void argmax_abs_kernel(const double* v, long long n, long long stride
                                   const long long* banned, int nbanned, double* pv, long long* pi) {
   __shared__ double sv[256];
   __shared__ long long si[256];
+  __shared__ long long sb[256];          // banned indices (smem broadcast reads)
+  const int nbs = min(nbanned, 256);
+  for (int k = threadIdx.x; k < nbs; k += blockDim.x) sb[k] = banned[k];
+  __syncthreads();
   double bv = -2.0;
   long long bi = 0x7fffffffffffffffLL;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double s = fabs(v[i * stride]);
-    for (int k = 0; k < nbanned; ++k)
-      if (banned[k] == i) s = -1.0;
-    better(s, i, bv, bi);
+    bool ban = false;
+    for (int k = 0; k < nbs; ++k) ban |= sb[k] == i;
+    for (int k = nbs; k < nbanned; ++k) ban |= banned[k] == i;
+    better(ban ? -1.0 : s, i, bv, bi);
   }
   sv[threadIdx.x] = bv;
   si[threadIdx.x] = bi;

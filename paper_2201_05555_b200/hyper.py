@@ -211,82 +211,72 @@ class DEIMModel:
         return self.psi.shape[1]
 
 
-class DeimWindow:
-    """Ring of the last T+1 harvested sample blocks (each N x p*, device) with
-    the window Gram maintained incrementally (one new block x window per step)."""
-
-    def __init__(self, capacity):
-        self.capacity = int(capacity)
-        self.blocks = deque()
-        self._gram = {}          # (id_a, id_b) -> block Gram (host)
-        self._next = 0
-        self.ids = deque()
-
-    def __len__(self):
-        return len(self.blocks)
-
-    def append(self, block):
-        block = block.contiguous()
-        if len(self.blocks) == self.capacity:
-            old = self.ids.popleft()
-            self.blocks.popleft()
-            self._gram = {k: v for k, v in self._gram.items() if old not in k}
-        bid = self._next
-        self._next += 1
-        self.blocks.append(block)
-        self.ids.append(bid)
-        others = list(zip(self.ids, self.blocks))
-        # new block against every block in the window, <= 7 partners per call
-        for s in range(0, len(others), 7):
-            part = others[s:s + 7]
-            g = _cross(block, [b for _, b in part])
-            off = 0
-            for oid, ob in part:
-                w = ob.shape[1]
-                self._gram[(bid, oid)] = g[:, off:off + w]
-                self._gram[(oid, bid)] = g[:, off:off + w].T
-                off += w
-
-    def gram(self):
-        ids = list(self.ids)
-        return np.block([[self._gram[(a, b)] for b in ids] for a in ids])
-
-    def columns(self):
-        return list(self.blocks)
-
-
-def _cross(a, bs):
-    """a^T [b_0 | b_1 | ...] on the device (host result)."""
-    blocks = [a] + list(bs)
-    wa = a.shape[1]
-    wb = sum(b.shape[1] for b in bs)
-    out = torch.empty((wa, wb), dtype=torch.float64, device="cuda")
-    rows = a.shape[0]
-    arr = lambda t, v: (t * len(v))(*v)  # noqa: E731
-    _lib.call("picrom_cross_gram", len(blocks), 1, arr(C.c_void_p, [b.data_ptr() for b in blocks]),
-              arr(C.c_int, [int(b.stride(0)) for b in blocks]),
-              arr(C.c_int, [int(b.shape[1]) for b in blocks]), None, rows, out.data_ptr(),
-              _tall._ws(rows, 256).data_ptr(), dev.stream_handle())
+def _tsq(a, b, chunk=8192):
+    """a^T b for tall device blocks (N x ka, N x kb): batched DGEMM over row
+    chunks (split-K; a single GEMM with K = N runs on a handful of tiles), the
+    chunk products summed in a fixed order.  Host result."""
+    n = a.shape[0]
+    nb = n // chunk
+    out = None
+    if nb > 0:
+        m = nb * chunk
+        ab = a[:m].unflatten(0, (nb, chunk))
+        bb = b[:m].unflatten(0, (nb, chunk))
+        out = torch.bmm(ab.transpose(1, 2), bb).sum(dim=0)
+    if n > nb * chunk:
+        tail = a[nb * chunk:].T @ b[nb * chunk:]
+        out = tail if out is None else out + tail
     return out.cpu().numpy()
 
 
-def _blocks_times(blocks, m):
-    """[B_0 | B_1 | ...] @ m on the device (tall x small), m host (c x k)."""
-    rows = blocks[0].shape[0]
-    k = m.shape[1]
-    out = torch.zeros((rows, k), dtype=torch.float64, device="cuda")
-    off = 0
-    terms = []
-    for b in blocks:
-        w = b.shape[1]
-        terms.append((b, m[off:off + w]))
-        off += w
-    for c0 in range(0, k, 32):
-        c1 = min(k, c0 + 32)
-        for s in range(0, len(terms), 6):
-            chunk = [(b, mm[:, c0:c1], False) for b, mm in terms[s:s + 6]]
-            _tall.combine(chunk, out=out[:, c0:c1], accumulate=(s > 0))
-    return out
+class DeimWindow:
+    """Ring of the last T+1 harvested sample blocks (each N x p*, device),
+    stored as one contiguous (N x capacity*p*) matrix in slot order, with its
+    Gram maintained incrementally on the host (one new block x window product
+    per step).  Column order does not change the left singular vectors, so the
+    windowed SVD works in slot order; gram()/columns() give the ring order."""
+
+    def __init__(self, capacity):
+        self.capacity = int(capacity)
+        self.mat = None
+        self.w = None
+        self.slots = deque()     # slot of each block, oldest first
+        self.G = None            # host Gram in slot order
+
+    def __len__(self):
+        return len(self.slots)
+
+    def append(self, block):
+        if self.mat is None:
+            n, self.w = block.shape
+            self.mat = torch.empty((n, self.capacity * self.w), dtype=torch.float64, device="cuda")
+            self.G = np.zeros((self.capacity * self.w,) * 2)
+        if block.shape[1] != self.w:
+            raise ConfigurationError("DEIM window blocks must have equal widths")
+        w = self.w
+        slot = self.slots.popleft() if len(self.slots) == self.capacity else len(self.slots)
+        self.mat[:, slot * w:(slot + 1) * w].copy_(block)
+        self.slots.append(slot)
+        filled = len(self.slots) * w if len(self.slots) < self.capacity else self.capacity * w
+        # new block against the whole window (plain DGEMM)
+        g = _tsq(self.mat[:, slot * w:(slot + 1) * w], self.mat[:, :filled])
+        self.G[slot * w:(slot + 1) * w, :filled] = g
+        self.G[:filled, slot * w:(slot + 1) * w] = g.T
+
+    def _ring_cols(self):
+        return np.concatenate([np.arange(s * self.w, (s + 1) * self.w) for s in self.slots])
+
+    def gram(self):
+        idx = self._ring_cols()
+        return self.G[np.ix_(idx, idx)]
+
+    def columns(self):
+        return [self.mat[:, s * self.w:(s + 1) * self.w] for s in self.slots]
+
+    def matrix(self):
+        """(W (N x c) device view in slot order, its Gram (host))."""
+        c = len(self.slots) * self.w
+        return self.mat[:, :c], self.G[:c, :c]
 
 
 _ARGMAX_WS = {}
@@ -336,7 +326,7 @@ def deim_greedy(psi, keep=None):
             sub = _rows(psi, rows)
             coeff = np.linalg.solve(sub[:, :k], sub[:, k])
             m = np.concatenate([-coeff, [1.0]])[:, None]
-            res = _tall.combine([(psi[:, :k + 1].contiguous(), m, False)])[:, 0]
+            res = psi[:, :k + 1] @ torch.from_numpy(m[:, 0]).to("cuda")
         pick = _argmax_abs(res, banned)
         indices[k] = pick
         banned.append(pick)
@@ -344,42 +334,41 @@ def deim_greedy(psi, keep=None):
 
 
 def _orthonormalize(y):
-    """CholeskyQR2 of a tall device block (N x k, k <= 64): Q with Q^T Q = I to O(eps)."""
+    """CholeskyQR2 of a tall device block (N x k): Q with Q^T Q = I to O(eps)."""
     for _ in range(2):
-        g = _tall.gram([(y, False)])
+        g = _tsq(y, y)
         r = np.linalg.cholesky(g).T
-        y = _blocks_times([y], np.linalg.inv(r))
+        y = y @ torch.from_numpy(np.linalg.inv(r)).to("cuda")
     return y
 
 
 def _window_svd(window, dim, oversample=8, iterations=2):
     """Leading left singular vectors of the window W (N x c) without forming
-    more than an N x (d+q) block:
+    more than an N x (d+q) block (the products are plain DGEMMs on the
+    contiguous window):
       1. W^T W (sliding Gram) -> eigenpairs -> initial basis Y = W V_{d+q};
       2. `iterations` subspace-iteration steps Y <- W (W^T Q), Q = CholQR2(Y),
          which removes the squared-condition error of step 1;
       3. Rayleigh-Ritz: SVD of the small Q^T W, Psi = Q U_B[:, :d].
     The rank test is the reference's (hyper.py:263) on the Gram singular values."""
-    blocks = window.columns()
-    c = sum(b.shape[1] for b in blocks)
-    gram = window.gram()
+    W, gram = window.matrix()
+    c = W.shape[1]
     lam, vec = np.linalg.eigh(gram)
     order = np.argsort(lam)[::-1]
     lam, vec = lam[order], vec[:, order]
     sing = np.sqrt(np.clip(lam, 0.0, None))
-    nrows = blocks[0].shape[0]
+    nrows = W.shape[0]
     rank = int((sing >= max(nrows, c) * np.finfo(float).eps * sing[0]).sum())
     d_eff = min(int(dim), rank)
     if d_eff < dim:
         warnings.warn(f"DEIM samples have numerical rank {rank} < {dim}; basis reduced to {d_eff}")
     k = min(c, rank, d_eff + oversample, 64)
-    q = _orthonormalize(_blocks_times(blocks, vec[:, :k] / sing[:k]))
+    q = _orthonormalize(W @ torch.from_numpy(vec[:, :k] / sing[:k]).to("cuda"))
     for _ in range(iterations):
-        wtq = np.concatenate([_cross(b, [q]) for b in blocks], axis=0)      # (c x k)
-        q = _orthonormalize(_blocks_times(blocks, wtq))
-    qtw = np.concatenate([_cross(q, [b]) for b in blocks], axis=1)          # (k x c)
+        q = _orthonormalize(W @ torch.from_numpy(_tsq(W, q)).to("cuda"))
+    qtw = _tsq(W, q).T
     ub, _, _ = svd(qtw, full_matrices=False)
-    psi = _blocks_times([q], ub[:, :d_eff])
+    psi = q @ torch.from_numpy(np.ascontiguousarray(ub[:, :d_eff])).to("cuda")
     return psi, d_eff
 
 
@@ -411,11 +400,7 @@ def fit_deim(samples, dim, charge, prev=None, full=True, n_update=None, printed_
     if not bool(torch.any(samples != 0)):
         raise DegenerateDataError("DEIM sample window is identically zero")
     win = DeimWindow(1)
-    # split wide sample blocks so each Gram call stays <= 256 columns
-    cols = samples.shape[1]
-    win.capacity = (cols + 63) // 64
-    for c0 in range(0, cols, 64):
-        win.append(samples[:, c0:c0 + 64].contiguous())
+    win.append(samples)
     return fit_deim_device(win, dim, charge, prev=prev, full=full, n_update=n_update,
                            printed_ranking=printed_ranking)
 
