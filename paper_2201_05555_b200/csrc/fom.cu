@@ -111,6 +111,17 @@ static int step_nt() { return 128; }
 
 static int choose_k(int nx, int degree) {
   int budget = hist_budget_bytes();
+  // opt-in (PICROM_WARP_HIST=1): one histogram per warp for large meshes,
+  // cell-mod-4 phases with match-ranked rounds (the K = 32 path).  Correct
+  // (tests/test_fullorder_gpu.py) but measured 2.3x slower at C5 than K = 8
+  // lane groups (profiles/r01b): __match_any_sync + the round loop cost more
+  // than the occupancy it buys.
+  static int warp_hist = -1;
+  if (warp_hist < 0) {
+    const char* s = getenv("PICROM_WARP_HIST");
+    warp_hist = s ? atoi(s) : 0;
+  }
+  if (warp_hist && nx >= 256 && degree <= 3) return 32;
   for (int k = 1; k <= 32; k <<= 1) {
     size_t bytes = (size_t)(nx + degree) * (step_nt() / k) * sizeof(double);
     if ((int)bytes <= budget) return k;
@@ -775,6 +786,32 @@ step_kernel(StepArgs a, SolveArgs sa) {
         }
         hrow[u] = hist_base + (unsigned int)(cl[u] * H) * 8u;
       }
+      if constexpr (K == 32) {
+        // one histogram per warp (large meshes, e.g. C5's Nx = 512): four
+        // phases by cell mod 4 -- two cells of one phase are either equal or
+        // >= 4 apart, so their D+1 <= 4 rows are disjoint -- and, inside a
+        // phase, lanes with the same cell take turns by their rank among the
+        // lanes of that cell (__match_any_sync; fixed order, deterministic)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool in = ok[u] && (cl[u] & 3) == q;
+            const unsigned int peers = __match_any_sync(0xffffffffu, in ? cl[u] : -1 - lane);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            const int rounds = __reduce_max_sync(0xffffffffu, in ? rank + 1 : 0);
+            for (int rr = 0; rr < rounds; ++rr) {
+              const bool act = in && rank == rr;
+              double cur[NW];
+#pragma unroll
+              for (int m = 0; m < NW; ++m) cur[m] = lds_f64_if(hrow[u] + m * H * 8u, act);
+#pragma unroll
+              for (int m = 0; m < NW; ++m) sts_f64_if(hrow[u] + m * H * 8u, cur[m] + w[u][m], act);
+              __syncwarp();
+            }
+          }
+        }
+      } else {
 #pragma unroll
       for (int q = 0; q < K; ++q) {
 #pragma unroll
@@ -791,6 +828,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
           for (int m = 0; m < NW; ++m) sts_f64_if(hrow[u] + m * H * 8u, cur[m] + w[u][m], act);
         }
         if constexpr (K > 1) __syncwarp();
+      }
       }
     };
 

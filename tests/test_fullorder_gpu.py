@@ -9,12 +9,15 @@
   (/root/reference/pkg/tests/test_fullorder.py:19-101).
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
-
 from conftest import GOLDEN
 from oracle import fe_bspline as fe
 from oracle import pic_loop
+
+ROOT = Path(__file__).resolve().parent.parent
 
 pytestmark = pytest.mark.gpu
 
@@ -115,6 +118,33 @@ def test_run_two_stream_cubic(mods):
     hist, rec, _, _ = _compare_run(mods, 3, 128, 20_000, 4, 300, 0.05, 10 * np.pi, two_stream, 5)
     worst = np.max(np.abs(rec.electric_history - hist.electric) / np.abs(hist.electric))
     assert worst <= 1e-9, worst
+
+
+@pytest.mark.parametrize("warp_hist", ["1", "0"])
+def test_run_bump_on_tail_large_mesh(mods, warp_hist, monkeypatch):
+    """C5-like (bump-on-tail, Nx = 512, cubic, 3 instances, 60 steps): the
+    large-mesh deposit (one histogram per warp, cell-mod-4 phases with
+    match-ranked rounds for equal cells) and the K-lane-shared fallback."""
+    import subprocess
+    import sys
+    code = f"""
+import os, sys
+os.environ["PICROM_WARP_HIST"] = "{warp_hist}"
+sys.path.insert(0, {str(ROOT)!r})
+sys.path.insert(0, {str(ROOT / "tests")!r})
+import numpy as np
+from test_fullorder_gpu import _compare_run
+from paper_2201_05555_b200 import fem, fullorder as fo
+def bot(r, s):
+    return np.where(r.uniform(size=s) < 0.9, 0.0, 4.5) + np.where(r.uniform(size=s) < 0.9, 1.0, 0.5) * r.standard_normal(s)
+hist, rec, _, _ = _compare_run((fem, fo), 3, 512, 40_000, 3, 60, 0.05, 2 * np.pi / 0.3, bot, 9)
+worst = np.max(np.abs(rec.electric_history - hist.electric) / np.abs(hist.electric))
+rho = np.linalg.norm(rec.charge_history[1] - hist.rho[1]) / np.linalg.norm(hist.rho[1])
+assert worst <= 1e-9 and rho <= 1e-12, (worst, rho)
+print("ok", worst, rho)
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 def test_teacher_forced_per_step_charge_and_potential(mods):
