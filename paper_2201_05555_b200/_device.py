@@ -75,6 +75,38 @@ def to_device(a):
     return out, meta
 
 
+_STAGE = {}
+_POOL = None
+
+
+def to_host(t):
+    """Device tensor -> fresh host numpy array: D2H into a cached pinned staging
+    buffer, then a multi-threaded copy into new pageable memory (a fresh pinned
+    buffer per call costs ~26 ms per 64 MB in cudaHostAlloc, a pageable D2H
+    ~30 ms, a single-threaded copy ~15 ms: the host page faults dominate)."""
+    global _POOL
+    t = t.contiguous()
+    nbytes = t.numel() * t.element_size()
+    if nbytes < (4 << 20):
+        return t.cpu().numpy()
+    stage = _STAGE.get(t.dtype)
+    if stage is None or stage.numel() < t.numel():
+        stage = _STAGE[t.dtype] = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+    src = stage[:t.numel()]
+    src.copy_(t.reshape(-1))
+    out = np.empty(t.numel(), dtype=src.numpy().dtype)
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=max(1, min(16, len(os.sched_getaffinity(0)))))
+    sv = src.numpy()
+    k = _POOL._max_workers
+    edges = np.linspace(0, t.numel(), k + 1).astype(np.int64)
+    list(_POOL.map(lambda i: np.copyto(out[edges[i]:edges[i + 1]], sv[edges[i]:edges[i + 1]]),
+                   range(k)))
+    return out.reshape(tuple(t.shape))
+
+
 def from_device(t_pn, meta, dtype=torch.float64):
     """(p, rows) device array -> the caller's kind/shape, reference layout."""
     p, rows = t_pn.shape
@@ -87,10 +119,8 @@ def from_device(t_pn, meta, dtype=torch.float64):
         name = "picrom_transpose_i64" if t_pn.dtype == torch.int64 else "picrom_transpose"
         _lib.call(name, t_pn.data_ptr(), p, rows, out.data_ptr(), stream_handle())
     if meta.kind == "numpy" or (meta.device is not None and not str(meta.device).startswith("cuda")):
-        # device -> pinned host staging (torch's caching host allocator reuses it)
-        host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-        host.copy_(out)
-        return host.numpy() if meta.kind == "numpy" else host
+        host = to_host(out)
+        return host if meta.kind == "numpy" else torch.from_numpy(host)
     return out
 
 

@@ -488,10 +488,10 @@ def run_full_order(system, initial: ParticleEnsemble, dt, t_final,
     total = ev0.elapsed_time(ev1) / 1e3
 
     # host-side assembly of the reference record at the requested strides
-    ee = run.ee_hist.cpu().numpy()
-    kin = run.kin_hist.cpu().numpy()
-    phi = run.phi_hist.cpu().numpy().transpose(0, 2, 1)        # (rows, Nx, p)
-    rho = run.rho_hist.cpu().numpy().transpose(0, 2, 1) if run.rho_hist is not None else None
+    ee = dev.to_host(run.ee_hist)
+    kin = dev.to_host(run.kin_hist)
+    phi = dev.to_host(run.phi_hist).transpose(0, 2, 1)         # (rows, Nx, p)
+    rho = dev.to_host(run.rho_hist).transpose(0, 2, 1) if run.rho_hist is not None else None
     taus = [t for t in range(num_steps + 1) if t % record.energy_stride == 0 or t == num_steps]
     energy_times = np.asarray([t * dt for t in taus])
     electric = ee[taus]
