@@ -1894,7 +1894,7 @@ extern "C" int picrom_argmax_abs(const double* v, long long n, long long stride,
 // sector read once), M sits in smem with a pitch = 4 mod 16 (conflict-free B
 // fragments), and a warp owns 32 rows = 4 row blocks x TBO column tiles of
 // independent accumulators.
-constexpr int WRB = 4;          // 8-row blocks per warp chunk
+constexpr int WRB = 2;          // 8-row blocks per warp chunk
 template <int TBO>
 __global__ void __launch_bounds__(256, 2) wide_combine_kernel(Terms t, const double* mats,
                                                            long long N, int cp) {
@@ -1937,18 +1937,47 @@ __global__ void __launch_bounds__(256, 2) wide_combine_kernel(Terms t, const dou
       }
       const int a = t.a[ti];
       const double* mrow = wsm + (size_t)koff[ti] * cp + g;
-#pragma unroll 4
-      for (int k0 = 0; k0 < a; k0 += 4) {
-        const int k = k0 + tq;
-        double av[WRB], bv[TBO];
+      // 16-column groups with the k order permuted inside the group: logical
+      // k = 16 grp + 4 ks + tq reads physical column 16 grp + 4 tq + ks, so a
+      // lane's 4 k-steps are one contiguous 32-byte load (2 x 16 B) and the 4
+      // lanes of a row cover a full 128-byte line; M rows use the same map.
+      // The next group's loads are in flight while this group's DMMAs run.
+      auto load_group = [&](int k0, double (*av)[4]) {
+        const int c0 = k0 + 4 * tq;
 #pragma unroll
-        for (int q = 0; q < WRB; ++q) av[q] = (rv[q] && k < a) ? sg[q] * __ldcs(base[q] + k) : 0.0;
+        for (int q = 0; q < WRB; ++q) {
+          if (rv[q] && c0 + 3 < a) {
+            const double2 lo = __ldg(reinterpret_cast<const double2*>(base[q] + c0));
+            const double2 hi = __ldg(reinterpret_cast<const double2*>(base[q] + c0 + 2));
+            av[q][0] = lo.x; av[q][1] = lo.y; av[q][2] = hi.x; av[q][3] = hi.y;
+          } else {
 #pragma unroll
-        for (int j = 0; j < TBO; ++j) bv[j] = mrow[(size_t)k * cp + 8 * j];
+            for (int e = 0; e < 4; ++e) av[q][e] = (rv[q] && c0 + e < a) ? __ldg(base[q] + c0 + e) : 0.0;
+          }
+        }
+      };
+      auto compute_group = [&](int k0, const double (*av)[4]) {
+        const int c0 = k0 + 4 * tq;
 #pragma unroll
-        for (int q = 0; q < WRB; ++q)
+        for (int ks = 0; ks < 4; ++ks) {
+          const int kp = c0 + ks;                   // physical column (M row)
+          double bv[TBO];
 #pragma unroll
-          for (int j = 0; j < TBO; ++j) dmma(acc[q][j][0], acc[q][j][1], av[q], bv[j]);
+          for (int j = 0; j < TBO; ++j) bv[j] = kp < a ? mrow[(size_t)kp * cp + 8 * j] : 0.0;
+#pragma unroll
+          for (int q = 0; q < WRB; ++q)
+#pragma unroll
+            for (int j = 0; j < TBO; ++j) dmma(acc[q][j][0], acc[q][j][1], sg[q] * av[q][ks], bv[j]);
+        }
+      };
+      double ga[WRB][4], gb[WRB][4];       // ping-pong: static indexing only
+      if (a > 0) load_group(0, ga);
+      for (int k0 = 0; k0 < a; k0 += 32) {
+        if (k0 + 16 < a) load_group(k0 + 16, gb);
+        compute_group(k0, ga);
+        if (k0 + 16 >= a) break;
+        if (k0 + 32 < a) load_group(k0 + 32, ga);
+        compute_group(k0 + 16, gb);
       }
     }
 #pragma unroll
@@ -2002,8 +2031,12 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
   const size_t sm = (size_t)mats_len * sizeof(double);
   if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
   cudaStream_t s = (cudaStream_t)stream;
-  bool wide = false;
-  for (int i = 0; i < nterms; ++i) wide |= widths[i] > 32;
+  bool wide = false, aligned = true;
+  for (int i = 0; i < nterms; ++i) {
+    wide |= widths[i] > 32;
+    aligned &= (lds[i] % 2 == 0) && ((reinterpret_cast<uintptr_t>(ins[i]) & 15) == 0);
+  }
+  wide &= aligned;        // the wide kernel reads rows in 16-byte pieces
   if (wide && getenv("PICROM_COMBINE_NO_WIDE") == nullptr && N >= 1024)
     return launch_wide_combine(t, mats, N, s);
   // DMMA path: even widths, rows 16-B aligned (ld even, 16-B aligned base)
