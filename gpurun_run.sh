@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_tall_gpu.py tests/test_rom_gpu.py -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-NCU=/usr/local/cuda/bin/ncu
-timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:wide_combine --csv --log-file gpurun_out/wide.csv python tools/prof_rom_step.py 1000000 > gpurun_out/ncu_wide.log 2>&1
-timeout 600 python tools/prof_rom_step.py > gpurun_out/prof_rom.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_full.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
 echo done
