@@ -271,7 +271,29 @@ def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_di
 
     U lives on the device for the whole run; Z and every small matrix on the
     host.  ``u0``/``z0`` may supply the initial basis (otherwise the complex
-    SVD of the snapshots, as in the reference)."""
+    SVD of the snapshots, as in the reference).  The host BLAS is capped at 4
+    threads for the run: the n x n / window-size algebra gains nothing from
+    more, and idle OpenBLAS threads spinning on 16 cores slowed every host
+    step (profiles/r01b: the 420 x 420 DEIM eigh 48 -> 8 ms, argmax round
+    trips 3x)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=4, user_api="blas"):
+        return _run_reduced(system, params, x0, v0, basis_dim=basis_dim, subsample=subsample,
+                            window=window, deim_dim=deim_dim, deim_period=deim_period,
+                            deim_update=deim_update, dt=dt, t_final=t_final,
+                            svd_tol_dmd=svd_tol_dmd, fp_tol=fp_tol, fp_max_iter=fp_max_iter,
+                            hyper_reduction=hyper_reduction,
+                            printed_subset_variant=printed_subset_variant,
+                            printed_deim_ranking=printed_deim_ranking,
+                            energy_stride=energy_stride, snapshot_stride=snapshot_stride,
+                            decomp_stride=decomp_stride, record_snapshots=record_snapshots,
+                            timers=timers, u0=u0, z0=z0)
+
+
+def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_dim, deim_period,
+                 deim_update, dt, t_final, svd_tol_dmd, fp_tol, fp_max_iter, hyper_reduction,
+                 printed_subset_variant, printed_deim_ranking, energy_stride, snapshot_stride,
+                 decomp_stride, record_snapshots, timers, u0, z0):
     from .diagnostics import PhaseTimers
     params = np.asarray(params, dtype=float)
     num_steps = int(round(t_final / dt))

@@ -55,7 +55,7 @@ def wrap(name):
     setattr(hyper, name, w)
 
 
-for nm in ("_argmax_abs", "_rows", "_orthonormalize"):
+for nm in ("_argmax_abs", "_rows", "_orthonormalize", "_tsq"):
     wrap(nm)
 _gram0 = hyper._tall.gram
 
@@ -70,6 +70,18 @@ def gram_t(blocks):
 
 
 hyper._tall.gram = gram_t
+_eigh0 = np.linalg.eigh
+
+
+def eigh_t(a):
+    t0 = time.perf_counter()
+    out = _eigh0(a)
+    TOT["np.eigh"] += time.perf_counter() - t0
+    CNT["np.eigh"] += 1
+    return out
+
+
+hyper.np.linalg.eigh = eigh_t
 _comb0 = hyper._tall.combine
 
 
