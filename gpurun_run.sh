@@ -1,5 +1,9 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_rom_gpu.py -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 1500 python tools/bench_rom.py --config C4 --steps 5 --warmup 1 > gpurun_out/rom_c4.log 2>&1; echo "rc=$?" >> gpurun_out/rom_c4.log
-timeout 900 python tools/bench_rom.py --config C3 --steps 5 --warmup 2 > gpurun_out/rom_c3.log 2>&1; echo "rc=$?" >> gpurun_out/rom_c3.log
+: > gpurun_out/variants.log
+for ms in 2048 512 1024 4096 8192; do
+  for c in C1; do
+    echo "== minseg $ms $c" >> gpurun_out/variants.log
+    PICROM_MIN_SEG=$ms timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-rom --e2e-steps 200 2>&1 | grep "^{" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value']/1e9, d['ms_per_step'], d['e2e']['value']/1e9)" >> gpurun_out/variants.log 2>&1
+  done
+done
 echo done

@@ -137,9 +137,18 @@ static size_t step_smem(int nx, int degree, int K, bool with_coef) {
   return h + c + 64 * sizeof(double);
 }
 
+static int min_seg() {
+  static int m = 0;
+  if (!m) {
+    const char* s = getenv("PICROM_MIN_SEG");
+    m = s ? std::max(256, atoi(s)) : 2048;
+  }
+  return m;
+}
+
 static int grid_for(long long total, int occ) {
   // exactly one resident wave: SMs x CTAs-per-SM (queried for the kernel)
-  long long want = (total + 2047) / 2048;     // >= 2048 particles per CTA
+  long long want = (total + min_seg() - 1) / min_seg();     // >= min_seg() particles per CTA
   long long g = std::min<long long>((long long)num_sms() * std::max(occ, 1), std::max<long long>(1, want));
   return (int)g;
 }

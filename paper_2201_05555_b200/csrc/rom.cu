@@ -2037,6 +2037,12 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
     aligned &= (lds[i] % 2 == 0) && ((reinterpret_cast<uintptr_t>(ins[i]) & 15) == 0);
   }
   wide &= aligned;        // the wide kernel reads rows in 16-byte pieces
+  static int wide_all = -1;
+  if (wide_all < 0) {
+    const char* e = getenv("PICROM_COMBINE_WIDE_ALL");
+    wide_all = e ? atoi(e) : 1;   // default: every aligned combine (measured >= the narrow kernel)
+  }
+  if (wide_all && aligned) wide = true;
   if (wide && getenv("PICROM_COMBINE_NO_WIDE") == nullptr && N >= 1024)
     return launch_wide_combine(t, mats, N, s);
   // DMMA path: even widths, rows 16-B aligned (ld even, 16-B aligned base)
