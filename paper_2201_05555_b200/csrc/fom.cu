@@ -636,24 +636,6 @@ step_kernel(StepArgs a, SolveArgs sa) {
     const double h = ip[I_H], inv_h = ip[I_INVH];
     const int mask = fast_mask(nx, h);
 
-#ifndef PICROM_EXP_NOHIST
-    for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
-#endif
-    if (MODE == MODE_LEAPFROG && j != last_j) {
-      const double* ph = a.phi + (size_t)j * nx;
-      const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
-      for (int c = tid; c < nx; c += NT) {
-        double pv[D + 1];
-#pragma unroll
-        for (int m = 0; m <= D; ++m) pv[m] = ph[wrap_node(c + Spline<D>::OFF + m, nx)];
-        double C[D];
-        deriv_coeffs<D>(pv, ecoef, g, C);
-#pragma unroll
-        for (int k = 0; k < D; ++k) coef[k * nx + c] = C[k];
-      }
-    }
-    __syncthreads();
-
     double kin = 0.0;
     double* X = a.x + (size_t)j * a.ld + seg_lo;
     double* V = a.v + (size_t)j * a.ld + seg_lo;
@@ -674,6 +656,29 @@ step_kernel(StepArgs a, SolveArgs sa) {
         if constexpr (MODE == MODE_DEPOSIT) lv[u] = (in && Y) ? __ldcs(Y + i) : 1.0;
       }
     };
+
+    // the first block's loads go out before the histogram zeroing and the
+    // field-polynomial build, so their DRAM latency overlaps that prologue
+    double ax[U], av[U], ae[U], bx[U], bv[U], be[U];
+    if (len > 0) load(0, ax, av, ae);
+
+#ifndef PICROM_EXP_NOHIST
+    for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
+#endif
+    if (MODE == MODE_LEAPFROG && j != last_j) {
+      const double* ph = a.phi + (size_t)j * nx;
+      const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
+      for (int c = tid; c < nx; c += NT) {
+        double pv[D + 1];
+#pragma unroll
+        for (int m = 0; m <= D; ++m) pv[m] = ph[wrap_node(c + Spline<D>::OFF + m, nx)];
+        double C[D];
+        deriv_coeffs<D>(pv, ecoef, g, C);
+#pragma unroll
+        for (int k = 0; k < D; ++k) coef[k * nx + c] = C[k];
+      }
+    }
+    __syncthreads();
 
     // the particle work of one SPAN block already in registers
     auto process = [&](int b0, const double* cx, const double* cv, const double* ce) {
@@ -843,8 +848,6 @@ step_kernel(StepArgs a, SolveArgs sa) {
 
     // ping-pong register buffers: the loads of one block are in flight while
     // the other block is processed; no register copies on the loop edge
-    double ax[U], av[U], ae[U], bx[U], bv[U], be[U];
-    if (len > 0) load(0, ax, av, ae);
     for (int b0 = 0; b0 < len; b0 += 2 * SPAN) {
       if (b0 + SPAN < len) load(b0 + SPAN, bx, bv, be);
       process(b0, ax, av, ae);
