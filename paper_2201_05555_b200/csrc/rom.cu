@@ -1199,10 +1199,9 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
   constexpr int NM = (4 * NK + 7) / 8;        // 8-row tiles of the projection (n <= 8 NM)
   constexpr int PS = MC + 1;                  // padded phi row (bank spread)
   const int n = a.n, nx = a.nx;
-  constexpr bool vproj = VPROJ;
   double* ut = smem;                          // [2][TR * n]
   double* phs = ut + 2 * TR * n;              // [nx][PS]
-  double* vt = phs + nx * PS;                 // [2][TR * n] U_V rows (vproj)
+  double* vt = phs + nx * PS;                 // [2][TR * n] U_V rows (VPROJ)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int cl = warp * 8 + g;
