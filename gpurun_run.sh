@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-NCU=/usr/local/cuda/bin/ncu
-timeout 900 $NCU --set full --import-source on --clock-control none -k regex:rom_deposit_mma -s 2 -c 1 -o gpurun_out/dep -f python tools/prof_rom_step.py 1000000 > gpurun_out/ncu_dep.log 2>&1
+timeout 900 python -m pytest tests/test_fullorder_gpu.py tests/test_fem_gpu.py -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --no-cpu-baseline --no-rom > gpurun_out/bench.log 2>&1
+timeout 600 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --no-rom > gpurun_out/bench_c5.log 2>&1
 echo done

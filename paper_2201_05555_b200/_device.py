@@ -9,6 +9,7 @@ transpose kernel, never by torch compute.
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 from fractions import Fraction
 from functools import lru_cache
@@ -77,18 +78,44 @@ def to_device(a):
 
 _STAGE = {}
 _POOL = None
+_PINNED = []                 # [pinned tensor, weakref of the array handed out | None]
+_PINNED_CAP = 8 << 30        # bytes of result buffers kept pinned
+
+
+def _free_pinned(numel, dtype):
+    for slot in _PINNED:
+        buf, ref = slot
+        if buf.dtype == dtype and buf.numel() >= numel and (ref is None or ref() is None):
+            return slot
+    if sum(b.numel() * b.element_size() for b, _ in _PINNED) + numel * 8 > _PINNED_CAP:
+        return None
+    slot = [torch.empty(numel, dtype=dtype, pin_memory=True), None]
+    _PINNED.append(slot)
+    return slot
 
 
 def to_host(t):
-    """Device tensor -> fresh host numpy array: D2H into a cached pinned staging
-    buffer, then a multi-threaded copy into new pageable memory (a fresh pinned
-    buffer per call costs ~26 ms per 64 MB in cudaHostAlloc, a pageable D2H
-    ~30 ms, a single-threaded copy ~15 ms: the host page faults dominate)."""
+    """Device tensor -> host numpy array.
+
+    Result buffers are pinned host memory recycled across calls: a buffer is
+    reused only once the array previously handed out from it has been dropped
+    (weak reference), so a result is never overwritten while the caller holds
+    it.  Pinning fresh memory costs ~26 ms per 64 MB and a pageable D2H ~30 ms,
+    against ~1.3 ms for the D2H into a recycled pinned buffer.  Beyond the pool
+    cap, the copy goes through one pinned staging buffer and a multi-threaded
+    copy into new pageable memory (~10 ms per 64 MB)."""
     global _POOL
     t = t.contiguous()
     nbytes = t.numel() * t.element_size()
     if nbytes < (4 << 20):
         return t.cpu().numpy()
+    slot = _free_pinned(t.numel(), t.dtype)
+    if slot is not None:
+        view = slot[0][:t.numel()]
+        view.copy_(t.reshape(-1))
+        out = view.numpy().reshape(tuple(t.shape))
+        slot[1] = weakref.ref(out)
+        return out
     stage = _STAGE.get(t.dtype)
     if stage is None or stage.numel() < t.numel():
         stage = _STAGE[t.dtype] = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
