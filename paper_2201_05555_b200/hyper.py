@@ -353,7 +353,10 @@ def _window_svd(window, dim, oversample=8, iterations=2):
     The rank test is the reference's (hyper.py:263) on the Gram singular values."""
     W, gram = window.matrix()
     c = W.shape[1]
-    lam, vec = np.linalg.eigh(gram)
+    # the c x c eigensolve on the device (cuSOLVER): ~8 ms per 420 x 420 in host
+    # LAPACK even with the BLAS threads capped
+    lam_d, vec_d = torch.linalg.eigh(torch.from_numpy(np.ascontiguousarray(gram)).to("cuda"))
+    lam, vec = lam_d.cpu().numpy(), vec_d.cpu().numpy()
     order = np.argsort(lam)[::-1]
     lam, vec = lam[order], vec[:, order]
     sing = np.sqrt(np.clip(lam, 0.0, None))
