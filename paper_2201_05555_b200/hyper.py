@@ -279,6 +279,54 @@ class DeimWindow:
         return self.mat[:, :c], self.G[:c, :c]
 
 
+def deim_greedy(psi, keep=None):
+    """Greedy interpolation indices (hyper.py:218-246) on a device basis psi (N x d):
+    residual psi_k - Psi_<k (Psi[I,<k])^-1 psi_k[I] (one tall GEMV), argmax by
+    picrom_argmax_abs with the assigned indices banned (first-max tie rule).
+    The banned list lives on the device and the chosen row of psi comes back
+    with the index: one host round trip per index."""
+    if not isinstance(psi, torch.Tensor):
+        psi = torch.from_numpy(np.ascontiguousarray(psi, dtype=np.float64)).to("cuda")
+    n, d = psi.shape
+    keep = keep or {}
+    indices = np.empty(d, dtype=np.int64)
+    rows = np.empty((d, d))                    # psi[indices[k], :] as they are chosen
+    banned = torch.empty(d, dtype=torch.int64, device="cuda")
+    nb = 0
+    if keep:
+        kept = np.array(sorted(keep.items()), dtype=np.int64)
+        banned[:len(kept)] = torch.from_numpy(kept[:, 1].copy()).to("cuda")
+        nb = len(kept)
+        kept_rows = _rows(psi, kept[:, 1])
+        for (k, idx), r in zip(kept, kept_rows):
+            indices[k] = idx
+            rows[k] = r
+    key = torch.cuda.current_device()
+    ws = _ARGMAX_WS.get(key)
+    if ws is None:
+        ws = _ARGMAX_WS[key] = torch.empty(1 << 16, dtype=torch.float64, device="cuda")
+    out_i = torch.empty(1, dtype=torch.int64, device="cuda")
+    for k in range(d):
+        if k in keep:
+            continue
+        if k == 0:
+            res = psi[:, 0]
+        else:
+            sub = rows[:k]
+            coeff = np.linalg.solve(sub[:, :k], sub[:, k])
+            m = np.concatenate([-coeff, [1.0]])
+            res = psi[:, :k + 1] @ torch.from_numpy(m).to("cuda")
+        _lib.call("picrom_argmax_abs", res.data_ptr(), n, int(res.stride(0)), banned.data_ptr(),
+                  nb, out_i.data_ptr(), None, ws.data_ptr(), dev.stream_handle())
+        banned[nb:nb + 1].copy_(out_i)
+        nb += 1
+        pick_row = torch.cat([out_i.to(torch.float64), psi.index_select(0, out_i)[0]])
+        host = pick_row.cpu().numpy()
+        indices[k] = int(host[0])
+        rows[k] = host[1:]
+    return indices
+
+
 _ARGMAX_WS = {}
 
 
@@ -303,34 +351,6 @@ def _rows(psi, idx):
     _lib.call("picrom_rows_gather", psi.data_ptr(), int(psi.stride(0)), idx_d.data_ptr(), len(idx),
               psi.shape[1], out.data_ptr(), dev.stream_handle())
     return out.cpu().numpy()
-
-
-def deim_greedy(psi, keep=None):
-    """Greedy interpolation indices (hyper.py:218-246) on a device basis psi (N x d):
-    residual psi_k - Psi_<k (Psi[I,<k])^-1 psi_k[I] by one combine, argmax by
-    picrom_argmax_abs with the assigned indices banned (first-max tie rule)."""
-    if not isinstance(psi, torch.Tensor):
-        psi = torch.from_numpy(np.ascontiguousarray(psi, dtype=np.float64)).to("cuda")
-    n, d = psi.shape
-    keep = keep or {}
-    indices = np.empty(d, dtype=np.int64)
-    banned = [int(v) for v in keep.values()]
-    for k in range(d):
-        if k in keep:
-            indices[k] = keep[k]
-            continue
-        if k == 0:
-            res = psi[:, 0]
-        else:
-            rows = indices[:k]
-            sub = _rows(psi, rows)
-            coeff = np.linalg.solve(sub[:, :k], sub[:, k])
-            m = np.concatenate([-coeff, [1.0]])[:, None]
-            res = psi[:, :k + 1] @ torch.from_numpy(m[:, 0]).to("cuda")
-        pick = _argmax_abs(res, banned)
-        indices[k] = pick
-        banned.append(pick)
-    return indices
 
 
 def _orthonormalize(y):
