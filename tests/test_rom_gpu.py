@@ -180,3 +180,57 @@ def test_reduced_run_with_hyper_reduction(m):
         np.testing.assert_array_equal(a, b)
     ee_o = np.asarray(h.electric)
     assert np.max(np.abs(rec.electric_energy - ee_o) / np.abs(ee_o)) <= 1e-9
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_gather_uv_projections_vs_dense(m, d):
+    """picrom_rom_gather_uv's two DMMA projections (U_X^T E, U_V^T E) against the
+    dense products of the E it also returns and of the oracle's gradient."""
+    import torch
+    u, z, osys, gsys, *_ = _setup(m, d, True)
+    og, _, _ = orl.exact_gradients(osys, u, z)
+    ud = torch.from_numpy(u).cuda()
+    dg, _, _ = m.driver.exact_gradients_device(gsys, ud, z, harvest=False)
+    N = u.shape[0] // 2
+    e = og[:N]                                     # oracle E = coef d/dx (phi.Lambda)(U_X z)
+    assert rel(dg.e.cpu().numpy(), e) <= 1e-12
+    assert rel(dg.ux_e, u[:N].T @ e) <= 1e-12
+    assert rel(dg.uv_e, u[N:].T @ e) <= 1e-12
+
+
+def test_gram_tasks_blocks(m):
+    """Only the requested block products of a tall Gram (the tangent transport's
+    7 of 10), with and without the DMMA fast path (equal widths / a wider block)."""
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(3)
+    rows = 2 * 30011
+    for widths in ([20, 20, 20, 20], [20, 24, 20, 20]):
+        hs = [rng.standard_normal((rows, w)) for w in widths]
+        blocks = [(torch.from_numpy(h).cuda(), False) for h in hs]
+        tasks = [(0, 0), (0, 1), (0, 2), (0, 3), (1, 3), (2, 1), (2, 3)]
+        G = _tall.gram_tasks(blocks, tasks)
+        off = np.concatenate([[0], np.cumsum(widths)])
+        for i, j in tasks:
+            ref = hs[i].T @ hs[j]
+            got = G[off[i]:off[i + 1], off[j]:off[j + 1]]
+            assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (widths, i, j)
+
+
+def test_host_results_not_recycled_while_held(m):
+    """Result arrays come from recycled pinned buffers: a held result is never
+    overwritten by a later call; a dropped one's buffer is reused."""
+    import torch
+    from paper_2201_05555_b200 import _device as dev
+    a = torch.full((1 << 20,), 1.0, dtype=torch.float64, device="cuda")
+    b = torch.full((1 << 20,), 2.0, dtype=torch.float64, device="cuda")
+    ha = dev.to_host(a)
+    hb = dev.to_host(b)
+    assert ha.ctypes.data != hb.ctypes.data
+    assert (ha == 1.0).all() and (hb == 2.0).all()
+    del ha
+    live = [dev.to_host(b * k) for k in (3, 4, 5)]     # may reuse ha's buffer, never hb's
+    assert (hb == 2.0).all()
+    for k, h in zip((3, 4, 5), live):
+        assert (h == 2.0 * k).all()
+    assert len({h.ctypes.data for h in live} | {hb.ctypes.data}) == 4
