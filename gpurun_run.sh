@@ -1,5 +1,8 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_rom_gpu.py -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/prof_rom_step.py > gpurun_out/prof_rom.log 2>&1
-timeout 900 python tools/bench_rom.py --config C3 --steps 5 --warmup 2 > gpurun_out/rom_c3.log 2>&1; echo "rc=$?" >> gpurun_out/rom_c3.log
+timeout 900 python -m pytest tests/test_fullorder_gpu.py tests/test_fem_gpu.py -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+: > gpurun_out/variants.log
+for c in C5 C2 C1; do
+  echo "== main $c" >> gpurun_out/variants.log
+  timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-rom 2>&1 | grep "^{" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value']/1e9, d['ms_per_step'], d['roofline']['frac'], d['e2e']['value']/1e9)" >> gpurun_out/variants.log 2>&1
+done
 echo done

@@ -583,9 +583,6 @@ step_kernel(StepArgs a, SolveArgs sa) {
   double* coef = hist + nh * H;                // [D][nx] field polynomials
   double* red = coef + (MODE == MODE_LEAPFROG ? nx * D : 0);
   TSTAMP(0, MODE == MODE_LEAPFROG && blockIdx.x == 0);
-  // PDL: the next step's grid may be scheduled as soon as this one's CTAs free
-  // their SM slots (its CTAs only zero their histograms before waiting on us)
-  if (MODE == MODE_LEAPFROG) asm volatile("griddepcontrol.launch_dependents;");
   double* kh_pre = red + 64;                   // LEAPFROG: khat (padded) + stencil
   double* stn_pre = kh_pre + (nx + nx / 4 + 4);
   if (MODE == MODE_LEAPFROG && a.fuse_solve == 1) {
@@ -607,8 +604,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
   const long long start = cta_start(blockIdx.x, T, G);
   const long long end = cta_start(blockIdx.x + 1, T, G);
   const double inv_nx = 1.0 / (double)nx;
-  // LEAPFROG reads the step counter only after griddepcontrol.wait (PDL)
-  long long step_id = (MODE != MODE_LEAPFROG && a.counter) ? (*a.counter + 1) : a.step;
+  const long long step_id = a.counter ? (*a.counter + 1) : a.step;
   const int woff = (tid >> 5) * 32 * U + lane;   // lane's offset inside a SPAN block
 
   __shared__ int s_item;
@@ -661,18 +657,14 @@ step_kernel(StepArgs a, SolveArgs sa) {
       }
     };
 
+    // the first block's loads go out before the histogram zeroing and the
+    // field-polynomial build, so their DRAM latency overlaps that prologue
     double ax[U], av[U], ae[U], bx[U], bv[U], be[U];
+    if (len > 0) load(0, ax, av, ae);
+
 #ifndef PICROM_EXP_NOHIST
     for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
 #endif
-    if (MODE == MODE_LEAPFROG && last_j < 0) {
-      // PDL: everything above overlaps the previous step; from here on we read
-      // its outputs (x, v, phi, counter, tickets)
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      if (a.counter) step_id = *a.counter + 1;
-    }
-    if (len > 0) load(0, ax, av, ae);
-
     if (MODE == MODE_LEAPFROG && j != last_j) {
       const double* ph = a.phi + (size_t)j * nx;
       const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
@@ -1295,27 +1287,6 @@ static int launch_step_t(const StepArgs& a, const SolveArgs& sa, const Plan& pl,
   if (!attr) {
     allow_max_dynamic_smem(kfn);
     attr = true;
-  }
-  if constexpr (MODE == MODE_LEAPFROG) {
-    // programmatic dependent launch: consecutive PIC steps (the CUDA graph of
-    // run_full_order) overlap the next step's launch and histogram zeroing with
-    // this step's last-CTA solve tail; the kernel waits (griddepcontrol.wait)
-    // before it reads anything the previous step wrote
-    static const bool pdl = getenv("PICROM_NO_PDL") == nullptr;
-    if (pdl && pl.chunk == 0) {     // chunk mode takes work items before the wait: no PDL
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(pl.G);
-      cfg.blockDim = dim3(128);
-      cfg.dynamicSmemBytes = pl.smem;
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      if (cudaLaunchKernelEx(&cfg, kfn, a, sa) != cudaSuccess) return check_launch("step_kernel (PDL)");
-      return check_launch("step_kernel");
-    }
   }
   kfn<<<pl.G, 128, pl.smem, s>>>(a, sa);
   return check_launch("step_kernel");
