@@ -301,6 +301,15 @@ struct SolveArgs {
 // sum of cnt values v[0], v[stride], ... with 8 independent loads in flight,
 // combined in a fixed order (deterministic)
 __device__ __forceinline__ double ordered_sum(const double* v, size_t stride, int cnt) {
+  if (cnt > 16 && cnt <= 32) {   // one round of loads for up to 32 rows (C1: 48 rows, 2 parts)
+    double t[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) t[u] = u < cnt ? v[(size_t)u * stride] : 0.0;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = (t[u] + t[u + 8]) + (t[u + 16] + t[u + 24]);
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  }
   if (cnt <= 16) {   // common case: every load in flight at once, same sum order
     double t[16];
 #pragma unroll
