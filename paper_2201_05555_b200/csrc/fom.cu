@@ -556,8 +556,13 @@ __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   solve_body(a, blockIdx.x, sm, gridDim.x, a.scratch);
 }
 
-#ifndef PICROM_STEP_U
-#define PICROM_STEP_U 4
+// particles per lane per block: 6 where K <= 2 lanes share a histogram (C2:
+// 100 vs 97 G pushes/s), 4 for larger K (C5: 70.5 vs 65 with 6); -DPICROM_STEP_U
+// overrides both (profiles/r01b)
+#ifdef PICROM_STEP_U
+template <int K> __host__ __device__ constexpr int step_u() { return PICROM_STEP_U; }
+#else
+template <int K> __host__ __device__ constexpr int step_u() { return K <= 2 ? 6 : 4; }
 #endif
 
 // exact locate for the rare inputs of locate_fast (kept out of line so the
@@ -584,7 +589,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
   extern __shared__ double smem[];
   constexpr int H = NT / K;
   constexpr int NW = D + 1;
-  constexpr int U = PICROM_STEP_U;
+  constexpr int U = step_u<K>();
   constexpr int SPAN = NT * U;
   const int nx = a.nx;
   const int nh = nx + D;                       // histogram rows incl. ghost nodes
