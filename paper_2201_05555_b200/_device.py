@@ -64,7 +64,10 @@ def to_device(a):
         t = t.reshape(1)
         meta = Meta(meta.kind, 1, meta.device)
     if t.dim() == 1:
-        return t.contiguous().reshape(1, -1), meta
+        t = t.contiguous()
+        if isinstance(a, torch.Tensor) and t.data_ptr() == a.data_ptr():
+            t = t.clone()           # never alias the caller's array (tables are lazy)
+        return t.reshape(1, -1), meta
     if t.dim() != 2:
         raise ConfigurationError("particle/grid arrays must be 1-D or 2-D")
     t = t.contiguous()
@@ -78,17 +81,44 @@ def to_device(a):
 
 _STAGE = {}
 _POOL = None
-_PINNED = []                 # [pinned tensor, weakref of the array handed out | None]
-_PINNED_CAP = 8 << 30        # bytes of result buffers kept pinned
+_PINNED = []                 # [pinned tensor, weakref of the owner of the array handed out | None]
+_PINNED_CAP = 6 << 30        # bytes of result buffers kept pinned (C5 state: 2 x 2.05 GB)
+
+
+class _PinnedResult:
+    """Owner of one pinned slot handed out as a numpy array.
+
+    ``np.asarray(owner)`` makes an array whose ``.base`` is this object, and every
+    numpy view derived from it (transpose, slice, reshape) collapses its base to
+    the same object -- so the slot stays reserved while ANY view is alive, not
+    just the array first handed out."""
+
+    def __init__(self, buf, shape, typestr):
+        self.buf = buf
+        self.__array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                    "data": (buf.data_ptr(), False), "version": 3}
+
+
+def _slot_free(slot):
+    return slot[1] is None or slot[1]() is None
 
 
 def _free_pinned(numel, dtype):
-    for slot in _PINNED:
-        buf, ref = slot
-        if buf.dtype == dtype and buf.numel() >= numel and (ref is None or ref() is None):
-            return slot
-    if sum(b.numel() * b.element_size() for b, _ in _PINNED) + numel * 8 > _PINNED_CAP:
-        return None
+    # best fit: the smallest idle slot that holds the result, so repeated
+    # calls with the same result sizes settle on one slot per result
+    fits = [s for s in _PINNED if s[0].dtype == dtype and s[0].numel() >= numel and _slot_free(s)]
+    if fits:
+        return min(fits, key=lambda s: s[0].numel())
+    held = sum(b.numel() * b.element_size() for b, _ in _PINNED)
+    if held + numel * 8 > _PINNED_CAP:
+        # release idle slots (largest first) before giving up on the pool
+        for slot in sorted([s for s in _PINNED if _slot_free(s)], key=lambda s: -s[0].numel()):
+            _PINNED.remove(slot)
+            held -= slot[0].numel() * slot[0].element_size()
+            if held + numel * 8 <= _PINNED_CAP:
+                break
+        if held + numel * 8 > _PINNED_CAP:
+            return None
     slot = [torch.empty(numel, dtype=dtype, pin_memory=True), None]
     _PINNED.append(slot)
     return slot
@@ -98,12 +128,14 @@ def to_host(t):
     """Device tensor -> host numpy array.
 
     Result buffers are pinned host memory recycled across calls: a buffer is
-    reused only once the array previously handed out from it has been dropped
-    (weak reference), so a result is never overwritten while the caller holds
-    it.  Pinning fresh memory costs ~26 ms per 64 MB and a pageable D2H ~30 ms,
-    against ~1.3 ms for the D2H into a recycled pinned buffer.  Beyond the pool
-    cap, the copy goes through one pinned staging buffer and a multi-threaded
-    copy into new pageable memory (~10 ms per 64 MB)."""
+    reused only once the array handed out from it AND every view of that array
+    have been dropped (weak reference to a per-result owner object, see
+    _PinnedResult), so a result is never overwritten while the caller holds any
+    part of it.  Pinning fresh memory costs ~26 ms per 64 MB and a pageable D2H
+    ~30 ms, against ~1.3 ms for the D2H into a recycled pinned buffer.  The pool
+    is capped (_PINNED_CAP; idle slots are released to make room); beyond it the
+    copy goes through one pinned staging buffer and a multi-threaded copy into
+    new pageable memory (~10 ms per 64 MB)."""
     global _POOL
     t = t.contiguous()
     nbytes = t.numel() * t.element_size()
@@ -113,8 +145,10 @@ def to_host(t):
     if slot is not None:
         view = slot[0][:t.numel()]
         view.copy_(t.reshape(-1))
-        out = view.numpy().reshape(tuple(t.shape))
-        slot[1] = weakref.ref(out)
+        owner = _PinnedResult(view, t.shape, view.numpy().dtype.str)
+        slot[1] = weakref.ref(owner)
+        out = np.asarray(owner)
+        assert out.base is owner
         return out
     stage = _STAGE.get(t.dtype)
     if stage is None or stage.numel() < t.numel():

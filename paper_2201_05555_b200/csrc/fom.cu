@@ -565,6 +565,12 @@ template <int K> __host__ __device__ constexpr int step_u() { return PICROM_STEP
 template <int K> __host__ __device__ constexpr int step_u() { return K <= 2 ? 6 : 4; }
 #endif
 
+// L2 prefetch distance of the leapfrog pass, in SPAN blocks (0 = off)
+#ifndef PICROM_STEP_PF
+#define PICROM_STEP_PF 0
+#endif
+constexpr int PF = PICROM_STEP_PF;
+
 // exact locate for the rare inputs of locate_fast (kept out of line so the
 // common path stays a straight-line instruction stream)
 struct CellFrac {
@@ -658,8 +664,27 @@ step_kernel(StepArgs a, SolveArgs sa) {
     double* XO = (MODE == MODE_DRIFT) ? a.xo + (size_t)j * a.ld + seg_lo : nullptr;
     const int len = (int)(seg_hi - seg_lo);             // < 2^31 (checked on the host)
 
+    // L2 bulk prefetch (TMA engine, no registers) of this warp's slice of the
+    // SPAN block at local offset b0: lane 0 issues one cp.async.bulk.prefetch
+    // per array; the range is trimmed to 16-byte boundaries inside the segment
+    auto prefetch = [&](int b0) {
+      if (PF > 0 && (MODE == MODE_LEAPFROG) && lane == 0 && b0 < len) {
+        const int lo = b0 + (tid >> 5) * 32 * U;
+        const int hi = min(len, lo + 32 * U);
+        if (lo < hi) {
+          const uintptr_t xa = (reinterpret_cast<uintptr_t>(X + lo)) & ~uintptr_t(15);
+          const uintptr_t xe = (reinterpret_cast<uintptr_t>(X + hi)) & ~uintptr_t(15);
+          const uintptr_t va = (reinterpret_cast<uintptr_t>(V + lo)) & ~uintptr_t(15);
+          const uintptr_t ve = (reinterpret_cast<uintptr_t>(V + hi)) & ~uintptr_t(15);
+          if (xe > xa) bulk_prefetch_l2(reinterpret_cast<const void*>(xa), (uint32_t)(xe - xa));
+          if (ve > va) bulk_prefetch_l2(reinterpret_cast<const void*>(va), (uint32_t)(ve - va));
+        }
+      }
+    };
+
     // loads of one SPAN block starting at local offset b0 into (lx, lv, le)
     auto load = [&](int b0, double* lx, double* lv, double* le) {
+      if constexpr (PF > 0) prefetch(b0 + PF * SPAN);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = b0 + woff + u * 32;
@@ -674,6 +699,10 @@ step_kernel(StepArgs a, SolveArgs sa) {
     // the first block's loads go out before the histogram zeroing and the
     // field-polynomial build, so their DRAM latency overlaps that prologue
     double ax[U], av[U], ae[U], bx[U], bv[U], be[U];
+    if constexpr (PF > 1) {
+#pragma unroll
+      for (int q = 1; q < PF; ++q) prefetch(q * SPAN);
+    }
     if (len > 0) load(0, ax, av, ae);
 
 #ifndef PICROM_EXP_NOHIST

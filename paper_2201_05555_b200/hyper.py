@@ -435,7 +435,7 @@ def make_hyper_stage_device(dmd, deim, t_stage, system, params=None):
     g(z) = (U_V^T U_V) z + m_p^-1 U_X[I]^T (dphi|_I * w), with the DMD potential
     extrapolated on the device once per stage and the DEIM-sampled gather +
     projection in picrom_deim_gather."""
-    from .driver import _inst_table, _column_charge
+    from .driver import _column_charge, _inst_table, _raise_eval
     idx = np.asarray(deim.indices, dtype=np.int64)
     qw_ref = system.charge.charge_weight
 
@@ -459,14 +459,23 @@ def make_hyper_stage_device(dmd, deim, t_stage, system, params=None):
                 cache["scale"] = (None if np.all(scale == 1.0)
                                   else torch.from_numpy(scale).to("cuda"))
             zd = torch.from_numpy(np.ascontiguousarray(z)).to("cuda")
-            out = torch.empty((n, p), dtype=torch.float64, device="cuda")
-            st = dev.new_status()
+            # result and status word in one buffer: one sync per call
+            out = torch.empty((n * p + 2,), dtype=torch.float64, device="cuda")
+            st = out[n * p:].view(torch.int64)
+            st.fill_(-1)
             inst = _inst_table(system, p)
             _lib.call("picrom_deim_gather", uxd.data_ptr(), zd.data_ptr(), p, cache["phi"].data_ptr(),
                       inst.data_ptr(), None, w.data_ptr(), dev.ptr(cache["scale"]), len(idx), n, p,
                       system.mesh.num_cells, system.mesh.degree, out.data_ptr(), p, st.data_ptr(),
                       dev.stream_handle())
-            return uvtuv @ z + out.cpu().numpy()
+            host = out.cpu()
+            stat = host[n * p:].view(torch.int64)
+            if int(stat[0]) != -1:
+                # a non-finite reconstructed DEIM position: the reference's
+                # _check_finite (fem.py:101-105) raises EvaluationError here,
+                # which run_reduced turns into DivergenceError (driver.py:210-214)
+                _raise_eval(stat, p)
+            return uvtuv @ z + host[:n * p].numpy().reshape(n, p)
 
         return g
 

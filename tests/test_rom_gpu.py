@@ -234,3 +234,33 @@ def test_host_results_not_recycled_while_held(m):
     for k, h in zip((3, 4, 5), live):
         assert (h == 2.0 * k).all()
     assert len({h.ctypes.data for h in live} | {hb.ctypes.data}) == 4
+
+
+def test_host_result_views_keep_their_buffer(m):
+    """A numpy VIEW of a recycled pinned result (transpose / slice, as
+    run_full_order's potential history) keeps the slot reserved after the
+    original array is dropped (the history views once aliased)."""
+    import torch
+    from paper_2201_05555_b200 import _device as dev
+    rows = (5 << 20) // (8 * 12)                       # >= 4 MiB: the recycled path
+    a = torch.full((rows, 3, 4), 1.0, dtype=torch.float64, device="cuda")
+    b = torch.full((rows, 3, 4), 2.0, dtype=torch.float64, device="cuda")
+    va = dev.to_host(a).transpose(0, 2, 1)             # the array itself is dropped at once
+    vs = dev.to_host(a)[::2]
+    hb = dev.to_host(b)                                # same size: must not reuse va's/vs's slot
+    assert (va == 1.0).all() and (vs == 1.0).all() and (hb == 2.0).all()
+    # end to end: potential and charge histories of a run at >= 4 MiB stay distinct
+    fem, fo = m.fem, m.fullorder
+    n, p, nx, steps = 2048, 32, 128, 160               # 161 x 32 x 128 x 8 B = 5.3 MB each
+    rng = np.random.default_rng(0)
+    L = 4 * np.pi
+    x, v = rng.uniform(0, L, (n, p)), rng.standard_normal((n, p))
+    sysm = fo.VlasovSystem(fem.build_mesh(L, nx, 1), fem.ChargeConfig(n, L))
+    rec = fo.run_full_order(sysm, fo.ParticleEnsemble(x, v), 0.05, steps * 0.05,
+                            record=fo.RecordOptions(energy_stride=1, record_snapshots=False))
+    assert rec.potential_history.nbytes >= (4 << 20)
+    assert not np.array_equal(rec.potential_history, rec.charge_history)
+    np.testing.assert_array_equal(rec.potentials, rec.potential_history)
+    # the potential solves the Poisson problem of the recorded charge
+    phi = m.fem.PoissonOperator(sysm.mesh).solve(rec.charge_history[-1])
+    assert rel(phi, rec.potential_history[-1]) <= 1e-12
