@@ -61,7 +61,7 @@ int picrom_device_info(int* num_sms, int* cc_major, int* cc_minor);
 /* ---------------------------------------------------------------- FOM --- */
 
 /* Bytes of scratch the deposit / PIC-step calls need for (n, p, nx, degree).
- * The workspace holds per-instance and work-item tickets: it must be
+ * The workspace holds per-instance tickets: it must be
  * zero-filled once before its first picrom_pic_step / picrom_pic_push (every
  * call leaves them zeroed); the one-shot entry points (deposit, rmatvec,
  * verlet_drift) clear them themselves. */

@@ -88,43 +88,29 @@ static void allow_max_dynamic_smem(F kfn) {
 // rows of the CTAs covering [j*N, (j+1)*N) in CTA order -> deterministic.
 
 struct Plan {
-  int chunk;    // > 0: dynamic instance-major work items of `chunk` particles
-  int nc;       // items per instance
-  bool tma;     // leapfrog pass uses the TMA-fed kernel
   int G;        // CTAs
   int K;        // lanes sharing one smem histogram
   int H;        // histograms per CTA
   size_t smem;  // dynamic smem bytes
 };
 
-static int hist_budget_bytes() {
-  static int b = -1;
-  if (b < 0) {
-    const char* s = getenv("PICROM_HIST_KB");
-    b = (s ? atoi(s) : 72) * 1024;
-  }
-  return b;
-}
+// shared-memory budget of the K-lane histograms (72 KB: K = 2 at C2's Nx = 128,
+// 3 CTAs per SM; profiles/r01b measured K = 4 / 8 slower there)
+constexpr int kHistBudget = 72 * 1024;
+// minimum particles per CTA segment
+constexpr int kMinSeg = 2048;
 
 // 128 threads per CTA measured best (profiles/r01; 256 was slower at every K)
 static int step_nt() { return 128; }
 
+// lanes per histogram: the fewest whose histograms fit the budget; beyond
+// K = 16 (Nx > ~1150) one histogram per warp (K = 32: cell-mod-4 phases with
+// match-ranked rounds, measured 2.3x slower than K = 8 at C5 but the only
+// option once K-lane groups no longer fit)
 static int choose_k(int nx, int degree) {
-  int budget = hist_budget_bytes();
-  // opt-in (PICROM_WARP_HIST=1): one histogram per warp for large meshes,
-  // cell-mod-4 phases with match-ranked rounds (the K = 32 path).  Correct
-  // (tests/test_fullorder_gpu.py) but measured 2.3x slower at C5 than K = 8
-  // lane groups (profiles/r01b): __match_any_sync + the round loop cost more
-  // than the occupancy it buys.
-  static int warp_hist = -1;
-  if (warp_hist < 0) {
-    const char* s = getenv("PICROM_WARP_HIST");
-    warp_hist = s ? atoi(s) : 0;
-  }
-  if (warp_hist && nx >= 256 && degree <= 3) return 32;
-  for (int k = 1; k <= 32; k <<= 1) {
+  for (int k = 1; k <= 16; k <<= 1) {
     size_t bytes = (size_t)(nx + degree) * (step_nt() / k) * sizeof(double);
-    if ((int)bytes <= budget) return k;
+    if ((int)bytes <= kHistBudget) return k;
   }
   return 32;
 }
@@ -137,29 +123,14 @@ static size_t step_smem(int nx, int degree, int K, bool with_coef) {
   return h + c + 64 * sizeof(double);
 }
 
-static int min_seg() {
-  static int m = 0;
-  if (!m) {
-    const char* s = getenv("PICROM_MIN_SEG");
-    m = s ? std::max(256, atoi(s)) : 2048;
-  }
-  return m;
-}
-
 static int grid_for(long long total, int occ) {
   // exactly one resident wave: SMs x CTAs-per-SM (queried for the kernel)
-  long long want = (total + min_seg() - 1) / min_seg();     // >= min_seg() particles per CTA
+  long long want = (total + kMinSeg - 1) / kMinSeg;     // >= kMinSeg particles per CTA
   long long g = std::min<long long>((long long)num_sms() * std::max(occ, 1), std::max<long long>(1, want));
   return (int)g;
 }
 
 static int step_occupancy(int degree, int K, size_t smem);
-
-struct TmaCfg {
-  int ncw, k, stages;
-  size_t smem;
-};
-static bool tma_config(int nx, int degree, TmaCfg* cfg);
 
 static Plan make_plan(long long n, int p, int nx, int degree, bool with_coef) {
   Plan pl;
@@ -169,35 +140,15 @@ static Plan make_plan(long long n, int p, int nx, int degree, bool with_coef) {
   // grid independent of the mode so workspace sizes agree across calls: the
   // occupancy of the leapfrog kernel (largest smem + registers) sizes it
   pl.G = grid_for((long long)n * p, step_occupancy(degree, pl.K, step_smem(nx, degree, pl.K, true)));
-  TmaCfg tc;
-  pl.tma = tma_config(nx, degree, &tc) && (long long)n * p >= 4096LL * num_sms();
-  if (pl.tma) pl.G = num_sms();     // one warp-specialised CTA per SM
-  // ~4 items per CTA, multiples of 512 particles, never across instances
-  static int chunk_env = -1;
-  if (chunk_env < 0) {
-    const char* s = getenv("PICROM_CHUNK");
-    chunk_env = s ? atoi(s) : 0;    // opt-in: measured slower than the static partition (r01)
-  }
-  pl.chunk = 0;
-  pl.nc = 0;
-  if (chunk_env && !pl.tma) {
-    long long c = ((long long)n * p + 4LL * pl.G - 1) / (4LL * pl.G);
-    c = ((c + 511) / 512) * 512;
-    c = std::max<long long>(2048, std::min<long long>(c, n));
-    pl.chunk = (int)std::min<long long>(c, 1LL << 30);
-    pl.nc = (int)((n + pl.chunk - 1) / pl.chunk);
-  }
   return pl;
 }
 
-static size_t seg_rows(const Plan& pl, int p) {
-  return std::max((size_t)pl.G + (size_t)p, (size_t)p * (size_t)pl.nc);
-}
+static size_t seg_rows(const Plan& pl, int p) { return (size_t)pl.G + (size_t)p; }
 
 extern "C" size_t picrom_fom_workspace_bytes(long long n, int p, int nx, int degree) {
   Plan pl = make_plan(n, p, nx, degree, true);
   const size_t rows = seg_rows(pl, p);
-  return rows * (size_t)(nx + 1) * sizeof(double) + (size_t)(p + 3) * sizeof(unsigned int) + 256;
+  return rows * (size_t)(nx + 1) * sizeof(double) + (size_t)(p + 1) * sizeof(unsigned int) + 256;
 }
 
 // b*T and flat*G stay far below 2^63 (T < 2^40, G < 2^16)
@@ -240,12 +191,6 @@ struct StepArgs {
   // fused solve (LEAPFROG): the last CTA finishing an instance solves it
   int fuse_solve;
   unsigned int* inst_done;   // p tickets (zeroed; left zeroed)
-  // chunk mode (chunk > 0): work items = (instance, chunk of `chunk` particles)
-  // handed out in instance-major order by an atomic counter; segment row =
-  // item id, so results do not depend on which CTA took which item
-  int chunk;
-  unsigned int* item_ctr;    // zeroed; reset by the last CTA to exit
-  unsigned int* exit_ctr;
 };
 
 #ifdef PICROM_EXP_TIMING
@@ -292,7 +237,6 @@ struct SolveArgs {
   size_t hist_stride_e;     // elements per history row (energies)
   double* phi_hist;         // optional extra copy of phi (history)
   int seg_dense;            // > 0: dense segments seg[(b*p + j)*nx + nd], b < seg_dense
-  int seg_chunks;           // > 0: chunk-mode segment rows [j*seg_chunks, (j+1)*seg_chunks)
   long long hist_mod;       // > 0: history row = counter % hist_mod (ring)
   const int* cols;          // optional instance id per column
   size_t scratch;           // solve_kernel: dynamic smem in doubles
@@ -378,14 +322,6 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
       const double s = ordered_sum(a.seg_hist + (size_t)j * nx + nd, (size_t)a.p * nx, a.seg_dense);
       rho[nd] = a.raw ? s : fma(qw, s, bgh);
     }
-  } else if (a.seg_hist && a.seg_chunks > 0) {
-    const double qw = ip[I_QW], bgh = ip[I_BGH];
-    const int nc = a.seg_chunks;
-    for (int nd = tid; nd < nx; nd += blockDim.x) {
-      const double s = ordered_sum(a.seg_hist + (size_t)j * nc * nx + nd, nx, nc);
-      rho[nd] = a.raw ? s : fma(qw, s, bgh);
-    }
-    if (kin_out && tid == 0) kin_out[j] = 0.5 * ordered_sum(a.seg_kin + (size_t)j * nc, 1, nc);
   } else if (a.seg_hist) {
     const long long T = a.n * (long long)a.p;
     const int b_lo = cta_of((long long)j * a.n, T, a.G);
@@ -627,31 +563,13 @@ step_kernel(StepArgs a, SolveArgs sa) {
   const long long step_id = a.counter ? (*a.counter + 1) : a.step;
   const int woff = (tid >> 5) * 32 * U + lane;   // lane's offset inside a SPAN block
 
-  __shared__ int s_item;
-  const int nc = a.chunk > 0 ? (int)((a.n + a.chunk - 1) / a.chunk) : 0;
-  const int total_items = a.p * nc;
   int last_j = -1;
   long long pos = start;
-  while (true) {
-    int j, seg;
-    long long seg_lo, seg_hi;
-    if (a.chunk > 0) {
-      if (tid == 0) s_item = (int)atomicAdd(a.item_ctr, 1u);
-      __syncthreads();
-      const int item = s_item;
-      __syncthreads();
-      if (item >= total_items) break;
-      j = item / nc;
-      seg_lo = (long long)(item - j * nc) * a.chunk;
-      seg_hi = min(a.n, seg_lo + (long long)a.chunk);
-      seg = item;
-    } else {
-      if (pos >= end) break;
-      j = (int)(pos / a.n);
-      seg_lo = pos - (long long)j * a.n;
-      seg_hi = min(a.n, end - (long long)j * a.n);
-      seg = blockIdx.x + j;
-    }
+  while (pos < end) {
+    const int j = (int)(pos / a.n);
+    const long long seg_lo = pos - (long long)j * a.n;
+    const long long seg_hi = min(a.n, end - (long long)j * a.n);
+    const int seg = blockIdx.x + j;
     const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
     const double h = ip[I_H], inv_h = ip[I_INVH];
     const int mask = fast_mask(nx, h);
@@ -934,14 +852,9 @@ step_kernel(StepArgs a, SolveArgs sa) {
         __syncthreads();
         if (tid == 0) {
           __threadfence();
-          unsigned int need;
-          if (a.chunk > 0) {
-            need = (unsigned int)(nc - 1);
-          } else {
-            const int b_lo = cta_of((long long)j * a.n, T, G);
-            const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, G);
-            need = (unsigned int)(b_hi - b_lo);
-          }
+          const int b_lo = cta_of((long long)j * a.n, T, G);
+          const int b_hi = cta_of((long long)(j + 1) * a.n - 1, T, G);
+          const unsigned int need = (unsigned int)(b_hi - b_lo);
           const unsigned int prev = atomicAdd(&a.inst_done[j], 1u);
           s_last = prev == need;
           if (s_last) a.inst_done[j] = 0u;
@@ -964,333 +877,6 @@ step_kernel(StepArgs a, SolveArgs sa) {
     __syncthreads();
     last_j = j;
     pos = (long long)(j + 1) * a.n;
-  }
-  if (a.chunk > 0 && tid == 0) {
-    // the last CTA to run out of items resets the item counter for the next launch
-    __threadfence();
-    if (atomicAdd(a.exit_ctr, 1u) == gridDim.x - 1) {
-      *a.item_ctr = 0u;
-      *a.exit_ctr = 0u;
-      __threadfence();
-    }
-  }
-}
-
-// ------------------------------------------- TMA-fed fused step kernel
-//
-// Warp-specialised version of MODE_LEAPFROG for sm_100a: warp NCW (one elected
-// lane) streams each chunk of x and v into a ring of S shared-memory stages
-// with cp.async.bulk (TMA bulk copies, mbarrier complete_tx), so the bytes in
-// flight per SM (S x 2 x CH x 8) no longer depend on registers or occupancy;
-// the NCW consumer warps keep private (K = 1) or K-lane-shared histograms
-// [row][H] (bank = histogram id mod 16: conflict-free) and write x', v' with
-// streaming stores.  One CTA per SM; same segment/partial layout as
-// step_kernel, so picrom_pic_solve is unchanged.
-
-__device__ __forceinline__ void consumers_sync(int nthreads) {
-  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
-constexpr int kTmaU = 4;          // particles per consumer thread per chunk
-
-struct TmaChunk {                 // one chunk of one instance segment
-  long long g0;                   // first element (global index j*ld + i)
-  int cnt;                        // particles
-  int lead;                       // 1 if the copy starts one element early (16 B alignment)
-  int ncopy;                      // elements copied by TMA (even); the rest loaded directly
-};
-
-__device__ __forceinline__ TmaChunk make_chunk(long long g0, int cnt, long long last_valid) {
-  TmaChunk c;
-  c.g0 = g0;
-  c.cnt = cnt;
-  c.lead = (int)(g0 & 1);
-  int nc = ((cnt + c.lead) + 1) & ~1;
-  // never read past the last element of the array
-  while (nc > 0 && g0 - c.lead + nc - 1 > last_valid) nc -= 2;
-  c.ncopy = nc;
-  return c;
-}
-
-template <int D, int K, int NCW>
-__global__ void __launch_bounds__(NCW * 32 + 32, 1) step_tma_kernel(StepArgs a, int S) {
-  constexpr int NC = NCW * 32;
-  constexpr int H = NC / K;
-  constexpr int CH = NC * kTmaU;
-  constexpr int SL = CH + 2;                   // stage length in doubles (lead + round up)
-  constexpr int NW = D + 1;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double* stages = reinterpret_cast<double*>(smraw);              // [S][2][SL]
-  const int nx = a.nx;
-  const int nh = nx + D;
-  double* hist = stages + (size_t)S * 2 * SL;                     // [nh + 1][H]
-  double* coef = hist + (size_t)(nh + 1) * H;                     // [D][nx]
-  double* red = coef + (size_t)D * nx;                            // [32]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 32);         // [S]
-  uint64_t* empty = full + S;                                     // [S]
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  const int G = gridDim.x;
-  const long long T = a.n * (long long)a.p;
-  const long long start = cta_start(blockIdx.x, T, G);
-  const long long end = cta_start(blockIdx.x + 1, T, G);
-  const long long last_valid = (long long)(a.p - 1) * a.ld + a.n - 1;
-
-  if (warp == NCW) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      long long pos = start;
-      while (pos < end) {
-        const int j = (int)(pos / a.n);
-        const long long lo = pos - (long long)j * a.n;
-        const long long hi = min(a.n, end - (long long)j * a.n);
-        for (long long c0 = lo; c0 < hi; c0 += CH) {
-          const TmaChunk ck = make_chunk((long long)j * a.ld + c0, (int)min((long long)CH, hi - c0),
-                                         last_valid);
-          mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t bytes = (uint32_t)ck.ncopy * 8u;
-          mbar_expect_tx(&full[stage], 2u * bytes);
-          if (bytes) {
-            double* dx = stages + (size_t)stage * 2 * SL;
-            bulk_g2s(dx, a.x + (ck.g0 - ck.lead), bytes, &full[stage]);
-            bulk_g2s(dx + SL, a.v + (ck.g0 - ck.lead), bytes, &full[stage]);
-          }
-          if (++stage == S) { stage = 0; phase ^= 1; }
-        }
-        pos = (long long)(j + 1) * a.n;
-      }
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------- consumers
-  const int myh = tid / K;
-  const int klane = lane % K;
-  const double inv_nx = 1.0 / (double)nx;
-  const long long step_id = a.counter ? (*a.counter + 1) : a.step;
-  int stage = 0;
-  uint32_t phase = 0;
-  long long pos = start;
-  while (pos < end) {
-    const int j = (int)(pos / a.n);
-    const long long lo = pos - (long long)j * a.n;
-    const long long hi = min(a.n, end - (long long)j * a.n);
-    const double* ip = a.inst + (size_t)j * PICROM_INST_STRIDE;
-    const double h = ip[I_H], inv_h = ip[I_INVH];
-    const int mask = fast_mask(nx, h);
-    for (int q = tid; q < nh * H; q += NC) hist[q] = 0.0;
-    {
-      const double* ph = a.phi + (size_t)j * nx;
-      const double ecoef = ip[I_ECOEF], g = ip[I_INVH];
-      for (int c = tid; c < nx; c += NC) {
-        double pv[D + 1];
-#pragma unroll
-        for (int m = 0; m <= D; ++m) pv[m] = ph[wrap_node(c + Spline<D>::OFF + m, nx)];
-        double C[D];
-        deriv_coeffs<D>(pv, ecoef, g, C);
-#pragma unroll
-        for (int k = 0; k < D; ++k) coef[k * nx + c] = C[k];
-      }
-    }
-    consumers_sync(NC);
-    double kin = 0.0;
-    double* X = a.x + (size_t)j * a.ld;
-    double* V = a.v + (size_t)j * a.ld;
-    for (long long c0 = lo; c0 < hi; c0 += CH) {
-      const TmaChunk ck = make_chunk((long long)j * a.ld + c0, (int)min((long long)CH, hi - c0),
-                                     last_valid);
-      mbar_wait(&full[stage], phase);
-      const double* sx = stages + (size_t)stage * 2 * SL + ck.lead;
-      const double* sv = sx + SL;
-      double xs[kTmaU], vs[kTmaU];
-#pragma unroll
-      for (int u = 0; u < kTmaU; ++u) {
-        const int k = tid + u * NC;
-        xs[u] = 0.0; vs[u] = 0.0;
-        if (k < ck.cnt) {
-          if (k + ck.lead < ck.ncopy) { xs[u] = sx[k]; vs[u] = sv[k]; }
-          else { xs[u] = X[c0 + k]; vs[u] = V[c0 + k]; }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);   // stage values are in registers
-      if (++stage == S) { stage = 0; phase ^= 1; }
-
-      // pass 0: locate x_n (branch-free; rare inputs fixed up warp-uniformly)
-      int c0v[kTmaU];
-      double f0v[kTmaU];
-      bool r0[kTmaU], any0 = false;
-#pragma unroll
-      for (int u = 0; u < kTmaU; ++u) {
-        locate_fast(xs[u], h, inv_h, nx, mask, inv_nx, c0v[u], f0v[u], r0[u]);
-        r0[u] = r0[u] && (tid + u * NC < ck.cnt);
-        any0 |= r0[u];
-      }
-      if (__any_sync(0xffffffffu, any0)) {
-#pragma unroll
-        for (int u = 0; u < kTmaU; ++u)
-          if (r0[u]) locate(xs[u], h, inv_h, nx, inv_nx, c0v[u], f0v[u]);
-      }
-      // pass 1: gather, kick, drift, store, locate x_{n+1}
-      double xn[kTmaU], fr[kTmaU];
-      int cl[kTmaU];
-      bool ok[kTmaU], rare[kTmaU], any1 = false;
-#pragma unroll
-      for (int u = 0; u < kTmaU; ++u) {
-        const int k = tid + u * NC;
-        const bool valid = k < ck.cnt;
-        double C[D];
-#pragma unroll
-        for (int kk = 0; kk < D; ++kk) C[kk] = coef[kk * nx + c0v[u]];
-        const double E = horner<D>(C, f0v[u]);
-        const double vn = vs[u] + a.kfull * E;
-        kin = valid ? fma(vn, vn, kin) : kin;
-        const double vh = __dadd_rn(vs[u], __dmul_rn(a.kick, E));
-        xn[u] = __dadd_rn(xs[u], __dmul_rn(a.dt, vh));
-        if (valid) {
-          __stcs(X + c0 + k, xn[u]);
-          __stcs(V + c0 + k, vh);
-        }
-        ok[u] = valid && isfinite(xn[u]);
-        locate_fast(xn[u], h, inv_h, nx, mask, inv_nx, cl[u], fr[u], rare[u]);
-        rare[u] = rare[u] && valid;
-        any1 |= rare[u];
-      }
-      if (__any_sync(0xffffffffu, any1)) {
-#pragma unroll
-        for (int u = 0; u < kTmaU; ++u) {
-          if (!rare[u]) continue;
-          if (ok[u]) locate(xn[u], h, inv_h, nx, inv_nx, cl[u], fr[u]);
-          else { record_bad(a.status, step_id, c0 + tid + u * NC, j, a.p); cl[u] = 0; fr[u] = 0.0; }
-        }
-      }
-      // pass 2: deposit; inactive lanes address the private dummy row nh
-#pragma unroll
-      for (int u = 0; u < kTmaU; ++u) {
-        double w[NW];
-        Spline<D>::weights(fr[u], w);
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-          const bool act = ok[u] && klane == q;
-          double* hp = hist + (size_t)(act ? cl[u] : nh) * H + myh;
-          double cur[NW];
-#pragma unroll
-          for (int m = 0; m < NW; ++m) cur[m] = hp[act ? m * H : 0];
-#pragma unroll
-          for (int m = 0; m < NW; ++m)
-            if (act) hp[m * H] = cur[m] + w[m];
-          if constexpr (K > 1) __syncwarp();
-        }
-      }
-    }
-    consumers_sync(NC);
-    const int seg = blockIdx.x + j;
-    for (int nd = tid; nd < nx; nd += NC) {
-      double s = 0.0;
-      for (int r = (nd - Spline<D>::OFF) % nx; r < nh; r += nx) {
-        const double* row = hist + (size_t)r * H;
-        for (int hh = 0; hh < H; ++hh) s += row[hh];
-      }
-      a.seg_hist[(size_t)seg * nx + nd] = s;
-    }
-    // consumer-only fixed-order reduction of the kinetic partials
-    kin = warp_sum(kin);
-    if (lane == 0) red[warp] = kin;
-    consumers_sync(NC);
-    if (tid == 0) {
-      double ks = 0.0;
-      for (int w2 = 0; w2 < NCW; ++w2) ks += red[w2];
-      a.seg_kin[seg] = ks;
-    }
-    consumers_sync(NC);
-    pos = (long long)(j + 1) * a.n;
-  }
-}
-
-static size_t tma_smem(int nx, int degree, int ncw, int k, int stages) {
-  const int nc = ncw * 32;
-  const size_t st = (size_t)stages * 2 * (nc * kTmaU + 2) * sizeof(double);
-  const size_t hist = (size_t)(nx + degree + 1) * (nc / k) * sizeof(double);
-  const size_t coef = (size_t)degree * nx * sizeof(double);
-  return st + hist + coef + 32 * sizeof(double) + 2 * stages * sizeof(uint64_t) + 128;
-}
-
-// The TMA-fed variant is opt-in (PICROM_TMA=1): measured slower than the
-// occupancy-hidden step_kernel on B200 for these shapes (profiles/r01).
-static bool tma_disabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("PICROM_TMA");
-    v = (s && atoi(s)) ? 0 : 1;
-  }
-  return v == 1;
-}
-
-// pick (consumer warps, lanes per histogram, stages): fewest sharing lanes
-// first, then more consumer warps; ~48 KB of loads in flight per SM
-static bool tma_config(int nx, int degree, TmaCfg* cfg) {
-  if (tma_disabled()) return false;
-  static const int opts[][2] = {{8, 1}, {4, 1}, {8, 2}, {4, 2}, {8, 4}, {4, 4}, {8, 8}, {4, 8}};
-  const char* force = getenv("PICROM_TMA_CFG");      // "ncw,k" (tuning)
-  int fw = 0, fk = 0;
-  if (force && sscanf(force, "%d,%d", &fw, &fk) == 2) {
-    const int stages = fw == 8 ? 3 : 6;
-    const size_t sm = tma_smem(nx, degree, fw, fk, stages);
-    if (sm <= 225 * 1024) { *cfg = TmaCfg{fw, fk, stages, sm}; return true; }
-  }
-  for (auto& o : opts) {
-    const int ncw = o[0], k = o[1];
-    const int stages = ncw == 8 ? 3 : 6;
-    const size_t sm = tma_smem(nx, degree, ncw, k, stages);
-    if (sm <= 225 * 1024) {
-      *cfg = TmaCfg{ncw, k, stages, sm};
-      return true;
-    }
-  }
-  return false;
-}
-
-template <int D, int K, int NCW>
-static int launch_tma_t(const StepArgs& a, const TmaCfg& c, int G, cudaStream_t s) {
-  auto kfn = step_tma_kernel<D, K, NCW>;
-  static bool attr = false;
-  if (!attr) {
-    allow_max_dynamic_smem(kfn);
-    attr = true;
-  }
-  kfn<<<G, NCW * 32 + 32, c.smem, s>>>(a, c.stages);
-  return check_launch("step_tma_kernel");
-}
-
-template <int D>
-static int launch_tma_d(const StepArgs& a, const TmaCfg& c, int G, cudaStream_t s) {
-  if (c.ncw == 8 && c.k == 1) return launch_tma_t<D, 1, 8>(a, c, G, s);
-  if (c.ncw == 4 && c.k == 1) return launch_tma_t<D, 1, 4>(a, c, G, s);
-  if (c.ncw == 4 && c.k == 2) return launch_tma_t<D, 2, 4>(a, c, G, s);
-  if (c.ncw == 8 && c.k == 2) return launch_tma_t<D, 2, 8>(a, c, G, s);
-  if (c.ncw == 8 && c.k == 4) return launch_tma_t<D, 4, 8>(a, c, G, s);
-  if (c.ncw == 4 && c.k == 4) return launch_tma_t<D, 4, 4>(a, c, G, s);
-  if (c.ncw == 8 && c.k == 8) return launch_tma_t<D, 8, 8>(a, c, G, s);
-  return launch_tma_t<D, 8, 4>(a, c, G, s);
-}
-
-static int launch_tma(const StepArgs& a, int degree, const TmaCfg& c, int G, cudaStream_t s) {
-  switch (degree) {
-    case 1: return launch_tma_d<1>(a, c, G, s);
-    case 2: return launch_tma_d<2>(a, c, G, s);
-    default: return launch_tma_d<3>(a, c, G, s);
   }
 }
 
@@ -1404,27 +990,22 @@ static int check_cfg(long long n, int p, int nx, int degree) {
   return PICROM_OK;
 }
 
-// workspace: seg rows x nx | seg rows (kinetic) | p instance tickets | item
-// counter | exit counter   (tickets zeroed once, left zeroed by every call)
+// workspace: seg rows x nx | seg rows (kinetic) | p instance tickets
+// (tickets zeroed once, left zeroed by every call)
 static void ws_split(void* ws, const Plan& pl, int p, int nx, double** hist, double** kin,
-                     unsigned int** tickets = nullptr, StepArgs* a = nullptr) {
+                     unsigned int** tickets = nullptr) {
   double* base = reinterpret_cast<double*>(ws);
   const size_t rows = seg_rows(pl, p);
   *hist = base;
   *kin = base + rows * nx;
   unsigned int* t = reinterpret_cast<unsigned int*>(*kin + rows);
   if (tickets) *tickets = t;
-  if (a) {
-    a->chunk = pl.chunk;
-    a->item_ctr = t + p;
-    a->exit_ctr = t + p + 1;
-  }
 }
 
 // zero the ticket words of a workspace (one-shot entry points may be handed a
 // workspace last used with another shape)
 static void zero_tickets(const StepArgs& a, int p, cudaStream_t s) {
-  if (a.inst_done) cudaMemsetAsync(a.inst_done, 0, (size_t)(p + 3) * sizeof(unsigned int), s);
+  if (a.inst_done) cudaMemsetAsync(a.inst_done, 0, (size_t)(p + 1) * sizeof(unsigned int), s);
 }
 
 // ---------------------------------------------------------------- C-ABI
@@ -1439,13 +1020,13 @@ extern "C" int picrom_deposit(const double* x, long long n, int p, long long ld,
   StepArgs a{};
   a.x = const_cast<double*>(x);
   a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx; a.status = status;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
   zero_tickets(a, p, (cudaStream_t)stream);
   rc = launch_step<MODE_DEPOSIT>(a, degree, pl, s);
   if (rc) return rc;
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.inst = inst; sa.n = n; sa.p = p; sa.nx = nx;
-  sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc; sa.rho_out = rho; sa.solve = false;
+  sa.degree = degree; sa.G = pl.G; sa.rho_out = rho; sa.solve = false;
   return launch_solve(sa, s);
 }
 
@@ -1462,13 +1043,13 @@ extern "C" int picrom_rmatvec(const double* x, const double* y, long long n, int
   a.x = const_cast<double*>(x);
   a.y = y; a.wkind = kind;
   a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx; a.status = status;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
   zero_tickets(a, p, (cudaStream_t)stream);
   rc = launch_step<MODE_DEPOSIT>(a, degree, pl, s);
   if (rc) return rc;
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.inst = inst; sa.n = n; sa.p = p; sa.nx = nx;
-  sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc; sa.rho_out = out; sa.solve = false; sa.raw = true;
+  sa.degree = degree; sa.G = pl.G; sa.rho_out = out; sa.solve = false; sa.raw = true;
   return launch_solve(sa, s);
 }
 
@@ -1507,12 +1088,7 @@ extern "C" int picrom_pic_push(double* x, double* v, long long n, int p, long lo
   a.x = x; a.v = v; a.phi = phi; a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx;
   a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
   a.counter = counter;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
-  if (pl.tma) {
-    TmaCfg tc;
-    tma_config(nx, degree, &tc);
-    return launch_tma(a, degree, tc, pl.G, (cudaStream_t)stream);
-  }
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
   return launch_step<MODE_LEAPFROG>(a, degree, pl, (cudaStream_t)stream);
 }
 
@@ -1529,7 +1105,7 @@ extern "C" int picrom_pic_solve(long long n, int p, int nx, int degree, const do
   ws_split(ws, pl, p, nx, const_cast<double**>(&sa.seg_hist), &kin_seg);
   sa.seg_kin = kin_seg;
   sa.inst = inst; sa.khat = khat;
-  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc;
+  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G;
   sa.solve = true; sa.phi_out = phi;
   const size_t gp = (size_t)p * nx;
   sa.hist_stride_rho = gp;
@@ -1558,27 +1134,16 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
   int rc = check_cfg(n, p, nx, degree);
   if (rc) return rc;
   Plan pl = make_plan(n, p, nx, degree, true);
-  if (pl.tma) {   // the TMA variant has no fused solve: push + solve
-    rc = picrom_pic_push(x, v, n, p, ld, inst, nx, degree, phi, dt, kick, kfull, step, counter,
-                         ws, status, stream);
-    if (rc) return rc;
-    return picrom_pic_solve(n, p, nx, degree, inst, khat, stencil, phi, step, counter, hist_rows,
-                            rho_hist, phi_hist, ee_hist, kin_hist, ws, stream);
-  }
   StepArgs a{};
   a.x = x; a.v = v; a.phi = phi; a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx;
   a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
   a.counter = counter;
-  // timing experiments only: PICROM_NOSOLVE=1 drops the solve, =2 keeps the
-  // tickets but not the solve, =3 solves without the circulant/energy
-  static int nosolve = -1;
-  if (nosolve < 0) { const char* s = getenv("PICROM_NOSOLVE"); nosolve = s ? atoi(s) : 0; }
-  a.fuse_solve = nosolve == 1 ? 0 : (nosolve == 2 ? 2 : 1);
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
+  a.fuse_solve = 1;
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.seg_kin = a.seg_kin; sa.inst = inst; sa.khat = khat;
-  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc;
-  sa.solve = nosolve != 3; sa.phi_out = phi;
+  sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G;
+  sa.solve = true; sa.phi_out = phi;
   const size_t gp = (size_t)p * nx;
   sa.hist_stride_rho = gp;
   sa.hist_stride_e = (size_t)p;
@@ -1610,13 +1175,13 @@ extern "C" int picrom_verlet_drift(const double* x, const double* v, const doubl
   a.x = const_cast<double*>(x); a.v = const_cast<double*>(v); a.e0 = e0; a.xo = x1;
   a.inst = inst; a.n = n; a.ld = ld; a.p = p; a.nx = nx; a.dt = dt; a.kick = 0.5 * dt;
   a.step = step; a.status = status;
-  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done, &a);
+  ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
   zero_tickets(a, p, (cudaStream_t)stream);
   rc = launch_step<MODE_DRIFT>(a, degree, pl, s);
   if (rc) return rc;
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.inst = inst; sa.khat = khat; sa.stencil = stencil; sa.n = n;
-  sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.seg_chunks = pl.nc; sa.solve = true; sa.phi_out = phi1;
+  sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G; sa.solve = true; sa.phi_out = phi1;
   sa.rho_out = rho1; sa.energy_out = energy1;
   return launch_solve(sa, s);
 }

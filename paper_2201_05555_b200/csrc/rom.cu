@@ -25,6 +25,39 @@
 
 #include "common.cuh"
 
+// Compile-time kernel-path switches (dev variants via tools/build_variant.py
+// -DPICROM_...); the shipped library reads no environment variables.
+#ifdef PICROM_ROM_NO_MMA
+constexpr bool kNoRomMma = true;
+#else
+constexpr bool kNoRomMma = false;
+#endif
+#ifdef PICROM_GRAM_NO_MMA
+constexpr bool kNoGramMma = true;
+#else
+constexpr bool kNoGramMma = false;
+#endif
+#ifdef PICROM_GRAM_NO_TMA
+constexpr bool kNoGramTma = true;
+#else
+constexpr bool kNoGramTma = false;
+#endif
+#ifdef PICROM_COMBINE_NO_WIDE
+constexpr bool kNoCombineWide = true;
+#else
+constexpr bool kNoCombineWide = false;
+#endif
+#ifdef PICROM_COMBINE_NO_MMA
+constexpr bool kNoCombineMma = true;
+#else
+constexpr bool kNoCombineMma = false;
+#endif
+#ifdef PICROM_COMBINE_NO_TMA
+constexpr bool kNoCombineTma = true;
+#else
+constexpr bool kNoCombineTma = false;
+#endif
+
 using namespace picrom;
 
 extern int picrom_set_error(int code, const char* msg);
@@ -1366,11 +1399,9 @@ int rom_grid_mma(long long N, int p, int per_sm) {
 }
 constexpr int kGatherMmaPerSm = 3;   // 79 registers x 256 threads: 3 CTAs per SM
 
-bool rom_use_mma() {
-  static int use = -1;
-  if (use < 0) use = getenv("PICROM_ROM_NO_MMA") == nullptr;
-  return use == 1;
-}
+// kernel-path switches are compile time only (tools/build_variant.py -D...),
+// never environment-dependent: the DMMA F-evaluation kernels are the default
+bool rom_use_mma() { return !kNoRomMma; }
 
 }  // namespace
 
@@ -1733,7 +1764,7 @@ static int launch_gram_mma(const Blocks& b, const GramTasks& tk, int na, long lo
 
 static int gram_mma_try(const Blocks& b, int na, long long N, void* ws, cudaStream_t s,
                         double* out, const GramTasks* tasks = nullptr) {
-  if (getenv("PICROM_GRAM_NO_MMA") || N < 1024) return -1;
+  if (kNoGramMma || N < 1024) return -1;
   const int wdt = b.w[0];
   if (wdt > 32 || wdt < 2 || (wdt & 1)) return -1;
   for (int i = 0; i < b.nb; ++i)
@@ -1788,7 +1819,7 @@ static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* 
     return picrom_set_error(PICROM_ERR_CONFIG, "Gram: total width <= 256 and wa*wb <= 16384");
   const size_t sm = (size_t)2 * GTR * W * sizeof(double) + (size_t)W * (sizeof(void*) + 2 * sizeof(int));
   // TMA staging when every block is row-contiguous (ld == width) and 16-B aligned
-  bool tma = getenv("PICROM_GRAM_NO_TMA") == nullptr;
+  bool tma = !kNoGramTma;
   for (int i = 0; i < nblocks && tma; ++i)
     tma = lds[i] == widths[i] && ((widths[i] * 8) % 16 == 0) &&
           ((reinterpret_cast<uintptr_t>(ptrs[i]) & 15) == 0);
@@ -2036,16 +2067,12 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
     aligned &= (lds[i] % 2 == 0) && ((reinterpret_cast<uintptr_t>(ins[i]) & 15) == 0);
   }
   wide &= aligned;        // the wide kernel reads rows in 16-byte pieces
-  static int wide_all = -1;
-  if (wide_all < 0) {
-    const char* e = getenv("PICROM_COMBINE_WIDE_ALL");
-    wide_all = e ? atoi(e) : 1;   // default: every aligned combine (measured >= the narrow kernel)
-  }
-  if (wide_all && aligned) wide = true;
-  if (wide && getenv("PICROM_COMBINE_NO_WIDE") == nullptr && N >= 1024)
+  // every aligned combine takes the wide kernel (measured >= the narrow one)
+  if (aligned) wide = true;
+  if (wide && !kNoCombineWide && N >= 1024)
     return launch_wide_combine(t, mats, N, s);
   // DMMA path: even widths, rows 16-B aligned (ld even, 16-B aligned base)
-  bool mma = getenv("PICROM_COMBINE_NO_MMA") == nullptr && N >= 1024;
+  bool mma = !kNoCombineMma && N >= 1024;
   MmaTerms mt{};
   for (int i = 0; i < nterms && mma; ++i)
     mma = (widths[i] % 2 == 0) && (lds[i] % 2 == 0) && ((reinterpret_cast<uintptr_t>(ins[i]) & 15) == 0);
@@ -2076,7 +2103,7 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
     }
   }
   // TMA path: row-contiguous, 16-B aligned inputs
-  bool tma = getenv("PICROM_COMBINE_NO_TMA") == nullptr;
+  bool tma = !kNoCombineTma;
   int wsum = 0;
   for (int i = 0; i < nterms && tma; ++i) {
     tma = lds[i] == widths[i] && ((widths[i] * 8) % 16 == 0) &&

@@ -190,3 +190,110 @@ def test_c5_reduced_n_free_run(mods):
     assert ee <= 1e-9 and kin <= 1e-9, (ee, kin)
     assert rel(rec.charge_history[1], hist.rho[1]) <= 1e-12
     assert rel(rec.potential_history[1], hist.phi[1]) <= 1e-12
+
+
+# ------------------------------------------------------------------ C3 / C4
+
+@pytest.fixture(scope="module")
+def rom(lib_built):
+    from paper_2201_05555_b200 import driver, hyper, reduction
+    from paper_2201_05555_b200 import workloads as wl
+    return driver, reduction, hyper, wl
+
+
+def _rom_inputs(wl, name, n=None):
+    w = wl.config(name)
+    x0, v0 = wl.generate(w, num_particles=n)
+    params = np.stack([w.wavenumbers, w.alphas], axis=1)
+    return w, x0, v0, params
+
+
+def test_c3_full_scale_teacher_forced(rom):
+    """C3 at its size (N = 1e6, p = 128, n = 20, quadratic, per-instance k):
+    F(U Z) (charge -> potential -> gradient, the DEIM harvest Lambda phi), the
+    warm-up stage U^T F(U z) and the manifold maps (basis velocity, both
+    retractions, tangent transport) on the SAME (U, Z) for GPU and oracle, at
+    the initial basis and after two GPU steps; <= 1e-12 normwise."""
+    import torch
+    from oracle import manifold as omf
+    from oracle import rom_loop as orl
+    driver, red, _, wl = rom
+    w, x0, v0, params = _rom_inputs(wl, "C3")
+    N, nb = w.num_particles, w.extra["basis_dim"]
+    u0, z0 = red.complex_svd_basis(x0, v0, nb)
+    osys = orl.ParamSystem(w.lengths, w.num_cells, w.degree, N)
+    gsys = driver.ParametricVlasovSystem(w.lengths, w.num_cells, w.degree, N)
+    rec = driver.run_reduced(gsys, params, x0, v0, basis_dim=nb, subsample=w.p, window=3,
+                             deim_dim=8, deim_period=3, deim_update=2, dt=w.dt, t_final=2 * w.dt,
+                             hyper_reduction=False, energy_stride=10**9, snapshot_stride=2,
+                             decomp_stride=10**9, u0=u0, z0=z0)
+    del x0, v0
+    u2, z2 = rec.bases[-1]
+    dt = w.dt
+    for tag, u, z in (("step0", u0, z0), ("step2", u2.cpu().numpy(), z2)):
+        ud = torch.from_numpy(u).cuda()
+        og, ophi, olam = orl.exact_gradients(osys, u, z)
+        gg, gphi, glam = driver.exact_gradients(gsys, ud, z)
+        assert rel(gphi.cpu().numpy(), ophi) <= 1e-12, tag
+        assert rel(gg.cpu().numpy(), og) <= 1e-12, tag
+        assert rel(glam.cpu().numpy(), olam) <= 1e-12, tag
+        del gg, glam, olam
+        stage = driver.make_full_stage(gsys)(ud)(z)
+        assert rel(stage, u.T @ og) <= 1e-12, tag
+        # manifold maps: GPU basis velocity from its own implicit device gradient
+        dg, _, _ = driver.exact_gradients_device(gsys, ud, z, harvest=False)
+        xi_o = omf.velocity_of_basis(u, z, og)
+        xi_g = red.basis_velocity(ud, z, dg)
+        assert rel(xi_g.cpu().numpy(), xi_o) <= 1e-12, tag
+        del og, dg, xi_g
+        r_o = omf.cayley_retract(u, 0.5 * dt * xi_o)
+        r_g = red.retraction(ud, red.scaled(torch.from_numpy(xi_o).cuda(), 0.5 * dt))
+        assert rel(r_g.cpu().numpy(), r_o) <= 1e-12, tag
+        x_eval = xi_o[::-1].copy()                     # any tangent-sized operand
+        t_o = omf.transport_back(u, 0.5 * dt * xi_o, r_o, x_eval)
+        t_g = red.tangent_velocity(ud, red.scaled(torch.from_numpy(xi_o).cuda(), 0.5 * dt),
+                                   torch.from_numpy(r_o).cuda(), torch.from_numpy(x_eval).cuda())
+        assert rel(t_g.cpu().numpy(), t_o) <= 1e-12, tag
+        o_o, s_o = omf.structure_defects(r_o)
+        o_g, s_g = red.orthosymplectic_residuals(r_g)
+        assert abs(o_g - o_o) <= 1e-13 and abs(s_g - s_o) <= 1e-13, tag
+
+
+def _rom_free_run(rom, name):
+    from oracle import manifold as omf
+    driver, red, _, wl = rom
+    f = np.load(GOLDEN / f"config_{name}.npz")
+    n = int(f["num_particles"])
+    w, x0, v0, params = _rom_inputs(wl, name[:2], n)
+    ex = w.extra
+    nb = ex["basis_dim"]
+    u0, z0 = red.complex_svd_basis(x0, v0, nb)
+    # the box's LAPACK reproduces the fixture's initial basis (same seeded data)
+    assert rel(z0, f["z0"]) <= 1e-12
+    assert rel(u0[f["rows"]], f["u0_rows"]) <= 1e-12
+    gsys = driver.ParametricVlasovSystem(w.lengths, w.num_cells, w.degree, n)
+    steps, es = int(f["steps"]), int(f["energy_stride"])
+    rec = driver.run_reduced(
+        gsys, params, x0, v0, basis_dim=nb, subsample=ex.get("subsample", w.p),
+        window=ex.get("window", 3), deim_dim=ex.get("deim_dim", 8),
+        deim_period=ex.get("deim_period", 3), deim_update=ex.get("deim_update", 2), dt=w.dt,
+        t_final=steps * w.dt, hyper_reduction=name.startswith("C4"), energy_stride=es,
+        snapshot_stride=steps, decomp_stride=10**9, u0=u0, z0=z0)
+    np.testing.assert_array_equal(np.sort(omf.farthest_point_subset(z0, ex.get("subsample", w.p))),
+                                  f["sub"])
+    np.testing.assert_array_equal(rec.fp_iterations, f["fp_iterations"])
+    ee = np.max(np.abs(rec.electric_energy - f["electric"]) / np.abs(f["electric"]))
+    ham_o = f["kinetic"] + f["electric"]
+    ham = np.max(np.abs(rec.hamiltonian - ham_o) / np.abs(ham_o))
+    assert ee <= 1e-9 and ham <= 1e-9, (ee, ham)
+    u, z = rec.bases[-1]
+    assert rel(z, f["z_final"]) <= 1e-9
+    assert rel(u.cpu().numpy()[f["rows"]], f["u_final_rows"]) <= 1e-9
+    np.testing.assert_allclose(rec.ortho_residuals, f["ortho"], atol=1e-13)
+    return rec, f
+
+
+def test_c3_reduced_n_free_run(rom):
+    """C3's p = 128, n = 20, quadratic, per-instance k, 200 steps at N = 5e4:
+    fixed-point counts equal, energies <= 1e-9 vs the oracle's run (fixture)."""
+    _rom_free_run(rom, "C3r")

@@ -120,31 +120,62 @@ def test_run_two_stream_cubic(mods):
     assert worst <= 1e-9, worst
 
 
-@pytest.mark.parametrize("warp_hist", ["1", "0"])
-def test_run_bump_on_tail_large_mesh(mods, warp_hist, monkeypatch):
-    """C5-like (bump-on-tail, Nx = 512, cubic, 3 instances, 60 steps): the
-    large-mesh deposit (one histogram per warp, cell-mod-4 phases with
-    match-ranked rounds for equal cells) and the K-lane-shared fallback."""
-    import subprocess
-    import sys
-    code = f"""
-import os, sys
-os.environ["PICROM_WARP_HIST"] = "{warp_hist}"
-sys.path.insert(0, {str(ROOT)!r})
-sys.path.insert(0, {str(ROOT / "tests")!r})
-import numpy as np
-from test_fullorder_gpu import _compare_run
-from paper_2201_05555_b200 import fem, fullorder as fo
-def bot(r, s):
-    return np.where(r.uniform(size=s) < 0.9, 0.0, 4.5) + np.where(r.uniform(size=s) < 0.9, 1.0, 0.5) * r.standard_normal(s)
-hist, rec, _, _ = _compare_run((fem, fo), 3, 512, 40_000, 3, 60, 0.05, 2 * np.pi / 0.3, bot, 9)
-worst = np.max(np.abs(rec.electric_history - hist.electric) / np.abs(hist.electric))
-rho = np.linalg.norm(rec.charge_history[1] - hist.rho[1]) / np.linalg.norm(hist.rho[1])
-assert worst <= 1e-9 and rho <= 1e-12, (worst, rho)
-print("ok", worst, rho)
-"""
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout + r.stderr
+@pytest.mark.parametrize("nx", [512, 2048])
+def test_run_bump_on_tail_large_mesh(mods, nx):
+    """C5-like (bump-on-tail, cubic, 3 instances, 60 steps) on large meshes:
+    Nx = 512 takes the K = 8 lane-shared histograms (C5's path), Nx = 2048 the
+    one-histogram-per-warp path (cell-mod-4 phases with match-ranked rounds)
+    that the plan picks once K-lane histograms no longer fit shared memory."""
+    def bot(r, s):
+        return (np.where(r.uniform(size=s) < 0.9, 0.0, 4.5)
+                + np.where(r.uniform(size=s) < 0.9, 1.0, 0.5) * r.standard_normal(s))
+    hist, rec, _, _ = _compare_run(mods, 3, nx, 40_000, 3, 60, 0.05, 2 * np.pi / 0.3, bot, 9)
+    worst = np.max(np.abs(rec.electric_history - hist.electric) / np.abs(hist.electric))
+    rho = rel(rec.charge_history[1], hist.rho[1])
+    assert worst <= 1e-9 and rho <= 1e-12, (worst, rho)
+
+
+def test_push_plus_solve_equals_fused_step(mods):
+    """picrom_pic_push + picrom_pic_solve (the split C-ABI halves) reproduce
+    picrom_pic_step bit for bit (same segments, same fixed-order sums)."""
+    import torch
+    from paper_2201_05555_b200 import _device as dev
+    from paper_2201_05555_b200 import _lib
+    fem, fo = mods
+    rng = np.random.default_rng(6)
+    L, nx, d, n, p = 10 * np.pi, 128, 3, 60_000, 4
+    sysm = fo.VlasovSystem(fem.build_mesh(L, nx, d), fem.ChargeConfig(n, L))
+    x0 = torch.from_numpy(rng.uniform(0, L, (p, n))).cuda()
+    v0 = torch.from_numpy(rng.standard_normal((p, n))).cuda()
+    outs = []
+    for split in (False, True):
+        run = fo.PicRun(sysm, x0, v0, 0.05, 3, keep_rho=True)
+        run.init_field()
+        e = run.e
+        s = dev.stream_handle()
+        rho = torch.zeros((4, p, nx), dtype=torch.float64, device="cuda")
+        phi = torch.zeros_like(rho)
+        ee = torch.zeros((4, p), dtype=torch.float64, device="cuda")
+        kin = torch.zeros_like(ee)
+        for k in range(3):
+            kick, kfull = (0.025, 0.0) if k == 0 else (0.05, 0.025)
+            if split:
+                _lib.call("picrom_pic_push", e.x.data_ptr(), e.v.data_ptr(), n, p, n,
+                          e.inst.data_ptr(), nx, d, e.phi.data_ptr(), 0.05, kick, kfull, k,
+                          None, e.ws.data_ptr(), e.status.data_ptr(), s)
+                _lib.call("picrom_pic_solve", n, p, nx, d, e.inst.data_ptr(),
+                          e.c.khat.data_ptr(), e.c.stencil.data_ptr(), e.phi.data_ptr(), k,
+                          None, 0, rho.data_ptr(), phi.data_ptr(), ee.data_ptr(), kin.data_ptr(),
+                          e.ws.data_ptr(), s)
+            else:
+                _lib.call("picrom_pic_step", e.x.data_ptr(), e.v.data_ptr(), n, p, n,
+                          e.inst.data_ptr(), nx, d, e.c.khat.data_ptr(), e.c.stencil.data_ptr(),
+                          e.phi.data_ptr(), 0.05, kick, kfull, k, None, 0, rho.data_ptr(),
+                          phi.data_ptr(), ee.data_ptr(), kin.data_ptr(), e.ws.data_ptr(),
+                          e.status.data_ptr(), s)
+        outs.append([t.cpu().numpy() for t in (e.x, e.v, rho, phi, ee, kin)])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
 
 
 def test_teacher_forced_per_step_charge_and_potential(mods):
