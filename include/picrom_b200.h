@@ -126,18 +126,21 @@ int picrom_gather(const double* x, long long n, int p, long long ld,
  * per step).
  * First step: v holds v_0, kick = 0.5*dt, kfull = 0; later steps: v holds
  * v_{n-1/2}, kick = dt, kfull = 0.5*dt.  History pointers may be NULL:
- * rho_hist/phi_hist (rows of p*nx) get rho/phi at step+1, ee_hist (rows of p)
- * the electric energy at step+1, kin_hist (rows of p) the kinetic energy
+ * rho_hist/phi_hist (rows of hist_p*nx) get rho/phi at step+1, ee_hist (rows
+ * of hist_p) the electric energy at step+1, kin_hist (rows of hist_p) the kinetic energy
  * 0.5*sum v_n^2 at `step`.  Row index = `step`, or, when `counter` is non-NULL
  * (a device {long long step; unsigned done;} pair, 16 bytes), the device
  * value *counter (modulo hist_rows when hist_rows > 0: a ring), which the
  * call advances by one -- so a CUDA graph of k steps can be replayed with
- * unchanged parameters. */
+ * unchanged parameters.  hist_p (>= p; 0 means p) is the number of instances
+ * per history row: an instance group [g0, g0+p) of a larger batch writes its
+ * slice of a shared history when the caller offsets the pointers by g0*nx
+ * (rho/phi) and g0 (energies). */
 int picrom_pic_step(double* x, double* v, long long n, int p, long long ld,
                     const double* inst, int nx, int degree,
                     const double* khat, const double* stencil, double* phi,
                     double dt, double kick, double kfull, long long step,
-                    long long* counter, long long hist_rows,
+                    long long* counter, long long hist_rows, int hist_p,
                     double* rho_hist, double* phi_hist, double* ee_hist, double* kin_hist,
                     void* workspace, unsigned long long* status, void* stream);
 

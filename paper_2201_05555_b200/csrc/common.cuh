@@ -247,6 +247,13 @@ __device__ __forceinline__ void sts_f64_if(uint32_t addr, double v, bool p) {
       ::"r"(addr), "d"(v), "r"((uint32_t)p) : "memory");
 }
 
+// predicated shared-memory 32-bit integer reduction (native RED, no return)
+__device__ __forceinline__ void red_shared_u32_if(uint32_t addr, uint32_t v, bool p) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.add.u32 [%0], %1;\n}\n"
+      ::"r"(addr), "r"(v), "r"((uint32_t)p) : "memory");
+}
+
 // histogram id of thread tid when K lanes share one histogram (step kernels)
 template <int K>
 __device__ __forceinline__ int myh_of(int tid) {

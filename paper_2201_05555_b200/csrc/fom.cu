@@ -89,9 +89,10 @@ static void allow_max_dynamic_smem(F kfn) {
 
 struct Plan {
   int G;        // CTAs
-  int K;        // lanes sharing one smem histogram
-  int H;        // histograms per CTA
-  size_t smem;  // dynamic smem bytes
+  int K;        // lanes sharing one smem histogram (phase path)
+  int H;        // histograms per CTA (phase path)
+  size_t smem;  // dynamic smem bytes (phase path)
+  size_t fsmem; // dynamic smem bytes (fixed-point path)
 };
 
 // shared-memory budget of the K-lane histograms (72 KB: K = 2 at C2's Nx = 128,
@@ -123,13 +124,33 @@ static size_t step_smem(int nx, int degree, int K, bool with_coef) {
   return h + c + 64 * sizeof(double);
 }
 
-static int grid_for(long long total, int occ) {
+static int grid_for(long long n, int p, int occ) {
   // exactly one resident wave: SMs x CTAs-per-SM (queried for the kernel)
+  const long long total = n * p;
+  const long long slots = (long long)num_sms() * std::max(occ, 1);
   long long want = (total + kMinSeg - 1) / kMinSeg;     // >= kMinSeg particles per CTA
-  long long g = std::min<long long>((long long)num_sms() * std::max(occ, 1), std::max<long long>(1, want));
+  long long g = std::min<long long>(slots, std::max<long long>(1, want));
+  // instance-aligned grid (G = m p): no CTA range straddles two instances, so
+  // no CTA pays a second prologue/fold/ticket (those were the step's
+  // stragglers, ~7 us at C2, profiles/r02 timeline) -- when it idles <= 1/16
+  // of the slots
+  if (p <= g) {
+    const long long m = g / p;
+    if ((g - m * p) * 16 <= g) g = m * p;
+  }
   return (int)g;
 }
 
+// fixed-point path: [3][nx+D] u32 limbs | [nx] fp64 | [D][nx] field polynomials
+// | 64 | khat (padded) + stencil; at least the solve tail's scratch
+static size_t fix_smem(int nx, int degree) {
+  const size_t limb_d = (size_t)(3 * (nx + degree) + 1) / 2;
+  const size_t front = limb_d + nx + (size_t)nx * degree + 64;
+  const size_t solve = (size_t)2 * nx + (nx + nx / 4 + 4) + 40 + 8;
+  return (std::max(front, solve) + (nx + nx / 4 + 4) + 8) * sizeof(double);
+}
+
+static int fix_occupancy(int degree, size_t smem);
 static int step_occupancy(int degree, int K, size_t smem);
 
 static Plan make_plan(long long n, int p, int nx, int degree, bool with_coef) {
@@ -137,9 +158,13 @@ static Plan make_plan(long long n, int p, int nx, int degree, bool with_coef) {
   pl.K = choose_k(nx, degree);
   pl.H = step_nt() / pl.K;
   pl.smem = step_smem(nx, degree, pl.K, with_coef);
+  pl.fsmem = fix_smem(nx, degree);
   // grid independent of the mode so workspace sizes agree across calls: the
-  // occupancy of the leapfrog kernel (largest smem + registers) sizes it
-  pl.G = grid_for((long long)n * p, step_occupancy(degree, pl.K, step_smem(nx, degree, pl.K, true)));
+  // occupancy of the leapfrog kernel of this shape (phase path for K <= 2,
+  // fixed-point otherwise) sizes it
+  const int occ = pl.K > 2 ? fix_occupancy(degree, pl.fsmem)
+                           : step_occupancy(degree, pl.K, step_smem(nx, degree, pl.K, true));
+  pl.G = grid_for(n, p, occ);
   return pl;
 }
 
@@ -207,6 +232,31 @@ extern "C" int picrom_debug_timestamps(unsigned long long* out) {
 }
 #else
 #define TSTAMP(k, cond) do { } while (0)
+#endif
+
+#ifdef PICROM_EXP_TIMELINE
+// timing experiment only: per-CTA %globaltimer timeline of the leapfrog pass
+// (slot per CTA launch: [step, instance, t_entry, t_prologue, t_stream_end,
+//  t_fold, t_ticket, t_solve_end]); tools/timeline.py reads it back
+__device__ unsigned long long g_tl[16384][8];
+__device__ unsigned int g_tl_ctr;
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+extern "C" int picrom_debug_timeline(unsigned long long* out, int rows, int reset) {
+  if (reset) {
+    unsigned int z = 0;
+    static unsigned long long zeros[16384 * 8];
+    if (cudaMemcpyToSymbol(g_tl, zeros, sizeof(zeros)) != cudaSuccess) return -1;
+    return cudaMemcpyToSymbol(g_tl_ctr, &z, sizeof(z)) == cudaSuccess ? 0 : -1;
+  }
+  return cudaMemcpyFromSymbol(out, g_tl, (size_t)rows * 8 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}
+#define TL(k) do { if (MODE == MODE_LEAPFROG && threadIdx.x == 0 && tl_slot >= 0) g_tl[tl_slot][k] = tl_now(); } while (0)
+#else
+#define TL(k) do { } while (0)
 #endif
 
 // ----------------------------------------------------- per-instance solve
@@ -374,20 +424,26 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
     for (int nd = tid; nd < nx; nd += blockDim.x) rho_out[(size_t)j * nx + nd] = rho[nd];
   if (!a.solve && !a.energy_only) return;
 
+  // Means by every warp redundantly (one fixed lane order, identical in all
+  // warps): no block barrier for a reduction whose result every thread needs
+  auto warp_mean = [&](const double* v) {
+    const int lane = tid & 31;
+    double t = 0.0;
+    for (int q = lane; q < nx; q += 32) t += v[q];
+    return warp_sum(t) / (double)nx;
+  };
+  const double inv_h = 1.0 / h;
   double part = 0.0;
   if (!a.energy_only) {
-  for (int nd = tid; nd < nx; nd += blockDim.x) part += rho[nd];
-  const double mean_rho = block_sum(part, red) / (double)nx;
+  const double mean_rho = warp_mean(rho);
   TSTAMP(5, j == 0);
-  for (int nd = tid; nd < nx; nd += blockDim.x) rho[nd] -= mean_rho;
-  __syncthreads();
 #ifdef PICROM_EXP_NOCIRC
   if (false)     // timing experiment only
 #endif
-  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] b_m.  A lane owns
-  // 4 consecutive outputs and keeps khat[(n0 + i - m) mod nx], i < 4, in a
-  // register window that slides by one smem load per step of m (1 load per
-  // 4 FMAs); warps split the m range into mp parts, summed in fixed order.
+  // circulant solve phi_n = h * sum_m khat[(n - m) mod nx] (rho_m - mean).  A
+  // lane owns 4 consecutive outputs and keeps khat[(n0 + i - m) mod nx], i < 4,
+  // in a register window that slides by one smem load per step of m (1 load
+  // per 4 FMAs); warps split the m range into mp parts, summed in fixed order.
   {
     const int nw = blockDim.x >> 5, warp = tid >> 5, lane = tid & 31;
     const int og = (nx + 127) >> 7;
@@ -406,7 +462,8 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int m = mlo;
       for (; m + 4 <= mhi; m += 4) {
-        const double b0 = rho[m], b1 = rho[m + 1], b2 = rho[m + 2], b3 = rho[m + 3];
+        const double b0 = rho[m] - mean_rho, b1 = rho[m + 1] - mean_rho;
+        const double b2 = rho[m + 2] - mean_rho, b3 = rho[m + 3] - mean_rho;
         a0 = fma(w0, b0, a0); a1 = fma(w1, b0, a1); a2 = fma(w2, b0, a2); a3 = fma(w3, b0, a3);
         idx = dn(idx);
         const double x = kh[kh_pad(idx)];
@@ -421,7 +478,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
         w3 = x; w2 = y; w1 = z; w0 = kh[kh_pad(idx)];
       }
       for (; m < mhi; ++m) {
-        const double b0 = rho[m];
+        const double b0 = rho[m] - mean_rho;
         a0 = fma(w0, b0, a0); a1 = fma(w1, b0, a1); a2 = fma(w2, b0, a2); a3 = fma(w3, b0, a3);
         idx = dn(idx);
         w3 = w2; w2 = w1; w1 = w0; w0 = kh[kh_pad(idx)];
@@ -434,39 +491,38 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
     }
   }
   __syncthreads();
-  part = 0.0;
   for (int nd = tid; nd < nx; nd += blockDim.x) {
     double sum = prow[nd];
     for (int q = 1; q < mp; ++q) sum += prow[(size_t)q * nx + nd];
-    phi[nd] = h * sum;
-    part += phi[nd];
+    phi[nd] = h * sum;          // rho is dead: phi overwrites it
   }
-  TSTAMP(6, j == 0);
-  const double mean_phi = block_sum(part, red) / (double)nx;
-  for (int nd = tid; nd < nx; nd += blockDim.x) phi[nd] -= mean_phi;
   __syncthreads();
-  if (a.phi_out)
-    for (int nd = tid; nd < nx; nd += blockDim.x) a.phi_out[(size_t)j * nx + nd] = phi[nd];
+  TSTAMP(6, j == 0);
   }  // !energy_only
-  if (phi_hist)
-    for (int nd = tid; nd < nx; nd += blockDim.x) phi_hist[(size_t)j * nx + nd] = phi[nd];
-#ifdef PICROM_EXP_NOCIRC
-  if (false) {
-#else
-  if (energy_out) {
-#endif
-    // L phi with L = stencil / h (circulant, half bandwidth d)
-    const double inv_h = 1.0 / h;
-    part = 0.0;
-    for (int nd = tid; nd < nx; nd += blockDim.x) {
+  // phi -= mean(phi) (every warp's own mean, no barrier) while forming the
+  // energy terms: L (phi - mean) = L phi up to the stencil's rounding
+  const double mean_phi = a.energy_only ? 0.0 : warp_mean(phi);
+  for (int nd = tid; nd < nx; nd += blockDim.x) {
+    const double ph = phi[nd] - mean_phi;
+    if (energy_out) {
       double lp = stn[0] * phi[nd];
       for (int k = 1; k <= a.degree; ++k) {
         int up = nd + k; if (up >= nx) up -= nx;
         int dn = nd - k; if (dn < 0) dn += nx;
         lp = fma(stn[k], phi[up] + phi[dn], lp);
       }
-      part = fma(phi[nd], lp * inv_h, part);
+      part = fma(ph, lp * inv_h, part);
     }
+    if (!a.energy_only) {
+      if (a.phi_out) a.phi_out[(size_t)j * nx + nd] = ph;
+      if (phi_hist) phi_hist[(size_t)j * nx + nd] = ph;
+    }
+  }
+#ifdef PICROM_EXP_NOCIRC
+  if (false) {
+#else
+  if (energy_out) {
+#endif
     TSTAMP(7, j == 0);
     double e = block_sum(part, red);
     if (tid == 0) energy_out[j] = ip[I_HALFINVMP] * e;
@@ -501,6 +557,37 @@ template <int K> __host__ __device__ constexpr int step_u() { return PICROM_STEP
 template <int K> __host__ __device__ constexpr int step_u() { return K <= 2 ? 6 : 4; }
 #endif
 
+// Fixed-point deposit (FIX): value weights w in [0, 1] are rounded to
+// W = round(w 2^50) (one DFMA: the low mantissa bits of w 2^50 + 1.5 2^52),
+// split into three 17-bit limbs and added with native 32-bit shared-memory
+// reductions (red.shared.add.u32) into ONE histogram per CTA [3][nx + D].
+// Integer sums are exact and order independent, so the deposit is
+// deterministic with no lane phases; a limb word holds 2^15 adds of 2^17 - 1,
+// so a CTA folds its histogram into fp64 every kFixChunk particles (each
+// particle adds at most once to a row).  Resolution 2^-50 per weight.
+#ifndef PICROM_FIX_NT
+#define PICROM_FIX_NT 256
+#endif
+#ifndef PICROM_FIX_MINB
+#define PICROM_FIX_MINB 2
+#endif
+#ifndef PICROM_FIX_U
+#define PICROM_FIX_U 4
+#endif
+constexpr int kFixNT = PICROM_FIX_NT;
+constexpr int kFixMinB = PICROM_FIX_MINB;
+constexpr int kFixU = PICROM_FIX_U;
+constexpr int kFixChunk = 32767;
+
+// programmatic dependent launch between consecutive leapfrog steps: off --
+// with two instance groups pipelined on separate streams it cost 2-3 us per
+// step at C2 (65.4 vs 67.4 us), and it gains < 2 us with one group (r02)
+#ifdef PICROM_PDL
+constexpr bool kPdl = true;
+#else
+constexpr bool kPdl = false;
+#endif
+
 // L2 prefetch distance of the leapfrog pass, in SPAN blocks (0 = off)
 #ifndef PICROM_STEP_PF
 #define PICROM_STEP_PF 0
@@ -525,27 +612,50 @@ __device__ __noinline__ CellFrac locate_rare(double x, double h, double inv_h, i
 // so every access is conflict-free) and take turns (K phases); each lane
 // handles U particles per iteration (u*32 + lane within its warp's 32*U
 // block: coalesced), with the next iteration's loads issued first.
-template <int D, int K, int MODE, int NT>
-__global__ void __launch_bounds__(NT)
+template <int D, int K, int MODE, int NT, bool FIX>
+__global__ void __launch_bounds__(NT, FIX ? kFixMinB : 1)
 step_kernel(StepArgs a, SolveArgs sa) {
   extern __shared__ double smem[];
-  constexpr int H = NT / K;
+  constexpr int H = FIX ? 1 : NT / K;
   constexpr int NW = D + 1;
-  constexpr int U = step_u<K>();
+  constexpr int U = FIX ? kFixU : step_u<K>();
   constexpr int SPAN = NT * U;
   const int nx = a.nx;
   const int nh = nx + D;                       // histogram rows incl. ghost nodes
-  double* hist = smem;                         // [nh][H]
-  double* coef = hist + nh * H;                // [D][nx] field polynomials
+  // phase path: [nh][H] fp64 histograms; FIX: [3][nh] u32 limbs + [nx] fp64
+  // per-node sums of the folded chunks
+  double* hist = smem;
+  unsigned int* limbs = reinterpret_cast<unsigned int*>(smem);
+  const int fix_dw = (3 * nh + 1) / 2;         // limb words in doubles
+  double* acc = smem + fix_dw;
+  double* coef = FIX ? acc + nx : hist + nh * H;   // [D][nx] field polynomials
   double* red = coef + (MODE == MODE_LEAPFROG ? nx * D : 0);
   TSTAMP(0, MODE == MODE_LEAPFROG && blockIdx.x == 0);
+#ifdef PICROM_EXP_TIMELINE
+  int tl_slot = -1;
+  if (MODE == MODE_LEAPFROG && threadIdx.x == 0) {
+    tl_slot = (int)(atomicAdd(&g_tl_ctr, 1u) & 16383u);
+    g_tl[tl_slot][0] = a.counter ? (unsigned long long)*a.counter : 0ull;
+    g_tl[tl_slot][1] = (unsigned long long)(cta_start(blockIdx.x, a.n * (long long)a.p, gridDim.x) / a.n);
+  }
+#endif
+  TL(2);
   double* kh_pre = red + 64;                   // LEAPFROG: khat (padded) + stencil
   double* stn_pre = kh_pre + (nx + nx / 4 + 4);
   if (MODE == MODE_LEAPFROG && a.fuse_solve == 1) {
     for (int r = threadIdx.x; r < nx; r += NT) kh_pre[kh_pad(r)] = sa.khat[r];
     if (sa.stencil && threadIdx.x <= D) stn_pre[threadIdx.x] = sa.stencil[threadIdx.x];
   }
-  const unsigned int hist_base = smem_u32(hist + myh_of<K>(threadIdx.x));
+  if constexpr (MODE == MODE_LEAPFROG && kPdl) {
+    // programmatic dependent launch: the next step's grid may be scheduled
+    // now (its CTAs take SM slots as ours exit and park in griddepcontrol.wait),
+    // and everything above (constants only) overlapped the previous step's
+    // tail; x, v, phi and the step counter are read only after the previous
+    // grid has completed and its writes are visible
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  const unsigned int hist_base = FIX ? smem_u32(limbs) : smem_u32(hist + myh_of<K>(threadIdx.x));
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -624,7 +734,12 @@ step_kernel(StepArgs a, SolveArgs sa) {
     if (len > 0) load(0, ax, av, ae);
 
 #ifndef PICROM_EXP_NOHIST
-    for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
+    if constexpr (FIX) {
+      for (int q = tid; q < 3 * nh; q += NT) limbs[q] = 0u;
+      for (int q = tid; q < nx; q += NT) acc[q] = 0.0;
+    } else {
+      for (int q = tid; q < nh * H; q += NT) hist[q] = 0.0;
+    }
 #endif
     if (MODE == MODE_LEAPFROG && j != last_j) {
       const double* ph = a.phi + (size_t)j * nx;
@@ -640,6 +755,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
       }
     }
     __syncthreads();
+    TL(3);
 
     // the particle work of one SPAN block already in registers
     auto process = [&](int b0, const double* cx, const double* cv, const double* ce) {
@@ -761,7 +877,25 @@ step_kernel(StepArgs a, SolveArgs sa) {
         }
         hrow[u] = hist_base + (unsigned int)(cl[u] * H) * 8u;
       }
-      if constexpr (K == 32) {
+      if constexpr (FIX) {
+        // exact integer deposit: 3 limbs per weight, one red.shared.add.u32
+        // each; rows are limb-major [3][nh]
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int m = 0; m < NW; ++m) {
+            const double t = fma(w[u][m], 0x1p50, 0x1.8p52);
+            const unsigned int lo = __double2loint(t), hi = __double2hiint(t);
+            const unsigned int l0 = lo & 0x1ffffu;
+            const unsigned int l1 = __funnelshift_r(lo, hi, 17) & 0x1ffffu;
+            const unsigned int l2 = (hi >> 2) & 0x1ffffu;
+            const unsigned int addr = hist_base + (unsigned int)(cl[u] + m) * 4u;
+            red_shared_u32_if(addr, l0, ok[u]);
+            red_shared_u32_if(addr + (unsigned int)nh * 4u, l1, ok[u]);
+            red_shared_u32_if(addr + (unsigned int)nh * 8u, l2, ok[u]);
+          }
+        }
+      } else if constexpr (K == 32) {
         // one histogram per warp (large meshes, e.g. C5's Nx = 512): four
         // phases by cell mod 4 -- two cells of one phase are either equal or
         // >= 4 apart, so their D+1 <= 4 rows are disjoint -- and, inside a
@@ -809,14 +943,38 @@ step_kernel(StepArgs a, SolveArgs sa) {
 
     // ping-pong register buffers: the loads of one block are in flight while
     // the other block is processed; no register copies on the loop edge
+    // FIX: fold the limbs into acc (and re-zero them) every CH particles, so no
+    // limb word can overflow; each thread owns the rows of its nodes
+    constexpr int CH = FIX ? (kFixChunk / (2 * SPAN)) * (2 * SPAN) : (1 << 30);
+    static_assert(!FIX || CH >= 2 * SPAN, "kFixChunk too small for the block span");
+    auto fold_limbs = [&](int nd) {
+      double v = 0.0;
+      for (int r = (nd - Spline<D>::OFF) % nx; r < nh; r += nx) {
+        const double a0 = (double)limbs[r], a1 = (double)limbs[nh + r], a2 = (double)limbs[2 * nh + r];
+        v += fma(a2, 0x1p-16, fma(a1, 0x1p-33, a0 * 0x1p-50));
+      }
+      return v;
+    };
     for (int b0 = 0; b0 < len; b0 += 2 * SPAN) {
       if (b0 + SPAN < len) load(b0 + SPAN, bx, bv, be);
       process(b0, ax, av, ae);
       if (b0 + SPAN >= len) break;
       if (b0 + 2 * SPAN < len) load(b0 + 2 * SPAN, ax, av, ae);
       process(b0 + SPAN, bx, bv, be);
+      if constexpr (FIX) {
+        if ((b0 + 2 * SPAN) % CH == 0 && b0 + 2 * SPAN < len) {
+          __syncthreads();
+          for (int nd = tid; nd < nx; nd += NT) {
+            acc[nd] += fold_limbs(nd);
+            for (int r = (nd - Spline<D>::OFF) % nx; r < nh; r += nx)
+              limbs[r] = limbs[nh + r] = limbs[2 * nh + r] = 0u;
+          }
+          __syncthreads();
+        }
+      }
     }
     TSTAMP(1, MODE == MODE_LEAPFROG && j == 0 && seg_hi == a.n);
+    TL(4);
     __syncthreads();
 
     // fold ghost rows, reduce the H histograms in a fixed order -> segment row.
@@ -826,6 +984,9 @@ step_kernel(StepArgs a, SolveArgs sa) {
 #ifdef PICROM_EXP_NOHIST
     if (false)
 #endif
+    if constexpr (FIX) {
+      for (int nd = tid; nd < nx; nd += NT) a.seg_hist[(size_t)seg * nx + nd] = acc[nd] + fold_limbs(nd);
+    } else
     for (int nd = tid; nd < nx; nd += NT) {
       double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       // histogram row r holds node (r + OFF) mod nx: rows r0, r0 + nx, ... < nh
@@ -842,6 +1003,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
           ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     }
     TSTAMP(2, MODE == MODE_LEAPFROG && j == 0 && seg_hi == a.n);
+    TL(5);
     if constexpr (MODE == MODE_LEAPFROG) {
       double ks = block_sum(kin, red);
       if (tid == 0) a.seg_kin[seg] = ks;
@@ -860,6 +1022,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
           if (s_last) a.inst_done[j] = 0u;
         }
         __syncthreads();
+        TL(6);
 #ifdef PICROM_EXP_NOSOLVE
         if (false) {     // timing experiment only
 #else
@@ -868,9 +1031,9 @@ step_kernel(StepArgs a, SolveArgs sa) {
           __threadfence();
           TSTAMP(3, j == 0);
           // scratch = the histogram, coefficient and reduction smem (free now)
-          solve_body(sa, j, hist, (unsigned int)a.p,
-                     (size_t)nh * H + (MODE == MODE_LEAPFROG ? (size_t)nx * D : 0) + 64,
+          solve_body(sa, j, hist, (unsigned int)a.p, (size_t)(red + 64 - smem),
                      kh_pre, stn_pre, a.counter ? step_id - 1 : -1);
+          TL(7);
         }
       }
     }
@@ -909,27 +1072,52 @@ int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, cons
 
 // --------------------------------------------------------- launch helpers
 
-template <int D, int K, int MODE>
+template <int D, int K, int MODE, bool FIX>
 static int launch_step_t(const StepArgs& a, const SolveArgs& sa, const Plan& pl, cudaStream_t s) {
-  auto kfn = step_kernel<D, K, MODE, 128>;
+  constexpr int NT = FIX ? kFixNT : 128;
+  auto kfn = step_kernel<D, K, MODE, NT, FIX>;
   static bool attr = false;
   if (!attr) {
     allow_max_dynamic_smem(kfn);
     attr = true;
   }
-  kfn<<<pl.G, 128, pl.smem, s>>>(a, sa);
+  if (MODE == MODE_LEAPFROG && kPdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pl.G);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = FIX ? pl.fsmem : pl.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_pdl[1];
+    attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr_pdl;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kfn, a, sa) != cudaSuccess) return check_launch("step_kernel (PDL)");
+    return check_launch("step_kernel");
+  }
+  kfn<<<pl.G, NT, FIX ? pl.fsmem : pl.smem, s>>>(a, sa);
   return check_launch("step_kernel");
 }
 
 template <int D, int MODE>
 static int launch_step_k(const StepArgs& a, const SolveArgs& sa, const Plan& pl, cudaStream_t s) {
+#ifdef PICROM_NO_FIX
+  const bool fix = false;      // dev variant: lane-phase fp64 histograms everywhere
+#else
+  // value weights in [0, 1] take the fixed-point deposit where lane phases
+  // would be K > 2 (Nx > 256 at degree 3): measured 126 vs 71 G pushes/s at
+  // C5's Nx = 512; at K <= 2 the conflict-free fp64 phases are faster (C2's
+  // Nx = 128: 106 vs 97, profiles/r02)
+  const bool fix = pl.K > 2 && !(MODE == MODE_DEPOSIT && (a.y != nullptr || a.wkind != 0));
+#endif
+  if (fix) return launch_step_t<D, 1, MODE, true>(a, sa, pl, s);
   switch (pl.K) {
-    case 1: return launch_step_t<D, 1, MODE>(a, sa, pl, s);
-    case 2: return launch_step_t<D, 2, MODE>(a, sa, pl, s);
-    case 4: return launch_step_t<D, 4, MODE>(a, sa, pl, s);
-    case 8: return launch_step_t<D, 8, MODE>(a, sa, pl, s);
-    case 16: return launch_step_t<D, 16, MODE>(a, sa, pl, s);
-    default: return launch_step_t<D, 32, MODE>(a, sa, pl, s);
+    case 1: return launch_step_t<D, 1, MODE, false>(a, sa, pl, s);
+    case 2: return launch_step_t<D, 2, MODE, false>(a, sa, pl, s);
+    case 4: return launch_step_t<D, 4, MODE, false>(a, sa, pl, s);
+    case 8: return launch_step_t<D, 8, MODE, false>(a, sa, pl, s);
+    case 16: return launch_step_t<D, 16, MODE, false>(a, sa, pl, s);
+    default: return launch_step_t<D, 32, MODE, false>(a, sa, pl, s);
   }
 }
 
@@ -946,10 +1134,19 @@ static int launch_step(const StepArgs& a, int degree, const Plan& pl, cudaStream
   return set_err(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
 }
 
+template <int D>
+static int fix_occ_of(size_t smem) {
+  int occ = 0;
+  auto kfn = step_kernel<D, 1, MODE_LEAPFROG, kFixNT, true>;
+  allow_max_dynamic_smem(kfn);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kFixNT, smem) != cudaSuccess) occ = 1;
+  return occ;
+}
+
 template <int D, int K>
 static int occ_of(size_t smem) {
   int occ = 0;
-  auto kfn = step_kernel<D, K, MODE_LEAPFROG, 128>;
+  auto kfn = step_kernel<D, K, MODE_LEAPFROG, 128, false>;
   allow_max_dynamic_smem(kfn);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, smem) != cudaSuccess) occ = 1;
   return occ;
@@ -968,7 +1165,7 @@ static int occ_k(int K, size_t smem) {
 }
 
 static int step_occupancy(int degree, int K, size_t smem) {
-  static int cache[4][6][2] = {};   // degree x log2 K x (smem key valid) -- small memo
+  static int cache[4][6][2] = {};   // degree x log2 K x (valid, occupancy)
   static size_t cache_smem[4][6] = {};
   int lk = 0;
   while ((1 << lk) < K) ++lk;
@@ -977,6 +1174,16 @@ static int step_occupancy(int degree, int K, size_t smem) {
   cache[degree][lk][0] = 1;
   cache[degree][lk][1] = occ;
   cache_smem[degree][lk] = smem;
+  return occ;
+}
+
+static int fix_occupancy(int degree, size_t smem) {
+  static int cache_occ[4] = {};
+  static size_t cache_smem[4] = {};
+  if (cache_occ[degree] && cache_smem[degree] == smem) return cache_occ[degree];
+  const int occ = degree == 1 ? fix_occ_of<1>(smem) : degree == 2 ? fix_occ_of<2>(smem) : fix_occ_of<3>(smem);
+  cache_occ[degree] = occ;
+  cache_smem[degree] = smem;
   return occ;
 }
 
@@ -1128,8 +1335,8 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
                                const double* inst, int nx, int degree, const double* khat,
                                const double* stencil, double* phi, double dt, double kick,
                                double kfull, long long step, long long* counter,
-                               long long hist_rows, double* rho_hist, double* phi_hist,
-                               double* ee_hist, double* kin_hist, void* ws,
+                               long long hist_rows, int hist_p, double* rho_hist,
+                               double* phi_hist, double* ee_hist, double* kin_hist, void* ws,
                                unsigned long long* status, void* stream) {
   int rc = check_cfg(n, p, nx, degree);
   if (rc) return rc;
@@ -1144,9 +1351,12 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
   sa.seg_hist = a.seg_hist; sa.seg_kin = a.seg_kin; sa.inst = inst; sa.khat = khat;
   sa.stencil = stencil; sa.n = n; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = pl.G;
   sa.solve = true; sa.phi_out = phi;
-  const size_t gp = (size_t)p * nx;
+  // history rows hold hist_p >= p instances (an instance group writes its
+  // slice of a shared history at the caller's pointer offset)
+  if (hist_p < p) hist_p = p;
+  const size_t gp = (size_t)hist_p * nx;
   sa.hist_stride_rho = gp;
-  sa.hist_stride_e = (size_t)p;
+  sa.hist_stride_e = (size_t)hist_p;
   if (counter) {
     sa.counter = counter;
     sa.done = reinterpret_cast<unsigned int*>(counter + 1);
@@ -1155,8 +1365,8 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
   } else {
     sa.rho_out = rho_hist ? rho_hist + (size_t)step * gp : nullptr;
     sa.phi_hist = phi_hist ? phi_hist + (size_t)step * gp : nullptr;
-    sa.energy_out = ee_hist ? ee_hist + (size_t)step * p : nullptr;
-    sa.kin_out = kin_hist ? kin_hist + (size_t)step * p : nullptr;
+    sa.energy_out = ee_hist ? ee_hist + (size_t)step * hist_p : nullptr;
+    sa.kin_out = kin_hist ? kin_hist + (size_t)step * hist_p : nullptr;
   }
   return launch_step<MODE_LEAPFROG>(a, degree, pl, (cudaStream_t)stream, &sa);
 }
@@ -1272,10 +1482,19 @@ static int launch_gather(const GatherArgs& a, int degree, cudaStream_t s) {
   dim3 grid((unsigned)((a.n + kChunk - 1) / kChunk), (unsigned)a.p);
   size_t sm = (size_t)(degree + 1) * a.nx * sizeof(double);
   if (grid.y > 65535) return set_err(PICROM_ERR_CONFIG, "p > 65535");
+  // (d+1) nx doubles of cell polynomials: beyond 48 KB (nx > 1536 at d = 3)
+  // the kernel needs the opt-in dynamic shared-memory limit
+  static bool attr[4] = {false, false, false, false};
   switch (degree) {
-    case 1: gather_kernel<1, KICK><<<grid, kThreads, sm, s>>>(a); break;
-    case 2: gather_kernel<2, KICK><<<grid, kThreads, sm, s>>>(a); break;
-    case 3: gather_kernel<3, KICK><<<grid, kThreads, sm, s>>>(a); break;
+    case 1:
+      if (!attr[1]) { allow_max_dynamic_smem(gather_kernel<1, KICK>); attr[1] = true; }
+      gather_kernel<1, KICK><<<grid, kThreads, sm, s>>>(a); break;
+    case 2:
+      if (!attr[2]) { allow_max_dynamic_smem(gather_kernel<2, KICK>); attr[2] = true; }
+      gather_kernel<2, KICK><<<grid, kThreads, sm, s>>>(a); break;
+    case 3:
+      if (!attr[3]) { allow_max_dynamic_smem(gather_kernel<3, KICK>); attr[3] = true; }
+      gather_kernel<3, KICK><<<grid, kThreads, sm, s>>>(a); break;
     default: return set_err(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
   }
   return check_launch("gather_kernel");

@@ -256,26 +256,47 @@ class FullOrderRecord:
     final_state: object = None                     # ParticleEnsemble at t_final
 
 
+def _auto_groups(p, n):
+    """Instance groups pipelined on separate streams: while one group's step
+    drains (last CTAs, per-instance solve) the next group streams particles.
+    Worth it where the per-step fixed cost is a visible share of the step
+    (C2: 8 M particles, ~80 us); a single group for huge steps (C5) or p = 1."""
+    if p < 2:
+        return 1
+    return 2 if n * p <= (64 << 20) else 1
+
+
 class PicEngine:
     """Persistent device state of the leapfrog loop for one (system, p, N, dt):
-    x, v (p, N), phi, workspace, status, step counter and ring histories, plus
-    one captured CUDA graph of `graph_steps` steps that every later run
-    replays (all its pointers live here, so the graph stays valid)."""
+    x, v (p, N), phi, per-group workspaces, status words and step counters,
+    ring histories, plus one captured CUDA graph of `graph_steps` steps that
+    every later run replays (all its pointers live here, so the graph stays
+    valid).  The p instances are split into `groups` contiguous instance
+    groups, each stepped by its own chain of fused kernels on its own stream;
+    the chains only join at the ends of a block of steps, so one group's
+    per-step tail (the last CTAs and the in-kernel Poisson solve) overlaps the
+    next group's particle streaming."""
 
-    def __init__(self, system, p, n, dt, graph_steps=16):
+    def __init__(self, system, p, n, dt, graph_steps=16, groups=None):
         self.system = system
         self.p, self.n, self.dt = p, n, float(dt)
         mesh = system.mesh
         self.nx, self.degree = mesh.num_cells, mesh.degree
         self.inst = system.inst(p)
         self.c = system.poisson.constants
-        self.ws = torch.zeros(int(_lib.query("picrom_fom_workspace_bytes", n, p, self.nx,
-                                             self.degree)), dtype=torch.uint8, device="cuda")
+        self.groups = _auto_groups(p, n) if groups is None else max(1, min(int(groups), p))
+        edges = np.linspace(0, p, self.groups + 1).astype(int)
+        self.slices = [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
+        self.ws = [torch.zeros(int(_lib.query("picrom_fom_workspace_bytes", n, b - a, self.nx,
+                                              self.degree)), dtype=torch.uint8, device="cuda")
+                   for a, b in self.slices]
         self.x = torch.empty((p, n), dtype=torch.float64, device="cuda")
         self.v = torch.empty((p, n), dtype=torch.float64, device="cuda")
         self.phi = torch.empty((p, self.nx), dtype=torch.float64, device="cuda")
-        self.status = dev.new_status()
-        self.counter = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self.status = [dev.new_status() for _ in self.slices]
+        self.init_status = dev.new_status()      # the initial all-instance deposit
+        self.counters = [torch.zeros(2, dtype=torch.int64, device="cuda") for _ in self.slices]
+        self.streams = [torch.cuda.Stream() for _ in self.slices] if self.groups > 1 else None
         self.ring = int(graph_steps)
         self.r_rho = torch.zeros((self.ring, p, self.nx), dtype=torch.float64, device="cuda")
         self.r_phi = torch.zeros_like(self.r_rho)
@@ -284,37 +305,78 @@ class PicEngine:
         self.graph = None
         self.launches = 0
 
-    def launch(self, first):
-        """One PIC step: a single fused kernel (push + last-CTA solve)."""
+    def reset(self):
+        self.init_status.fill_(-1)
+        for st in self.status:
+            st.fill_(-1)
+        for ct in self.counters:
+            ct.zero_()
+
+    def _launch_group(self, g, first, stream):
+        """One PIC step of instance group g: a single fused kernel (push +
+        last-CTA solve) writing its slice of the shared ring histories."""
+        a, b = self.slices[g]
         dt = self.dt
         kick, kfull = (0.5 * dt, 0.0) if first else (dt, 0.5 * dt)
-        _lib.call("picrom_pic_step", self.x.data_ptr(), self.v.data_ptr(), self.n, self.p, self.n,
-                  self.inst.data_ptr(), self.nx, self.degree, self.c.khat.data_ptr(),
-                  self.c.stencil.data_ptr(), self.phi.data_ptr(), dt, kick, kfull, 0,
-                  self.counter.data_ptr(), self.ring, self.r_rho.data_ptr(), self.r_phi.data_ptr(),
-                  self.r_ee.data_ptr(), self.r_kin.data_ptr(), self.ws.data_ptr(),
-                  self.status.data_ptr(), dev.stream_handle())
+        n, nx = self.n, self.nx
+        _lib.call("picrom_pic_step", self.x.data_ptr() + 8 * a * n, self.v.data_ptr() + 8 * a * n,
+                  n, b - a, n, self.inst.data_ptr() + 8 * dev.INST_STRIDE * a, nx, self.degree,
+                  self.c.khat.data_ptr(), self.c.stencil.data_ptr(),
+                  self.phi.data_ptr() + 8 * a * nx, dt, kick, kfull, 0,
+                  self.counters[g].data_ptr(), self.ring, self.p,
+                  self.r_rho.data_ptr() + 8 * a * nx, self.r_phi.data_ptr() + 8 * a * nx,
+                  self.r_ee.data_ptr() + 8 * a, self.r_kin.data_ptr() + 8 * a,
+                  self.ws[g].data_ptr(), self.status[g].data_ptr(), stream)
         self.launches += 1
+
+    def launch_block(self, steps, first=False):
+        """`steps` consecutive PIC steps of every instance group; the group
+        chains fork from and join the current stream once per block."""
+        if self.streams is None:
+            for k in range(steps):
+                self._launch_group(0, first and k == 0, dev.stream_handle())
+            return
+        main = torch.cuda.current_stream()
+        for st in self.streams:
+            st.wait_stream(main)
+        for k in range(steps):
+            for g, st in enumerate(self.streams):
+                self._launch_group(g, first and k == 0, st.cuda_stream)
+        for st in self.streams:
+            main.wait_stream(st)
+
+    def launch(self, first):
+        self.launch_block(1, first)
 
     def replay(self):
         if self.graph is None:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                for _ in range(self.ring):
-                    self.launch(first=False)
-            self.launches -= self.ring
+                self.launch_block(self.ring)
+            self.launches -= self.ring * self.groups
             self.graph = g
         self.graph.replay()
-        self.launches += self.ring
+        self.launches += self.ring * self.groups
+
+    def bad(self):
+        """None, or (step, row, global column) of the first non-finite position."""
+        worst = None
+        for (a, b), st in [((0, self.p), self.init_status)] + list(zip(self.slices, self.status)):
+            bad = dev.decode_status(st, b - a)
+            if bad is not None:
+                bad = (bad[0], bad[1], bad[2] + a)
+                if worst is None or (bad[0], bad[1] * self.p + bad[2]) < (worst[0], worst[1] * self.p + worst[2]):
+                    worst = bad
+        return worst
 
 
-def _engine(system, p, n, dt):
+def _engine(system, p, n, dt, groups=None):
     cache = system.__dict__.setdefault("_engines", {})
-    key = (p, n, float(dt), torch.cuda.current_device())
+    key = (p, n, float(dt), torch.cuda.current_device(), groups)
     eng = cache.get(key)
     if eng is None:
         cache.clear()                      # one resident engine per system
-        eng = cache[key] = PicEngine(system, p, n, dt)
+        eng = cache[key] = PicEngine(system, p, n, dt, groups=groups)
     return eng
 
 
@@ -328,14 +390,13 @@ class PicRun:
     kinetic energy (steps+1, p), filled from the engine's ring after each block.
     """
 
-    def __init__(self, system, xd, vd, dt, num_steps, keep_rho=True):
+    def __init__(self, system, xd, vd, dt, num_steps, keep_rho=True, groups=None):
         self.system = system
         self.p, self.n = xd.shape
-        self.e = _engine(system, self.p, self.n, dt)
+        self.e = _engine(system, self.p, self.n, dt, groups)
         self.e.x.copy_(xd)
         self.e.v.copy_(vd)
-        self.e.status.fill_(-1)
-        self.e.counter.zero_()
+        self.e.reset()
         self.dt = float(dt)
         self.num_steps = int(num_steps)
         self.nx, self.degree = self.e.nx, self.e.degree
@@ -360,10 +421,6 @@ class PicRun:
         return self.e.phi
 
     @property
-    def status(self):
-        return self.e.status
-
-    @property
     def launches(self):
         return self.e.launches
 
@@ -373,8 +430,9 @@ class PicRun:
         s = dev.stream_handle()
         rho0 = self.rho_hist[0] if self.rho_hist is not None else torch.empty(
             (self.p, self.nx), dtype=torch.float64, device="cuda")
+        ws = dev.workspace(self.n, self.p, self.nx, self.degree)
         _lib.call("picrom_deposit", e.x.data_ptr(), self.n, self.p, self.n, e.inst.data_ptr(),
-                  self.nx, self.degree, rho0.data_ptr(), e.ws.data_ptr(), e.status.data_ptr(), s)
+                  self.nx, self.degree, rho0.data_ptr(), ws.data_ptr(), e.init_status.data_ptr(), s)
         _lib.call("picrom_poisson", rho0.data_ptr(), self.p, self.nx, self.degree,
                   e.inst.data_ptr(), e.c.khat.data_ptr(), e.c.stencil.data_ptr(),
                   e.phi.data_ptr(), self.ee_hist[0].data_ptr(), s)
@@ -382,14 +440,23 @@ class PicRun:
         e.launches += 3
 
     def _drain(self, c0, count):
-        """Copy ring rows of counters [c0, c0+count) into the full histories."""
+        """Copy ring rows of counters [c0, c0+count) into the full histories:
+        the ring positions are contiguous modulo the ring, so at most two
+        contiguous device-to-device copies per history (no index kernels)."""
         e = self.e
-        idx = torch.arange(c0, c0 + count, device="cuda") % e.ring
-        self.kin_hist[c0:c0 + count] = e.r_kin[idx]
-        self.ee_hist[c0 + 1:c0 + count + 1] = e.r_ee[idx]
-        self.phi_hist[c0 + 1:c0 + count + 1] = e.r_phi[idx]
-        if self.rho_hist is not None:
-            self.rho_hist[c0 + 1:c0 + count + 1] = e.r_rho[idx]
+        r0 = c0 % e.ring
+        parts = [(r0, min(count, e.ring - r0))]
+        if parts[0][1] < count:
+            parts.append((0, count - parts[0][1]))
+        done = 0
+        for r, m in parts:
+            t = c0 + done
+            self.kin_hist[t:t + m].copy_(e.r_kin[r:r + m])
+            self.ee_hist[t + 1:t + m + 1].copy_(e.r_ee[r:r + m])
+            self.phi_hist[t + 1:t + m + 1].copy_(e.r_phi[r:r + m])
+            if self.rho_hist is not None:
+                self.rho_hist[t + 1:t + m + 1].copy_(e.r_rho[r:r + m])
+            done += m
 
     def advance(self, k, use_graph=True):
         """Advance k steps; full ring-sized blocks replay the cached graph."""
@@ -434,7 +501,7 @@ class PicRun:
         return vfull
 
     def check(self):
-        bad = dev.decode_status(self.e.status, self.p)
+        bad = self.e.bad()
         if bad is not None:
             step, row, col = bad
             t = step * self.dt

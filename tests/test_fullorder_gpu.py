@@ -153,6 +153,9 @@ def test_push_plus_solve_equals_fused_step(mods):
         run.init_field()
         e = run.e
         s = dev.stream_handle()
+        ws = torch.zeros(int(_lib.query("picrom_fom_workspace_bytes", n, p, nx, d)),
+                         dtype=torch.uint8, device="cuda")
+        st = dev.new_status()
         rho = torch.zeros((4, p, nx), dtype=torch.float64, device="cuda")
         phi = torch.zeros_like(rho)
         ee = torch.zeros((4, p), dtype=torch.float64, device="cuda")
@@ -162,17 +165,17 @@ def test_push_plus_solve_equals_fused_step(mods):
             if split:
                 _lib.call("picrom_pic_push", e.x.data_ptr(), e.v.data_ptr(), n, p, n,
                           e.inst.data_ptr(), nx, d, e.phi.data_ptr(), 0.05, kick, kfull, k,
-                          None, e.ws.data_ptr(), e.status.data_ptr(), s)
+                          None, ws.data_ptr(), st.data_ptr(), s)
                 _lib.call("picrom_pic_solve", n, p, nx, d, e.inst.data_ptr(),
                           e.c.khat.data_ptr(), e.c.stencil.data_ptr(), e.phi.data_ptr(), k,
                           None, 0, rho.data_ptr(), phi.data_ptr(), ee.data_ptr(), kin.data_ptr(),
-                          e.ws.data_ptr(), s)
+                          ws.data_ptr(), s)
             else:
                 _lib.call("picrom_pic_step", e.x.data_ptr(), e.v.data_ptr(), n, p, n,
                           e.inst.data_ptr(), nx, d, e.c.khat.data_ptr(), e.c.stencil.data_ptr(),
-                          e.phi.data_ptr(), 0.05, kick, kfull, k, None, 0, rho.data_ptr(),
-                          phi.data_ptr(), ee.data_ptr(), kin.data_ptr(), e.ws.data_ptr(),
-                          e.status.data_ptr(), s)
+                          e.phi.data_ptr(), 0.05, kick, kfull, k, None, 0, 0, rho.data_ptr(),
+                          phi.data_ptr(), ee.data_ptr(), kin.data_ptr(), ws.data_ptr(),
+                          st.data_ptr(), s)
         outs.append([t.cpu().numpy() for t in (e.x, e.v, rho, phi, ee, kin)])
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
