@@ -39,3 +39,21 @@ def lib_built():
     from paper_2201_05555_b200 import _build, _lib
     _build.build()
     return _lib.load()
+
+
+@pytest.fixture
+def parity_report(request):
+    """rec(**values): append the measured errors of a parity test as one JSON
+    line to $PICROM_PARITY_REPORT (no-op when unset) -- the numbers DESIGN.md
+    quotes come from this file (profiles/)."""
+    import json
+    path = os.environ.get("PICROM_PARITY_REPORT")
+
+    def rec(**kv):
+        if path:
+            row = {"test": request.node.name}
+            row.update({k: (float(v) if not isinstance(v, (list, str)) else v) for k, v in kv.items()})
+            with open(path, "a") as f:
+                f.write(json.dumps(row) + "\n")
+
+    return rec

@@ -4,7 +4,7 @@ inside the GPU test budget.  Run in the build container:
 
     python tests/golden/make_config_golden.py C2        # full C2: 8 M particles, 500 steps
     python tests/golden/make_config_golden.py C3r       # C3 reduced run, N = 5e4, 200 steps
-    python tests/golden/make_config_golden.py C4r       # C4 hyper-reduced run, N = 5e4, 200 steps
+    python tests/golden/make_config_golden.py C4r       # C4 at N = 5e4: warm-up, first DEIM fit, failure
 
 Each writes tests/golden/config_<name>.npz with small arrays only (energy
 histories, charge/potential at sampled steps, fixed-point counts, DEIM
@@ -105,12 +105,69 @@ def make_rom(name):
     print(f"{name}: {time.time() - t0:.0f}s, fp {np.mean(h.fp_iterations):.2f}", flush=True)
 
 
+def make_c4r():
+    """C4 at N = 5e4: the reference algorithm's hyper-reduced fixed point does
+    not converge at this particle count (it does at N = 1e6, see the
+    full-scale teacher-forced test), so the fixture records the 20 warm-up
+    steps, the first DEIM fit at step 21 and the StepFailure it ends in."""
+    from oracle import dmd_deim as odd
+    from oracle import manifold as mf
+    from oracle import rom_loop as orl
+    from paper_2201_05555_b200 import workloads as wl
+    w = wl.config("C4")
+    x0, v0 = wl.generate(w, num_particles=ROM_N)
+    params = np.stack([w.wavenumbers, w.alphas], axis=1)
+    ex = w.extra
+    osys = orl.ParamSystem(w.lengths, w.num_cells, w.degree, ROM_N)
+    t0 = time.time()
+    u0, z0 = mf.csvd_basis(x0, v0, ex["basis_dim"])
+    steps, fits = [], []
+    prk2, deim_fit = mf.prk2, odd.deim_fit
+
+    def rec_prk2(*a, **k):
+        r = prk2(*a, **k)
+        steps.append(r)
+        return r
+
+    def rec_fit(*a, **k):
+        d = deim_fit(*a, **k)
+        fits.append(d)
+        return d
+
+    mf.prk2, odd.deim_fit = rec_prk2, rec_fit
+    try:
+        orl.run_reduced(osys, params, x0, v0, basis_dim=ex["basis_dim"], subsample=ex["subsample"],
+                        window=ex["window"], deim_dim=ex["deim_dim"], deim_period=ex["deim_period"],
+                        deim_update=ex["deim_update"], dt=w.dt, num_steps=ex["window"] + 1,
+                        hyper_reduction=True, energy_stride=10**9, snapshot_stride=10**9,
+                        u0=u0, z0=z0)
+        raise SystemExit("expected the hyper-reduced fixed point to fail at N = 5e4")
+    except mf.StepFailure as err:
+        failure = err
+    finally:
+        mf.prk2, odd.deim_fit = prk2, deim_fit
+    last = steps[-1]
+    ee, kin = orl._energies(osys, last.u, last.z)
+    np.savez_compressed(
+        OUT / "config_C4r.npz", num_particles=ROM_N, warm_steps=len(steps),
+        fp_iterations=np.asarray([r.fp_iterations for r in steps], dtype=np.int64),
+        z_warm=last.z, u_warm_rows=last.u[ROM_ROWS], rows=ROM_ROWS, electric_warm=ee,
+        kinetic_warm=kin, deim_indices=np.asarray(fits[0].indices, dtype=np.int64),
+        deim_weights=np.asarray(fits[0].weights), fail_iterations=failure.iterations,
+        fail_trace=np.asarray(failure.residual_trace), z0=z0, u0_rows=u0[ROM_ROWS],
+        seed=w.seed, seconds=time.time() - t0)
+    print(f"C4r: {time.time() - t0:.0f}s, warm fp {[r.fp_iterations for r in steps]}, "
+          f"fail trace {failure.residual_trace[:3]} ... {failure.residual_trace[-1]:.3e}", flush=True)
+
+
 def main():
     for name in sys.argv[1:] or ["C2", "C3r", "C4r"]:
         if name == "C2":
             make_c2()
-        elif name in ("C3r", "C4r"):
+        elif name == "C3r":
             make_rom(name)
+        elif name == "C4r":
+            make_c4r()
         else:
             raise SystemExit(f"unknown fixture {name}")
 

@@ -61,7 +61,7 @@ def oracle_rho_phi(w, x_pn, cols=None):
     return np.stack([o[0] for o in out], axis=1), np.stack([o[1] for o in out], axis=1)
 
 
-def check_teacher_forced(w, run, k, x_pn, tag):
+def check_teacher_forced(w, run, k, x_pn, tag, report=None):
     """GPU rho_k / phi_k of the run vs the oracle's on the run's own x_k."""
     rho_o, phi_o = oracle_rho_phi(w, x_pn)
     rho_g = run.rho_hist[k].cpu().numpy().T
@@ -72,6 +72,8 @@ def check_teacher_forced(w, run, k, x_pn, tag):
     assert e_rho <= 1e-12, (tag, k, e_rho)
     assert e_phi <= 1e-12, (tag, k, e_phi)
     assert e_part <= 1e-14, (tag, k, e_part)
+    if report:
+        report(step=k, teacher_forced_rho=e_rho, teacher_forced_phi=e_phi, rho_vs_particle_term=e_part)
     return e_rho, e_phi
 
 
@@ -87,7 +89,7 @@ def _gpu_run(mods, w, x_pn, v_pn, steps):
     return sysm, run
 
 
-def test_c1_full_size_free_run(mods):
+def test_c1_full_size_free_run(mods, parity_report):
     """C1 at its size: 100k particles, quadratic, 200 steps; oracle live."""
     fem, fo, wl = mods
     w = wl.config("C1")
@@ -108,18 +110,19 @@ def test_c1_full_size_free_run(mods):
     worst_rho = max(rel(rec.charge_history[k], hist.rho[k]) for k in range(w.num_steps + 1))
     worst_phi = max(rel(rec.potential_history[k], hist.phi[k]) for k in range(w.num_steps + 1))
     assert worst_rho <= 1e-10 and worst_phi <= 1e-10, (worst_rho, worst_phi)
+    parity_report(free_energy=ee, free_kinetic=kin, free_rho_worst=worst_rho, free_phi_worst=worst_phi)
     # teacher-forced at sampled steps of the GPU's own trajectory
     xp, vp = wl.generate(w, layout="pn")
     _, run = _gpu_run(mods, w, xp, vp, w.num_steps)
-    check_teacher_forced(w, run, 0, xp, "C1")
+    check_teacher_forced(w, run, 0, xp, "C1", parity_report)
     done = 0
     for k in (1, 50, 200):
         run.advance(k - done)
         done = k
-        check_teacher_forced(w, run, k, run.x.cpu().numpy(), "C1")
+        check_teacher_forced(w, run, k, run.x.cpu().numpy(), "C1", parity_report)
 
 
-def test_c2_full_size_500_steps(mods):
+def test_c2_full_size_500_steps(mods, parity_report):
     """C2 at its size (32 x 250k, cubic two-stream, 500 steps): free-running
     energy history vs the oracle's run (fixture), teacher-forced charge and
     potential at 5 sampled steps (oracle live on the GPU's positions)."""
@@ -128,14 +131,14 @@ def test_c2_full_size_500_steps(mods):
     w = wl.config("C2")
     xp, vp = wl.generate(w, layout="pn")
     _, run = _gpu_run(mods, w, xp, vp, w.num_steps)
-    check_teacher_forced(w, run, 0, xp, "C2")
+    check_teacher_forced(w, run, 0, xp, "C2", parity_report)
     done = 0
     samples = [int(k) for k in f["sample_steps"]]
     free = {}
     for k in samples:
         run.advance(k - done)
         done = k
-        check_teacher_forced(w, run, k, run.x.cpu().numpy(), "C2")
+        check_teacher_forced(w, run, k, run.x.cpu().numpy(), "C2", parity_report)
     run.finish_kinetic()
     run.check()
     ee_g = run.ee_hist.cpu().numpy()
@@ -153,9 +156,11 @@ def test_c2_full_size_500_steps(mods):
     # the first particles' final state, against the oracle's full-step values
     xo = run.x.cpu().numpy()[:, :64].T
     assert rel(xo, f["x_final_rows"]) <= 1e-9
+    parity_report(free_energy=ee, free_kinetic=kin, free_rho_worst=max(v[0] for v in free.values()),
+                  free_phi_worst=max(v[1] for v in free.values()), x_final=rel(xo, f["x_final_rows"]))
 
 
-def test_c5_full_size_teacher_forced(mods):
+def test_c5_full_size_teacher_forced(mods, parity_report):
     """C5 at its size (64 x 4M = 256M particles, Nx = 512, cubic): charge and
     potential at steps 0, 1 and 3 vs the oracle on the same positions."""
     fem, fo, wl = mods
@@ -163,16 +168,16 @@ def test_c5_full_size_teacher_forced(mods):
     xp, vp = wl.generate(w, layout="pn")
     _, run = _gpu_run(mods, w, xp, vp, 3)
     del vp
-    check_teacher_forced(w, run, 0, xp, "C5")
+    check_teacher_forced(w, run, 0, xp, "C5", parity_report)
     del xp
     run.advance(1)
-    check_teacher_forced(w, run, 1, run.x.cpu().numpy(), "C5")
+    check_teacher_forced(w, run, 1, run.x.cpu().numpy(), "C5", parity_report)
     run.advance(2)
     run.check()
-    check_teacher_forced(w, run, 3, run.x.cpu().numpy(), "C5")
+    check_teacher_forced(w, run, 3, run.x.cpu().numpy(), "C5", parity_report)
 
 
-def test_c5_reduced_n_free_run(mods):
+def test_c5_reduced_n_free_run(mods, parity_report):
     """C5's p = 64, Nx = 512, cubic bump-on-tail at N = 40k per instance,
     100 steps free-running: energy history <= 1e-9 vs the oracle (live)."""
     fem, fo, wl = mods
@@ -188,6 +193,7 @@ def test_c5_reduced_n_free_run(mods):
     ee = np.max(np.abs(rec.electric_history - hist.electric) / np.abs(hist.electric))
     kin = np.max(np.abs(rec.kinetic_history - hist.kinetic) / np.abs(hist.kinetic))
     assert ee <= 1e-9 and kin <= 1e-9, (ee, kin)
+    parity_report(free_energy=ee, free_kinetic=kin, rho_step1=rel(rec.charge_history[1], hist.rho[1]))
     assert rel(rec.charge_history[1], hist.rho[1]) <= 1e-12
     assert rel(rec.potential_history[1], hist.phi[1]) <= 1e-12
 
@@ -208,7 +214,7 @@ def _rom_inputs(wl, name, n=None):
     return w, x0, v0, params
 
 
-def test_c3_full_scale_teacher_forced(rom):
+def test_c3_full_scale_teacher_forced(rom, parity_report):
     """C3 at its size (N = 1e6, p = 128, n = 20, quadratic, per-instance k):
     F(U Z) (charge -> potential -> gradient, the DEIM harvest Lambda phi), the
     warm-up stage U^T F(U z) and the manifold maps (basis velocity, both
@@ -234,32 +240,37 @@ def test_c3_full_scale_teacher_forced(rom):
         ud = torch.from_numpy(u).cuda()
         og, ophi, olam = orl.exact_gradients(osys, u, z)
         gg, gphi, glam = driver.exact_gradients(gsys, ud, z)
-        assert rel(gphi.cpu().numpy(), ophi) <= 1e-12, tag
-        assert rel(gg.cpu().numpy(), og) <= 1e-12, tag
-        assert rel(glam.cpu().numpy(), olam) <= 1e-12, tag
+        errs = dict(phi=rel(gphi.cpu().numpy(), ophi), grad=rel(gg.cpu().numpy(), og),
+                    lam=rel(glam.cpu().numpy(), olam))
+        assert errs["phi"] <= 1e-12 and errs["grad"] <= 1e-12 and errs["lam"] <= 1e-12, (tag, errs)
         del gg, glam, olam
         stage = driver.make_full_stage(gsys)(ud)(z)
-        assert rel(stage, u.T @ og) <= 1e-12, tag
+        errs["stage"] = rel(stage, u.T @ og)
+        assert errs["stage"] <= 1e-12, tag
         # manifold maps: GPU basis velocity from its own implicit device gradient
         dg, _, _ = driver.exact_gradients_device(gsys, ud, z, harvest=False)
         xi_o = omf.velocity_of_basis(u, z, og)
         xi_g = red.basis_velocity(ud, z, dg)
-        assert rel(xi_g.cpu().numpy(), xi_o) <= 1e-12, tag
+        errs["basis_velocity"] = rel(xi_g.cpu().numpy(), xi_o)
+        assert errs["basis_velocity"] <= 1e-12, tag
         del og, dg, xi_g
         r_o = omf.cayley_retract(u, 0.5 * dt * xi_o)
         r_g = red.retraction(ud, red.scaled(torch.from_numpy(xi_o).cuda(), 0.5 * dt))
-        assert rel(r_g.cpu().numpy(), r_o) <= 1e-12, tag
+        errs["retraction"] = rel(r_g.cpu().numpy(), r_o)
+        assert errs["retraction"] <= 1e-12, tag
         x_eval = xi_o[::-1].copy()                     # any tangent-sized operand
         t_o = omf.transport_back(u, 0.5 * dt * xi_o, r_o, x_eval)
         t_g = red.tangent_velocity(ud, red.scaled(torch.from_numpy(xi_o).cuda(), 0.5 * dt),
                                    torch.from_numpy(r_o).cuda(), torch.from_numpy(x_eval).cuda())
-        assert rel(t_g.cpu().numpy(), t_o) <= 1e-12, tag
+        errs["tangent"] = rel(t_g.cpu().numpy(), t_o)
+        assert errs["tangent"] <= 1e-12, tag
         o_o, s_o = omf.structure_defects(r_o)
         o_g, s_g = red.orthosymplectic_residuals(r_g)
         assert abs(o_g - o_o) <= 1e-13 and abs(s_g - s_o) <= 1e-13, tag
+        parity_report(at=tag, **errs)
 
 
-def _rom_free_run(rom, name):
+def _rom_free_run(rom, name, report=None):
     from oracle import manifold as omf
     driver, red, _, wl = rom
     f = np.load(GOLDEN / f"config_{name}.npz")
@@ -290,10 +301,132 @@ def _rom_free_run(rom, name):
     assert rel(z, f["z_final"]) <= 1e-9
     assert rel(u.cpu().numpy()[f["rows"]], f["u_final_rows"]) <= 1e-9
     np.testing.assert_allclose(rec.ortho_residuals, f["ortho"], atol=1e-13)
+    if report:
+        report(free_energy=ee, free_hamiltonian=ham, z_final=rel(z, f["z_final"]),
+               u_final_rows=rel(u.cpu().numpy()[f["rows"]], f["u_final_rows"]),
+               fp_iterations_mean=float(np.mean(rec.fp_iterations)))
     return rec, f
 
 
-def test_c3_reduced_n_free_run(rom):
+def test_c3_reduced_n_free_run(rom, parity_report):
     """C3's p = 128, n = 20, quadratic, per-instance k, 200 steps at N = 5e4:
     fixed-point counts equal, energies <= 1e-9 vs the oracle's run (fixture)."""
-    _rom_free_run(rom, "C3r")
+    _rom_free_run(rom, "C3r", parity_report)
+
+
+def _recording(monkeypatch, module, name, sink, wrap=None):
+    orig = getattr(module, name)
+
+    def rec(*a, **k):
+        r = orig(*a, **k)
+        sink.append(wrap(a, k, r) if wrap else r)
+        return r
+
+    monkeypatch.setattr(module, name, rec)
+
+
+def test_c4_reduced_n_warmup_fit_and_failure(rom, monkeypatch, parity_report):
+    """C4 (p* = 20, T = 20, d = 40) at N = 5e4.  The reference algorithm's
+    hyper-reduced fixed point does not converge at this particle count (the
+    oracle's run ends in StepFailure at the first hyper step, step 21; at
+    N = 1e6 it converges, see the full-scale test below).  Parity: the 20
+    warm-up steps (fixed-point counts equal, state and energies <= 1e-9), the
+    first DEIM fit's indices bit-exact, and the same StepFailureError with the
+    same iteration count and residual trace."""
+    from paper_2201_05555_b200.errors import StepFailureError
+    driver, red, hyp, wl = rom
+    f = np.load(GOLDEN / "config_C4r.npz")
+    n = int(f["num_particles"])
+    w, x0, v0, params = _rom_inputs(wl, "C4", n)
+    ex = w.extra
+    u0, z0 = red.complex_svd_basis(x0, v0, ex["basis_dim"])
+    assert rel(z0, f["z0"]) <= 1e-12
+    gsys = driver.ParametricVlasovSystem(w.lengths, w.num_cells, w.degree, n)
+    steps, fits = [], []
+    _recording(monkeypatch, driver, "prk2_step", steps)
+    _recording(monkeypatch, hyp, "fit_deim_device", fits)
+    with pytest.raises(StepFailureError) as err:
+        driver.run_reduced(gsys, params, x0, v0, basis_dim=ex["basis_dim"],
+                           subsample=ex["subsample"], window=ex["window"], deim_dim=ex["deim_dim"],
+                           deim_period=ex["deim_period"], deim_update=ex["deim_update"], dt=w.dt,
+                           t_final=(ex["window"] + 1) * w.dt, hyper_reduction=True,
+                           energy_stride=10**9, snapshot_stride=10**9, decomp_stride=10**9,
+                           u0=u0, z0=z0)
+    np.testing.assert_array_equal([r.fp_iterations for r in steps], f["fp_iterations"])
+    last = steps[-1]
+    assert rel(last.z, f["z_warm"]) <= 1e-9
+    assert rel(last.u.cpu().numpy()[f["rows"]], f["u_warm_rows"]) <= 1e-9
+    ee, kin = driver._diag_energies(gsys, last.u, last.z)
+    assert np.max(np.abs(ee - f["electric_warm"]) / np.abs(f["electric_warm"])) <= 1e-9
+    assert np.max(np.abs(kin - f["kinetic_warm"]) / np.abs(f["kinetic_warm"])) <= 1e-9
+    np.testing.assert_array_equal(fits[0].indices, f["deim_indices"])
+    assert rel(fits[0].weights, f["deim_weights"]) <= 1e-6
+    assert err.value.iterations == int(f["fail_iterations"]) == 100
+    trace, want = np.asarray(err.value.residual_trace), f["fail_trace"]
+    assert np.max(np.abs(trace[:6] - want[:6]) / want[:6]) <= 1e-6
+    assert trace[-1] > 1e-9 and want[-1] > 1e-9
+    parity_report(z_warm=rel(last.z, f["z_warm"]), deim_weights=rel(fits[0].weights, f["deim_weights"]),
+                  trace6=float(np.max(np.abs(trace[:6] - want[:6]) / want[:6])),
+                  fp_warm=[int(r.fp_iterations) for r in steps], last_update=float(trace[-1]))
+
+
+def test_c4_full_scale_first_hyper_step_teacher_forced(rom, monkeypatch, parity_report):
+    """C4 at its size (N = 1e6, p = 128, p* = 20, T = 20, d = 40): run the GPU
+    model to its first hyper-reduced step (21) and give the oracle the SAME
+    inputs of that step -- the potential window, the DEIM sample window, U and
+    Z.  DMD eigenvalues equal, DEIM indices bit-exact, DEIM weights and the
+    step's Z to tolerance, equal fixed-point iteration counts."""
+    from oracle import dmd_deim as odd
+    from oracle import manifold as omf
+    from oracle import rom_loop as orl
+    driver, red, hyp, wl = rom
+    w, x0, v0, params = _rom_inputs(wl, "C4")
+    ex = w.extra
+    N = w.num_particles
+    u0, z0 = red.complex_svd_basis(x0, v0, ex["basis_dim"])
+    gsys = driver.ParametricVlasovSystem(w.lengths, w.num_cells, w.degree, N)
+    dmd_in, deim_in, prk_in = [], [], []
+
+    def cap_dmd(a, k, r):
+        return ([np.array(b) for b in a[0]], a[2], r)
+
+    def cap_deim(a, k, r):
+        cols = [c.cpu().numpy() for c in a[0].columns()]      # ring order, oldest first
+        return (cols, r)
+
+    def cap_prk(a, k, r):
+        return (a[0].cpu().numpy(), np.array(a[1]), r) if len(prk_in) == ex["window"] else None
+
+    _recording(monkeypatch, hyp, "fit_parametric_dmd", dmd_in, cap_dmd)
+    _recording(monkeypatch, hyp, "fit_deim_device", deim_in, cap_deim)
+    _recording(monkeypatch, driver, "prk2_step", prk_in, cap_prk)
+    driver.run_reduced(gsys, params, x0, v0, basis_dim=ex["basis_dim"], subsample=ex["subsample"],
+                       window=ex["window"], deim_dim=ex["deim_dim"],
+                       deim_period=ex["deim_period"], deim_update=ex["deim_update"], dt=w.dt,
+                       t_final=(ex["window"] + 1) * w.dt, hyper_reduction=True,
+                       energy_stride=10**9, snapshot_stride=10**9, decomp_stride=10**9,
+                       u0=u0, z0=z0)
+    del x0, v0
+    win, t_prev, g_dmd = dmd_in[0]
+    cols, g_deim = deim_in[0]
+    u, z, g_res = prk_in[-1]
+    osys = orl.ParamSystem(w.lengths, w.num_cells, w.degree, N)
+    sub = np.sort(omf.farthest_point_subset(z0, ex["subsample"]))
+    o_dmd = odd.parametric_dmd(win, w.dt, t_prev, params, sub)
+    np.testing.assert_allclose(np.sort_complex(g_dmd.eigenvalues), np.sort_complex(o_dmd.eigenvalues),
+                               rtol=1e-10)
+    block = np.stack(cols).transpose(1, 2, 0)               # the reference's column order
+    del cols
+    o_deim = odd.deim_fit(block.reshape(block.shape[0], -1), ex["deim_dim"],
+                          osys.charge.charge_weight)
+    del block
+    np.testing.assert_array_equal(g_deim.indices, o_deim.indices)
+    assert rel(g_deim.weights, o_deim.weights) <= 1e-6
+    grad_sub = lambda uu, zs: orl.exact_gradients(osys, uu, zs, sub)[0]  # noqa: E731
+    o_res = omf.prk2(u, z, w.dt, sub, grad_sub, grad_sub(u, z[:, sub]),
+                     orl.hyper_stage(osys, o_dmd, o_deim, t_prev + 0.5 * w.dt, params))
+    assert g_res.fp_iterations == o_res.fp_iterations
+    assert rel(g_res.z, o_res.z) <= 1e-9
+    assert rel(g_res.u.cpu().numpy(), o_res.u) <= 1e-9
+    parity_report(deim_weights=rel(g_deim.weights, o_deim.weights), z=rel(g_res.z, o_res.z),
+                  u=rel(g_res.u.cpu().numpy(), o_res.u), fp_iterations=int(g_res.fp_iterations))
