@@ -360,7 +360,7 @@ def test_c4_reduced_n_warmup_fit_and_failure(rom, monkeypatch, parity_report):
     assert np.max(np.abs(ee - f["electric_warm"]) / np.abs(f["electric_warm"])) <= 1e-9
     assert np.max(np.abs(kin - f["kinetic_warm"]) / np.abs(f["kinetic_warm"])) <= 1e-9
     np.testing.assert_array_equal(fits[0].indices, f["deim_indices"])
-    assert rel(fits[0].weights, f["deim_weights"]) <= 1e-6
+    assert rel(fits[0].weights, f["deim_weights"]) <= 1e-10
     assert err.value.iterations == int(f["fail_iterations"]) == 100
     trace, want = np.asarray(err.value.residual_trace), f["fail_trace"]
     assert np.max(np.abs(trace[:6] - want[:6]) / want[:6]) <= 1e-6
@@ -421,7 +421,7 @@ def test_c4_full_scale_first_hyper_step_teacher_forced(rom, monkeypatch, parity_
                           osys.charge.charge_weight)
     del block
     np.testing.assert_array_equal(g_deim.indices, o_deim.indices)
-    assert rel(g_deim.weights, o_deim.weights) <= 1e-6
+    assert rel(g_deim.weights, o_deim.weights) <= 1e-10
     grad_sub = lambda uu, zs: orl.exact_gradients(osys, uu, zs, sub)[0]  # noqa: E731
     o_res = omf.prk2(u, z, w.dt, sub, grad_sub, grad_sub(u, z[:, sub]),
                      orl.hyper_stage(osys, o_dmd, o_deim, t_prev + 0.5 * w.dt, params))
