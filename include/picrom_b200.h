@@ -261,6 +261,19 @@ int picrom_argmax_abs(const double* v, long long n, long long stride,
                       const long long* banned, int nbanned, long long* out_index,
                       double* out_value, void* workspace, void* stream);
 
+/* Scratch bytes of picrom_deim_greedy for an N x d basis. */
+size_t picrom_deim_workspace_bytes(long long N, int d);
+
+/* deim_greedy (hyper.py:218-246) fully on the device: psi (N x d, row stride
+ * ld >= d), keep (HOST array of d entries; entry k >= 0 pre-assigns position
+ * k -- the partial refresh of fit_deim, hyper.py:268-275 -- or NULL) ->
+ * idx (device, d int64) and rows (device, d x d: rows[k] = psi[idx[k], :]).
+ * Position k's index is the first max of |psi_k - Psi_{<k} c| with
+ * R[:k, :k] c = R[:k, k] and the indices already assigned scored -1; no host
+ * round trip between positions. d <= 64. */
+int picrom_deim_greedy(const double* psi, int ld, long long N, int d, const long long* keep,
+                       long long* idx, double* rows, void* workspace, void* stream);
+
 /* out (N x c, row stride ldo) (+)= sum_t op_t(in_t) (N x widths[t]) @ M_t,
  * op_t = J when jswap[t] (nullable), M_t (widths[t] x c) at mats + moffs[t]
  * (device); c <= 32, at most 6 terms. */

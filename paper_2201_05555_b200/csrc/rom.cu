@@ -20,6 +20,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <vector>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -1914,6 +1915,231 @@ extern "C" int picrom_argmax_abs(const double* v, long long n, long long stride,
   if (rc) return rc;
   argmax_final_kernel<<<1, 32, 0, s>>>(pv, pi, G, out_index, out_value);
   return picrom_check_launch("argmax_final");
+}
+
+// ------------------------------------------------------------ DEIM greedy
+//
+// deim_greedy (hyper.py:218-246) as one device-resident sequence: psi (N x d,
+// row-major) is copied once to column-major psiT (d x N) so every residual
+// pass reads coalesced columns; per selected position k
+//   1. deim_resid_kernel: r_i = psi_k[i] - sum_{j<k} psi_j[i] c_j, scored
+//      |r_i| (banned indices -1), per-block first-max partials;
+//   2. deim_pick_kernel (one CTA): final first-max -> I[k], R[k][:] =
+//      psi[I[k], :], banned += I[k]; then c for the next position k' from
+//      R[:k', :k'] c = R[:k', k'] (Gaussian elimination, partial pivoting) --
+//      the coefficient solve of hyper.py:239.
+// No host round trip between positions; kept positions (partial refresh,
+// hyper.py:268-275) are pre-assigned and banned from the start.
+
+constexpr int kDeimMaxD = 64;
+constexpr int kDeimThreads = 256;
+
+__global__ void deim_transpose_kernel(const double* psi, int ld, long long N, int d,
+                                      double* psiT) {
+  __shared__ double tile[32][33];
+  const long long r0 = (long long)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int q = threadIdx.y; q < 32; q += blockDim.y) {
+    const long long r = r0 + q;
+    const int c = c0 + threadIdx.x;
+    tile[q][threadIdx.x] = (r < N && c < d) ? psi[(size_t)r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int q = threadIdx.y; q < 32; q += blockDim.y) {
+    const int c = c0 + q;
+    const long long r = r0 + threadIdx.x;
+    if (c < d && r < N) psiT[(size_t)c * N + r] = tile[threadIdx.x][q];
+  }
+}
+
+__global__ void __launch_bounds__(kDeimThreads)
+deim_resid_kernel(const double* psiT, long long N, int k, const double* coef,
+                  const long long* banned, int nbanned, double* pv, long long* pi) {
+  __shared__ double sc[kDeimMaxD];
+  __shared__ long long sb[kDeimMaxD];
+  __shared__ double sv[kDeimThreads];
+  __shared__ long long si[kDeimThreads];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) sc[j] = coef[j];
+  for (int j = threadIdx.x; j < nbanned; j += blockDim.x) sb[j] = banned[j];
+  __syncthreads();
+  double bv = -2.0;
+  long long bi = 0x7fffffffffffffffLL;
+  const double* col_k = psiT + (size_t)k * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < k; ++j) acc = fma(psiT[(size_t)j * N + i], sc[j], acc);
+    const double r = col_k[i] - acc;
+    bool ban = false;
+    for (int q = 0; q < nbanned; ++q) ban |= sb[q] == i;
+    better(ban ? -1.0 : fabs(r), i, bv, bi);
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      double cv = sv[threadIdx.x];
+      long long ci = si[threadIdx.x];
+      better(sv[threadIdx.x + o], si[threadIdx.x + o], cv, ci);
+      sv[threadIdx.x] = cv;
+      si[threadIdx.x] = ci;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pv[blockIdx.x] = sv[0];
+    pi[blockIdx.x] = si[0];
+  }
+}
+
+// rows[k][:] = psi[idx[k], :] for the pre-assigned (kept) positions
+__global__ void deim_keep_rows_kernel(const double* psiT, long long N, int d, const long long* idx,
+                                      double* rows) {
+  const int k = blockIdx.x;
+  const long long i = idx[k];
+  if (i < 0) return;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) rows[(size_t)k * d + j] = psiT[(size_t)j * N + i];
+}
+
+// One CTA: finish position k (k < 0: nothing to finish), prepare position kn
+// (kn < 0: done).  m holds c (kn entries) for the next residual pass.
+__global__ void __launch_bounds__(kDeimThreads)
+deim_pick_kernel(const double* pv, const long long* pi, int nparts, const double* psiT, long long N,
+                 int d, int k, int kn, long long* idx, double* rows, long long* banned, int nb,
+                 double* coef) {
+  __shared__ double sv[kDeimThreads];
+  __shared__ long long si[kDeimThreads];
+  __shared__ double a[kDeimMaxD][kDeimMaxD + 1];
+  __shared__ int s_piv;
+  const int tid = threadIdx.x;
+  if (k >= 0) {
+    double bv = -2.0;
+    long long bi = 0x7fffffffffffffffLL;
+    for (int q = tid; q < nparts; q += blockDim.x) better(pv[q], pi[q], bv, bi);
+    sv[tid] = bv;
+    si[tid] = bi;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (tid < o) {
+        double cv = sv[tid];
+        long long ci = si[tid];
+        better(sv[tid + o], si[tid + o], cv, ci);
+        sv[tid] = cv;
+        si[tid] = ci;
+      }
+      __syncthreads();
+    }
+    const long long pick = si[0];
+    if (tid == 0) {
+      idx[k] = pick;
+      banned[nb] = pick;
+    }
+    for (int j = tid; j < d; j += blockDim.x) rows[(size_t)k * d + j] = psiT[(size_t)j * N + pick];
+    __syncthreads();
+    __threadfence_block();
+  }
+  if (kn <= 0) return;
+  // augmented system [R[:kn, :kn] | R[:kn, kn]], row r = position r
+  const int m = kn;
+  for (int q = tid; q < m * (m + 1); q += blockDim.x) {
+    const int r = q / (m + 1), c = q % (m + 1);
+    a[r][c] = rows[(size_t)r * d + (c < m ? c : kn)];
+  }
+  __syncthreads();
+  for (int col = 0; col < m; ++col) {
+    if (tid == 0) {             // partial pivoting, first max (LAPACK idamax)
+      int piv = col;
+      double best = fabs(a[col][col]);
+      for (int r = col + 1; r < m; ++r)
+        if (fabs(a[r][col]) > best) { best = fabs(a[r][col]); piv = r; }
+      s_piv = piv;
+    }
+    __syncthreads();
+    const int piv = s_piv;
+    if (piv != col)
+      for (int c = tid; c <= m; c += blockDim.x) {
+        const double t = a[col][c];
+        a[col][c] = a[piv][c];
+        a[piv][c] = t;
+      }
+    __syncthreads();
+    const double inv = 1.0 / a[col][col];
+    for (int q = tid; q < (m - col - 1) * (m - col); q += blockDim.x) {
+      const int r = col + 1 + q / (m - col), c = col + 1 + q % (m - col);
+      a[r][c] = fma(-(a[r][col] * inv), a[col][c], a[r][c]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {               // back substitution (serial: m <= 64)
+    for (int r = m - 1; r >= 0; --r) {
+      double t = a[r][m];
+      for (int c = r + 1; c < m; ++c) t = fma(-a[r][c], a[c][m], t);
+      a[r][m] = t / a[r][r];
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < m; r += blockDim.x) coef[r] = a[r][m];
+}
+
+extern "C" size_t picrom_deim_workspace_bytes(long long N, int d) {
+  const int G = (int)std::min<long long>(4LL * picrom_num_sms(), (N + 255) / 256);
+  return (size_t)d * N * sizeof(double) + (size_t)G * (sizeof(double) + sizeof(long long)) +
+         (size_t)(3 * kDeimMaxD) * sizeof(double) + 256;
+}
+
+extern "C" int picrom_deim_greedy(const double* psi, int ld, long long N, int d,
+                                  const long long* keep, long long* idx, double* rows, void* ws,
+                                  void* stream) {
+  if (N < 1 || d < 1 || d > kDeimMaxD || ld < d)
+    return picrom_set_error(PICROM_ERR_CONFIG, "deim_greedy: need N >= 1, 1 <= d <= 64, ld >= d");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int G = (int)std::min<long long>(4LL * picrom_num_sms(), (N + 255) / 256);
+  double* psiT = (double*)ws;
+  double* pv = psiT + (size_t)d * N;
+  long long* pi = (long long*)(pv + G);
+  double* coef = (double*)(pi + G);
+  long long* banned = (long long*)(coef + kDeimMaxD);
+  // keep: host array of d entries (index >= 0: pre-assigned position)
+  int nb = 0;
+  std::vector<int> order;
+  std::vector<long long> kept;
+  for (int k = 0; k < d; ++k) {
+    if (keep && keep[k] >= 0) kept.push_back(keep[k]);
+    else order.push_back(k);
+  }
+  std::vector<long long> idx_init(d, -1);
+  for (int k = 0; k < d; ++k) if (keep && keep[k] >= 0) idx_init[k] = keep[k];
+  cudaMemcpyAsync(idx, idx_init.data(), d * sizeof(long long), cudaMemcpyHostToDevice, s);
+  if (!kept.empty())
+    cudaMemcpyAsync(banned, kept.data(), kept.size() * sizeof(long long), cudaMemcpyHostToDevice, s);
+  nb = (int)kept.size();
+  dim3 tg((unsigned)((N + 31) / 32), (unsigned)((d + 31) / 32));
+  deim_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(psi, ld, N, d, psiT);
+  int rc = picrom_check_launch("deim_transpose");
+  if (rc) return rc;
+  if (!kept.empty()) {
+    deim_keep_rows_kernel<<<d, 64, 0, s>>>(psiT, N, d, idx, rows);
+    if ((rc = picrom_check_launch("deim_keep_rows"))) return rc;
+  }
+  // coefficients of the first position
+  const int k0 = order.empty() ? -1 : order[0];
+  if (k0 > 0) {
+    deim_pick_kernel<<<1, kDeimThreads, 0, s>>>(pv, pi, G, psiT, N, d, -1, k0, idx, rows, banned,
+                                                nb, coef);
+    if ((rc = picrom_check_launch("deim_pick"))) return rc;
+  }
+  for (size_t q = 0; q < order.size(); ++q) {
+    const int k = order[q];
+    const int kn = q + 1 < order.size() ? order[q + 1] : -1;
+    deim_resid_kernel<<<G, kDeimThreads, 0, s>>>(psiT, N, k, coef, banned, nb, pv, pi);
+    if ((rc = picrom_check_launch("deim_resid"))) return rc;
+    deim_pick_kernel<<<1, kDeimThreads, 0, s>>>(pv, pi, G, psiT, N, d, k, kn, idx, rows, banned,
+                                                nb, coef);
+    if ((rc = picrom_check_launch("deim_pick"))) return rc;
+    ++nb;
+  }
+  return PICROM_OK;
 }
 
 // out (N x c) (+)= sum_t in_t (N x a_t) @ M_t (a_t x c); mats is a device buffer

@@ -373,7 +373,10 @@ def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_d
                     system, u, z[:, sub], subcols, harvest=hyper_reduction)
             pot_window.append(phi_sub.t().cpu().numpy())
             if hyper_reduction:
-                deim_window.append(lam_sub)
+                # the window's incremental Gram (new block x window) is the
+                # DEIM fit's SVD work: timed with it
+                with timers.phase("deim_fit"):
+                    deim_window.append(lam_sub)
             hyper_now = hyper_reduction and len(pot_window) == window + 1
             if hyper_now:
                 hyper_engaged = True

@@ -9,11 +9,12 @@ Split by size:
   the RBF system over p* parameter nodes, DEIM weight solve d x d) is tiny and
   stays in host LAPACK, as in the reference;
 * everything that scales with the particle count N runs on the device:
-  the DEIM window Gram (sliding, picrom_cross_gram), the basis
-  Psi = W V Sigma^-1 (picrom_combine), the greedy residuals + argmax
-  (picrom_combine, picrom_argmax_abs), U_X[I] (picrom_rows_gather), and per
-  stage the DMD extrapolation (picrom_dmd_extrapolate) and the DEIM-sampled
-  gather + projection (picrom_deim_gather).
+  the DEIM window Gram (sliding, one new block x window per step), the
+  window SVD (Gram eigenvectors refined by subspace iteration: plain tall
+  GEMMs), the whole greedy index selection (picrom_deim_greedy, one device
+  sequence, no host round trip per index), U_X[I] (picrom_rows_gather), and
+  per stage the DMD extrapolation (picrom_dmd_extrapolate) and the
+  DEIM-sampled gather + projection (picrom_deim_gather).
 
 The DEIM SVD is computed from the window Gram (eigen-decomposition on the
 host) followed by one Rayleigh-Ritz refinement on the device; its accuracy
@@ -279,69 +280,41 @@ class DeimWindow:
         return self.mat[:, :c], self.G[:c, :c]
 
 
+def _greedy_device(psi, keep=None):
+    """picrom_deim_greedy: (indices (d,) int64 device, rows (d x d) device)."""
+    n, d = psi.shape
+    if psi.stride(1) != 1:
+        psi = psi.contiguous()
+    need = int(_lib.query("picrom_deim_workspace_bytes", int(n), int(d)))
+    key = torch.cuda.current_device()
+    ws = _GREEDY_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = _GREEDY_WS[key] = torch.empty(need, dtype=torch.uint8, device="cuda")
+    keep_arr = None
+    if keep:
+        keep_arr = np.full(d, -1, dtype=np.int64)
+        for k, i in keep.items():
+            keep_arr[int(k)] = int(i)
+    idx = torch.empty(d, dtype=torch.int64, device="cuda")
+    rows = torch.empty((d, d), dtype=torch.float64, device="cuda")
+    _lib.call("picrom_deim_greedy", psi.data_ptr(), int(psi.stride(0)), int(n), int(d),
+              None if keep_arr is None else keep_arr.ctypes.data_as(C.c_void_p), idx.data_ptr(),
+              rows.data_ptr(), ws.data_ptr(), dev.stream_handle())
+    return idx, rows
+
+
+_GREEDY_WS = {}
+
+
 def deim_greedy(psi, keep=None):
-    """Greedy interpolation indices (hyper.py:218-246) on a device basis psi (N x d):
-    residual psi_k - Psi_<k (Psi[I,<k])^-1 psi_k[I] (one tall GEMV), argmax by
-    picrom_argmax_abs with the assigned indices banned (first-max tie rule).
-    The banned list lives on the device and the chosen row of psi comes back
-    with the index: one host round trip per index."""
+    """Greedy interpolation indices (hyper.py:218-246) on a device basis psi
+    (N x d): all d positions in one device sequence (picrom_deim_greedy) --
+    residual psi_k - Psi_<k (Psi[I,<k])^-1 psi_k[I], first max of |.| with
+    the assigned indices banned -- and one transfer of the indices back."""
     if not isinstance(psi, torch.Tensor):
         psi = torch.from_numpy(np.ascontiguousarray(psi, dtype=np.float64)).to("cuda")
-    n, d = psi.shape
-    keep = keep or {}
-    indices = np.empty(d, dtype=np.int64)
-    rows = np.empty((d, d))                    # psi[indices[k], :] as they are chosen
-    banned = torch.empty(d, dtype=torch.int64, device="cuda")
-    nb = 0
-    if keep:
-        kept = np.array(sorted(keep.items()), dtype=np.int64)
-        banned[:len(kept)] = torch.from_numpy(kept[:, 1].copy()).to("cuda")
-        nb = len(kept)
-        kept_rows = _rows(psi, kept[:, 1])
-        for (k, idx), r in zip(kept, kept_rows):
-            indices[k] = idx
-            rows[k] = r
-    key = torch.cuda.current_device()
-    ws = _ARGMAX_WS.get(key)
-    if ws is None:
-        ws = _ARGMAX_WS[key] = torch.empty(1 << 16, dtype=torch.float64, device="cuda")
-    out_i = torch.empty(1, dtype=torch.int64, device="cuda")
-    for k in range(d):
-        if k in keep:
-            continue
-        if k == 0:
-            res = psi[:, 0]
-        else:
-            sub = rows[:k]
-            coeff = np.linalg.solve(sub[:, :k], sub[:, k])
-            m = np.concatenate([-coeff, [1.0]])
-            res = psi[:, :k + 1] @ torch.from_numpy(m).to("cuda")
-        _lib.call("picrom_argmax_abs", res.data_ptr(), n, int(res.stride(0)), banned.data_ptr(),
-                  nb, out_i.data_ptr(), None, ws.data_ptr(), dev.stream_handle())
-        banned[nb:nb + 1].copy_(out_i)
-        nb += 1
-        pick_row = torch.cat([out_i.to(torch.float64), psi.index_select(0, out_i)[0]])
-        host = pick_row.cpu().numpy()
-        indices[k] = int(host[0])
-        rows[k] = host[1:]
-    return indices
-
-
-_ARGMAX_WS = {}
-
-
-def _argmax_abs(v, banned):
-    n = v.shape[0]
-    key = torch.cuda.current_device()
-    ws = _ARGMAX_WS.get(key)
-    if ws is None:
-        ws = _ARGMAX_WS[key] = torch.empty(1 << 16, dtype=torch.float64, device="cuda")
-    out_i = torch.empty(1, dtype=torch.int64, device="cuda")
-    b = (torch.as_tensor(np.asarray(banned, dtype=np.int64)).to("cuda") if len(banned)
-         else None)
-    _lib.call("picrom_argmax_abs", v.data_ptr(), n, int(v.stride(0)), dev.ptr(b), len(banned),
-              out_i.data_ptr(), None, ws.data_ptr(), dev.stream_handle())
-    return int(out_i.item())
+    idx, _ = _greedy_device(psi, keep)
+    return idx.cpu().numpy()
 
 
 def _rows(psi, idx):
@@ -353,12 +326,19 @@ def _rows(psi, idx):
     return out.cpu().numpy()
 
 
-def _orthonormalize(y):
-    """CholeskyQR2 of a tall device block (N x k): Q with Q^T Q = I to O(eps)."""
+def _orthonormalize(y, kappa_one=16.0):
+    """Cholesky QR of a tall device block (N x k): Q with Q^T Q = I to O(eps).
+    CholQR's orthogonality error is ~eps kappa(Y)^2, so a second round (CholQR2)
+    runs only when the first factor is not well conditioned -- the balanced
+    blocks of _window_svd (columns pre-scaled by the inverse singular values)
+    need one round, an arbitrary block two."""
     for _ in range(2):
         g = _tsq(y, y)
         r = np.linalg.cholesky(g).T
         y = y @ torch.from_numpy(np.linalg.inv(r)).to("cuda")
+        sv = np.linalg.svd(r, compute_uv=False)
+        if sv[0] <= kappa_one * sv[-1]:
+            break
     return y
 
 
@@ -367,8 +347,9 @@ def _window_svd(window, dim, oversample=8, iterations=2):
     more than an N x (d+q) block (the products are plain DGEMMs on the
     contiguous window):
       1. W^T W (sliding Gram) -> eigenpairs -> initial basis Y = W V_{d+q};
-      2. `iterations` subspace-iteration steps Y <- W (W^T Q), Q = CholQR2(Y),
-         which removes the squared-condition error of step 1;
+      2. `iterations` subspace-iteration steps Y <- W (W^T Q) Sigma^-2, Q =
+         CholQR(Y) (a second round only if Y is not balanced), which removes
+         the squared-condition error of step 1;
       3. Rayleigh-Ritz: SVD of the small Q^T W, Psi = Q U_B[:, :d].
     The rank test is the reference's (hyper.py:263) on the Gram singular values."""
     W, gram = window.matrix()
@@ -388,7 +369,9 @@ def _window_svd(window, dim, oversample=8, iterations=2):
     k = min(c, rank, d_eff + oversample, 64)
     q = _orthonormalize(W @ torch.from_numpy(vec[:, :k] / sing[:k]).to("cuda"))
     for _ in range(iterations):
-        q = _orthonormalize(W @ torch.from_numpy(_tsq(W, q)).to("cuda"))
+        # W W^T Q ~ Q Sigma^2: dividing column j by sigma_j^2 keeps the block
+        # balanced (kappa ~ 1), so one Cholesky QR round suffices
+        q = _orthonormalize(W @ torch.from_numpy(_tsq(W, q) / lam[:k]).to("cuda"))
     qtw = _tsq(W, q).T
     ub, _, _ = svd(qtw, full_matrices=False)
     psi = q @ torch.from_numpy(np.ascontiguousarray(ub[:, :d_eff])).to("cuda")
@@ -409,10 +392,12 @@ def fit_deim_device(window, dim, charge, prev=None, full=True, n_update=None,
         order = np.argsort(align)
         refresh = {int(i) for i in (order[::-1] if printed_ranking else order)[:n_update]}
         keep = {k: int(prev.indices[k]) for k in range(d_eff) if k not in refresh}
-    indices = deim_greedy(psi, keep=keep)
+    idx_d, rows_d = _greedy_device(psi, keep)
     ones = torch.ones((psi.shape[0], 1), dtype=torch.float64, device="cuda")
-    colsum = _tall.gram([(psi, False), (ones, False)])[:d_eff, d_eff]
-    weights = np.linalg.solve(_rows(psi, indices).T, charge.charge_weight * colsum)
+    colsum = _tall.gram([(psi, False), (ones, False)])[:d_eff, d_eff]     # one sync
+    indices = idx_d.cpu().numpy()
+    # weights = solve(Psi[I]^T, qw Psi^T 1) (hyper.py:276), Psi[I] from the greedy
+    weights = np.linalg.solve(rows_d.cpu().numpy().T, charge.charge_weight * colsum)
     return DEIMModel(psi=psi, indices=indices, weights=weights)
 
 

@@ -55,7 +55,7 @@ def wrap(name):
     setattr(hyper, name, w)
 
 
-for nm in ("_argmax_abs", "_rows", "_orthonormalize", "_tsq"):
+for nm in ("_greedy_device", "_rows", "_orthonormalize", "_tsq"):
     wrap(nm)
 _gram0 = hyper._tall.gram
 
