@@ -142,7 +142,13 @@ int picrom_pic_step(double* x, double* v, long long n, int p, long long ld,
                     double dt, double kick, double kfull, long long step,
                     long long* counter, long long hist_rows, int hist_p,
                     double* rho_hist, double* phi_hist, double* ee_hist, double* kin_hist,
-                    void* workspace, unsigned long long* status, void* stream);
+                    unsigned long long* t_hist, void* workspace,
+                    unsigned long long* status, void* stream);
+
+/* %globaltimer (ns) into *out when the stream reaches this point (per-step
+ * timing of a replayed step graph: picrom_pic_step's t_hist, nullable, gets
+ * the time its counter advanced, i.e. the end of the step's last solve). */
+int picrom_timestamp(unsigned long long* out, void* stream);
 
 /* The two halves of picrom_pic_step, for callers that time or schedule them
  * separately: the fused particle pass (writes the deposit segments and the

@@ -120,6 +120,30 @@ def hyper_stage(system, dmd, deim, t_stage, params):
     return factory
 
 
+def hyper_energy(system, dmd, deim, u, z, t, params):
+    """hyper_hamiltonian (hyper.py:280-296) with per-column mesh / mass and the
+    hyper stage's per-column weight rescaling."""
+    if system.single:
+        mesh, charge, _ = system.column(0)
+        dmd.ensure_coords(params)
+        return dd.hyper_energy(dmd, deim, u, z, t, mesh, charge.particle_mass)
+    half = u.shape[0] // 2
+    ux_d = u[deim.indices, :]
+    uv = u[half:]
+    kin = 0.5 * np.einsum("ij,ij->j", z, (uv.T @ uv) @ z)
+    dmd.ensure_coords(params)
+    phi = dmd.potential(t)
+    xd = ux_d @ z
+    qw_ref = system.charge.charge_weight
+    fld = np.empty(z.shape[1])
+    for j in range(z.shape[1]):
+        mesh, charge, _ = system.column(j)
+        lam = fe.eval_basis(mesh, xd[:, j]).matvec(phi[:, j])
+        w = deim.weights * (charge.charge_weight / qw_ref)
+        fld[j] = (0.5 / charge.particle_mass) * (w @ lam)
+    return kin + fld
+
+
 @dataclass
 class RomHistory:
     u: np.ndarray
@@ -136,6 +160,10 @@ class RomHistory:
     sub: np.ndarray = None
     bases: list = field(default_factory=list)
     hyper_engaged: bool = False
+    decomp_times: list = field(default_factory=list)
+    dh_total: list = field(default_factory=list)
+    dh_coeff: list = field(default_factory=list)
+    dh_coeff_dd: list = field(default_factory=list)
 
 
 def _energies(system, u, z):
@@ -156,9 +184,10 @@ def _energies(system, u, z):
 
 def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_dim, deim_period,
                 deim_update, dt, num_steps, svd_tol_dmd=1e-5, fp_tol=1e-9, fp_max_iter=100,
-                hyper_reduction=True, energy_stride=10, snapshot_stride=None, u0=None, z0=None):
-    """Algorithm-2 loop (driver.py:117-274) without the off-path Hamiltonian
-    decomposition diagnostics."""
+                hyper_reduction=True, energy_stride=10, snapshot_stride=None, u0=None, z0=None,
+                decomp_stride=None):
+    """Algorithm-2 loop (driver.py:117-274); the Hamiltonian-error
+    decomposition (driver.py:229-246) at `decomp_stride` when given."""
     params = np.asarray(params, dtype=float)
     snap = max(1, int(snapshot_stride)) if snapshot_stride else max(1, num_steps // 40)
     if u0 is None:
@@ -209,7 +238,20 @@ def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_di
         else:
             stage = fstage
         res = mf.prk2(u, z, dt, sub, grad_sub, g0, stage, fp_tol=fp_tol, fp_max_iter=fp_max_iter)
+        u_prev, z_prev = u, z
         u, z = res.u, res.z
+        if hyper_now and decomp_stride and tau % decomp_stride == 0:
+            def ham(uu, zz):
+                ee, kin = _energies(system, uu, zz)
+                return kin + ee
+            h_new, h_prev = ham(u, z), ham(u_prev, z_prev)
+            hm_new, hm_prev = ham(res.u_mid, z), ham(res.u_mid, z_prev)
+            hd_new = hyper_energy(system, dmd, deim, res.u_mid, z, tau * dt, params)
+            hd_prev = hyper_energy(system, dmd, deim, res.u_mid, z_prev, t_prev, params)
+            hist.decomp_times.append(tau * dt)
+            hist.dh_total.append(float(np.linalg.norm(np.atleast_1d(h_new - h_prev))))
+            hist.dh_coeff.append(float(np.linalg.norm(np.atleast_1d(hm_new - hm_prev))))
+            hist.dh_coeff_dd.append(float(np.linalg.norm(np.atleast_1d(hd_new - hd_prev))))
         o, s = mf.structure_defects(u)
         hist.ortho.append(o)
         hist.sympl.append(s)

@@ -31,7 +31,9 @@ SIGNATURES = {
     "picrom_field_energy": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "picrom_gather": (_i, [_vp, _ll, _i, _ll, _vp, _i, _i, _vp, _i, _vp, _ll, _vp, _vp]),
     "picrom_pic_step": (_i, [_vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _vp, _vp,
-                             _d, _d, _d, _ll, _vp, _ll, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+                             _d, _d, _d, _ll, _vp, _ll, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                             _vp]),
+    "picrom_timestamp": (_i, [_vp, _vp]),
     "picrom_pic_push": (_i, [_vp, _vp, _ll, _i, _ll, _vp, _i, _i, _vp, _d, _d, _d, _ll, _vp,
                              _vp, _vp, _vp]),
     "picrom_pic_solve": (_i, [_ll, _i, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _ll, _vp, _vp, _vp,

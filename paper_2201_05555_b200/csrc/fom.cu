@@ -36,6 +36,17 @@ static int check_launch(const char* what) {
 
 extern "C" const char* picrom_last_error(void) { return g_err; }
 
+__global__ void timestamp_kernel(unsigned long long* out) {
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+  *out = now;
+}
+
+extern "C" int picrom_timestamp(unsigned long long* out, void* stream) {
+  timestamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(out);
+  return check_launch("timestamp");
+}
+
 // internal (C++ linkage) helpers shared with rom.cu
 int picrom_set_error(int code, const char* msg) { return set_err(code, msg); }
 int picrom_check_launch(const char* what) { return check_launch(what); }
@@ -290,6 +301,8 @@ struct SolveArgs {
   long long hist_mod;       // > 0: history row = counter % hist_mod (ring)
   const int* cols;          // optional instance id per column
   size_t scratch;           // solve_kernel: dynamic smem in doubles
+  unsigned long long* t_hist;  // optional %globaltimer (ns) per history row, written
+                               // when the counter advances (the step's last solve)
 };
 
 // sum of cnt values v[0], v[stride], ... with 8 independent loads in flight,
@@ -538,6 +551,11 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
         *a.done = 0u;
         __threadfence();
         *a.counter = crow + 1;
+        if (a.t_hist) {
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+          a.t_hist[row] = now;
+        }
       }
     }
   }
@@ -1336,7 +1354,8 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
                                const double* stencil, double* phi, double dt, double kick,
                                double kfull, long long step, long long* counter,
                                long long hist_rows, int hist_p, double* rho_hist,
-                               double* phi_hist, double* ee_hist, double* kin_hist, void* ws,
+                               double* phi_hist, double* ee_hist, double* kin_hist,
+                               unsigned long long* t_hist, void* ws,
                                unsigned long long* status, void* stream) {
   int rc = check_cfg(n, p, nx, degree);
   if (rc) return rc;
@@ -1362,6 +1381,7 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
     sa.done = reinterpret_cast<unsigned int*>(counter + 1);
     sa.hist_mod = hist_rows;
     sa.rho_out = rho_hist; sa.phi_hist = phi_hist; sa.energy_out = ee_hist; sa.kin_out = kin_hist;
+    sa.t_hist = t_hist;
   } else {
     sa.rho_out = rho_hist ? rho_hist + (size_t)step * gp : nullptr;
     sa.phi_hist = phi_hist ? phi_hist + (size_t)step * gp : nullptr;

@@ -254,23 +254,31 @@ def make_full_stage(system):
 
 @dataclass
 class RomRecord:
-    """Time series of a reduced run (driver.py:92-114, diagnostics subset)."""
+    """Time series and reduced snapshots of a reduced run (driver.py:92-114):
+    every field of the reference record, plus the DEIM indices of each hyper
+    step and per-step wall seconds."""
 
     times: np.ndarray
     energy_times: np.ndarray
-    electric_energy: np.ndarray
+    electric_energy: np.ndarray       # (T_e, p), from reconstructed states
     hamiltonian: np.ndarray
     snapshot_times: np.ndarray
-    bases: list
-    ortho_residuals: np.ndarray
+    bases: list                       # [(U, Z)] at snapshot times (U on the device)
+    ortho_residuals: np.ndarray       # per step, after the step
     sympl_residuals: np.ndarray
     fp_iterations: np.ndarray
     dmd_ranks: np.ndarray
     s_conds: np.ndarray
+    decomp_times: np.ndarray
+    dh_total: np.ndarray
+    dh_coeff: np.ndarray
+    dh_coeff_dd: np.ndarray
+    timers: object
+    dmd_imag_defect: float
     hyper_engaged: bool
+    notes: dict = field(default_factory=dict)
     deim_indices: list = field(default_factory=list)
     step_seconds: np.ndarray = None
-    notes: dict = field(default_factory=dict)
 
 
 def _diag_energies(system, ud, z):
@@ -349,6 +357,12 @@ def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_d
     s_conds = np.zeros(num_steps)
     deim_hist = []
     step_seconds = np.zeros(num_steps)
+    decomp_times, dh_tot, dh_z, dh_zdd = [], [], [], []
+    imag_defect = 0.0
+
+    def ham(u_now, z_now):
+        ee, kin = _diag_energies(system, u_now, z_now)
+        return kin + ee
 
     def diagnostics(tau, u_now, z_now):
         t_now = tau * dt
@@ -403,6 +417,7 @@ def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_d
             raise StepFailureError(f"step {tau} (t = {tau * dt:.6g}): {err}",
                                    iterations=err.iterations,
                                    residual_trace=err.residual_trace) from err
+        u_prev, z_prev = u, z
         u, z = res.u, res.z
         timers.flush_step()
         step_seconds[tau - 1] = _time.perf_counter() - tic
@@ -411,6 +426,20 @@ def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_d
         s_conds[tau - 1] = res.s_cond
         if hyper_now:
             dmd_ranks[tau - 1] = dmd_model.rank
+            imag_defect = max(imag_defect, dmd_model.imag_defect)
+        if hyper_now and decomp_stride and tau % decomp_stride == 0:
+            # Hamiltonian-error decomposition (driver.py:229-246): total, the
+            # coefficient part at the midpoint basis, and its DMD-DEIM surrogate
+            h_new, h_prev = ham(u, z), ham(u_prev, z_prev)
+            h_mid_new, h_mid_prev = ham(res.u_mid, z), ham(res.u_mid, z_prev)
+            hdd_new = hyp.hyper_hamiltonian_device(dmd_model, deim_model, res.u_mid, z, tau * dt,
+                                                   system, params)
+            hdd_prev = hyp.hyper_hamiltonian_device(dmd_model, deim_model, res.u_mid, z_prev,
+                                                    t_prev, system, params)
+            decomp_times.append(tau * dt)
+            dh_tot.append(float(np.linalg.norm(np.atleast_1d(h_new - h_prev))))
+            dh_z.append(float(np.linalg.norm(np.atleast_1d(h_mid_new - h_mid_prev))))
+            dh_zdd.append(float(np.linalg.norm(np.atleast_1d(hdd_new - hdd_prev))))
         diagnostics(tau, u, z)
 
     notes = {} if hyper_engaged else {"no_hyper_reduction_engaged": True}
@@ -419,5 +448,7 @@ def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_d
         electric_energy=np.asarray(energies), hamiltonian=np.asarray(hams),
         snapshot_times=np.asarray(snap_times), bases=bases, ortho_residuals=ortho_res,
         sympl_residuals=sympl_res, fp_iterations=fp_iters, dmd_ranks=dmd_ranks, s_conds=s_conds,
-        hyper_engaged=hyper_engaged, deim_indices=deim_hist, step_seconds=step_seconds,
-        notes=notes)
+        decomp_times=np.asarray(decomp_times), dh_total=np.asarray(dh_tot),
+        dh_coeff=np.asarray(dh_z), dh_coeff_dd=np.asarray(dh_zdd), timers=timers,
+        dmd_imag_defect=imag_defect, hyper_engaged=hyper_engaged, notes=notes,
+        deim_indices=deim_hist, step_seconds=step_seconds)

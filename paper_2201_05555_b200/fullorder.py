@@ -302,6 +302,8 @@ class PicEngine:
         self.r_phi = torch.zeros_like(self.r_rho)
         self.r_ee = torch.zeros((self.ring, p), dtype=torch.float64, device="cuda")
         self.r_kin = torch.zeros_like(self.r_ee)
+        # %globaltimer at the end of each ring step, per instance group
+        self.r_t = torch.zeros((self.groups, self.ring), dtype=torch.int64, device="cuda")
         self.graph = None
         self.launches = 0
 
@@ -326,7 +328,7 @@ class PicEngine:
                   self.counters[g].data_ptr(), self.ring, self.p,
                   self.r_rho.data_ptr() + 8 * a * nx, self.r_phi.data_ptr() + 8 * a * nx,
                   self.r_ee.data_ptr() + 8 * a, self.r_kin.data_ptr() + 8 * a,
-                  self.ws[g].data_ptr(), self.status[g].data_ptr(), stream)
+                  self.r_t[g].data_ptr(), self.ws[g].data_ptr(), self.status[g].data_ptr(), stream)
         self.launches += 1
 
     def launch_block(self, steps, first=False):
@@ -406,6 +408,9 @@ class PicRun:
         self.phi_hist = torch.zeros((rows, self.p, self.nx), dtype=torch.float64, device="cuda")
         self.ee_hist = torch.zeros((rows, self.p), dtype=torch.float64, device="cuda")
         self.kin_hist = torch.zeros((rows, self.p), dtype=torch.float64, device="cuda")
+        # device step end times (ns): row 0 = after the initial field, row k =
+        # when step k's last instance-group solve finished (max over groups)
+        self.t_hist = torch.zeros((self.e.groups, rows), dtype=torch.int64, device="cuda")
         self.tau = 0
 
     @property
@@ -437,7 +442,8 @@ class PicRun:
                   e.inst.data_ptr(), e.c.khat.data_ptr(), e.c.stencil.data_ptr(),
                   e.phi.data_ptr(), self.ee_hist[0].data_ptr(), s)
         self.phi_hist[0].copy_(e.phi)
-        e.launches += 3
+        _lib.call("picrom_timestamp", self.t_hist[0, 0:1].data_ptr(), s)
+        e.launches += 4
 
     def _drain(self, c0, count):
         """Copy ring rows of counters [c0, c0+count) into the full histories:
@@ -456,6 +462,8 @@ class PicRun:
             self.phi_hist[t + 1:t + m + 1].copy_(e.r_phi[r:r + m])
             if self.rho_hist is not None:
                 self.rho_hist[t + 1:t + m + 1].copy_(e.r_rho[r:r + m])
+            for g in range(e.groups):
+                self.t_hist[g, t + 1:t + m + 1].copy_(e.r_t[g, r:r + m])
             done += m
 
     def advance(self, k, use_graph=True):
@@ -477,6 +485,11 @@ class PicRun:
             self._drain(self.tau, 1)
             self.tau += 1
             k -= 1
+
+    def step_seconds(self):
+        """Device seconds of each completed step (host array, one sync)."""
+        t = self.t_hist[:, :self.tau + 1].cpu().numpy().max(axis=0).astype(np.float64)
+        return np.diff(t) * 1e-9
 
     def full_velocity(self):
         """v_tau = v_{tau-1/2} + 0.5 dt E(x_tau) (device), or v_0 before any step."""
@@ -566,7 +579,7 @@ def run_full_order(system, initial: ParticleEnsemble, dt, t_final,
     pots = phi[taus]
     if meta.ndim == 1:
         pots = pots.reshape(len(taus), system.mesh.num_cells, 1)
-    step_seconds = np.full(num_steps, total / max(num_steps, 1))
+    step_seconds = run.step_seconds()
     final = ParticleEnsemble(dev.from_device(run.x, meta), dev.from_device(vfinal, meta),
                              num_steps * dt)
     shape = tuple(initial.x.shape)

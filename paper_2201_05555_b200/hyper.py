@@ -39,7 +39,7 @@ from .errors import ConfigurationError, DegenerateDataError
 
 __all__ = ["DMDModel", "fit_dmd", "RBFInterpolant", "fit_parametric_dmd", "DEIMModel",
            "deim_greedy", "fit_deim", "hyper_hamiltonian", "make_hyper_stage", "DeimWindow",
-           "fit_deim_device", "make_hyper_stage_device"]
+           "fit_deim_device", "make_hyper_stage_device", "hyper_hamiltonian_device"]
 
 MODE_DISCARD = 1e-12          # |lambda| below this is dropped (hyper.py:40)
 IMAG_WARN = 1e-3              # relative imaginary defect warning level (hyper.py:41)
@@ -471,6 +471,45 @@ def make_hyper_stage(dmd, deim, t_stage, mesh, charge, params=None):
     """Reference signature (single mesh): see make_hyper_stage_device."""
     from .fullorder import VlasovSystem
     return make_hyper_stage_device(dmd, deim, t_stage, VlasovSystem(mesh, charge), params)
+
+
+def hyper_hamiltonian_device(dmd, deim, u, z, t, system, params=None):
+    """hyper_hamiltonian (hyper.py:280-296) for a system with one mesh per column
+    (ParametricVlasovSystem, C3/C4) or a single mesh: kinetic 0.5 z^T (U_V^T U_V) z
+    from one Gram, the field term (0.5/m_p,j) (w_j . lambda(U_X[I] z_j) phi_j)
+    with the value gather at the d x p sampled positions on the device
+    (picrom_gather, each column's own mesh; weights rescaled by the column's
+    charge weight as in the hyper stage)."""
+    from .driver import _column_charge, _inst_table
+    if not isinstance(u, torch.Tensor):
+        u = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).to("cuda")
+    z = np.asarray(z, dtype=float)
+    n2, n = u.shape
+    N, p = n2 // 2, z.shape[1]
+    idx = np.asarray(deim.indices, dtype=np.int64)
+    d = len(idx)
+    uxd = _rows(u, idx)                                      # d x n
+    gv = _tall.gram([(u[N:], False)])
+    kin = 0.5 * np.einsum("ij,ij->j", z, gv @ z)
+    if params is not None:
+        dmd.ensure_coords(params)
+    phi = dmd.potential_device(t)                            # (p, nx)
+    xd = torch.from_numpy(np.ascontiguousarray((uxd @ z).T)).to("cuda")   # (p, d)
+    lam = torch.empty((p, d), dtype=torch.float64, device="cuda")
+    st = dev.new_status()
+    mesh = system.mesh
+    _lib.call("picrom_gather", xd.data_ptr(), d, p, d, _inst_table(system, p).data_ptr(),
+              mesh.num_cells, mesh.degree, phi.data_ptr(), 0, lam.data_ptr(), d, st.data_ptr(),
+              dev.stream_handle())
+    lam_h = lam.cpu().numpy()
+    dev.raise_if_bad(st, p, 2)
+    qw_ref = system.charge.charge_weight
+    w = np.asarray(deim.weights, dtype=float)
+    fld = np.empty(p)
+    for j in range(p):
+        ch = _column_charge(system, j)
+        fld[j] = (0.5 / ch.particle_mass) * ((w * (ch.charge_weight / qw_ref)) @ lam_h[j])
+    return kin + fld
 
 
 def hyper_hamiltonian(dmd, deim, u, z, t, mesh, charge):

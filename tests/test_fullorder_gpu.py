@@ -174,7 +174,7 @@ def test_push_plus_solve_equals_fused_step(mods):
                 _lib.call("picrom_pic_step", e.x.data_ptr(), e.v.data_ptr(), n, p, n,
                           e.inst.data_ptr(), nx, d, e.c.khat.data_ptr(), e.c.stencil.data_ptr(),
                           e.phi.data_ptr(), 0.05, kick, kfull, k, None, 0, 0, rho.data_ptr(),
-                          phi.data_ptr(), ee.data_ptr(), kin.data_ptr(), ws.data_ptr(),
+                          phi.data_ptr(), ee.data_ptr(), kin.data_ptr(), None, ws.data_ptr(),
                           st.data_ptr(), s)
         outs.append([t.cpu().numpy() for t in (e.x, e.v, rho, phi, ee, kin)])
     for a, b in zip(*outs):
@@ -248,3 +248,53 @@ def test_divergence_error_reports_parameter_and_time(mods):
     with pytest.raises(fo.DivergenceError) as err:
         fo.VerletStepper(sysm).step(fo.ParticleEnsemble(x, v, 0.0), 0.01)
     assert err.value.parameter_index == 1
+
+
+def test_step_seconds_are_per_step_device_times(mods):
+    """run_full_order's step_seconds are the device times of each step (the
+    end of each step's last solve, %globaltimer), not a uniform fill."""
+    fem, fo = mods
+    rng = np.random.default_rng(12)
+    L, n, p, steps = 10 * np.pi, 50_000, 8, 40
+    x, v = rng.uniform(0, L, (n, p)), rng.standard_normal((n, p))
+    sysm = fo.VlasovSystem(fem.build_mesh(L, 128, 3), fem.ChargeConfig(n, L))
+    rec = fo.run_full_order(sysm, fo.ParticleEnsemble(x, v), 0.05, steps * 0.05,
+                            record=fo.RecordOptions(energy_stride=1, record_snapshots=False))
+    ss = rec.step_seconds
+    assert ss.shape == (steps,) and np.all(ss > 0) and np.all(ss < 0.05)
+    assert len(np.unique(ss)) > steps // 2
+    assert ss.sum() <= rec.phase_seconds["fom_step"] * 1.01
+
+
+def test_reference_stepper_drives_gpu_system(mods):
+    """The unmodified reference's own VerletStepper / run_full_order (picrom
+    from baseline/_ref, installed from /root/reference/pkg) driving the GPU
+    VlasovSystem through its duck-typed `field` seam (fullorder.py:111-114):
+    identical to the reference with its own P1 system to 1e-12."""
+    import sys
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "picrom").exists():
+        pytest.skip("baseline/_ref not installed (pip install --target baseline/_ref)")
+    sys.path.insert(0, str(ref))
+    try:
+        from picrom import fem as rfem
+        from picrom import fullorder as rfo
+    finally:
+        sys.path.remove(str(ref))
+    fem, fo = mods
+    rng = np.random.default_rng(13)
+    L, nx, n, p = 4 * np.pi, 32, 6000, 3
+    x, v = rng.uniform(0, L, (n, p)), rng.standard_normal((n, p))
+    rsys = rfo.VlasovSystem(rfem.build_mesh(L, nx), rfem.ChargeConfig(num_particles=n, length=L))
+    gsys = fo.VlasovSystem(fem.build_mesh(L, nx), fem.ChargeConfig(n, L))
+    opts = rfo.RecordOptions(energy_stride=1, snapshot_stride=5)
+    want = rfo.run_full_order(rsys, rfo.ParticleEnsemble(x.copy(), v.copy()), 0.05, 1.0, opts)
+    got = rfo.run_full_order(gsys, rfo.ParticleEnsemble(x.copy(), v.copy()), 0.05, 1.0, opts)
+    assert rel(got.snapshots_x, want.snapshots_x) <= 1e-12
+    assert rel(got.snapshots_v, want.snapshots_v) <= 1e-12
+    assert np.max(np.abs(got.electric_energy - want.electric_energy)
+                  / np.abs(want.electric_energy)) <= 1e-10
+    st = rfo.VerletStepper(gsys)
+    e1 = st.step(rfo.ParticleEnsemble(x.copy(), v.copy()), 0.05)
+    e1r = rfo.VerletStepper(rsys).step(rfo.ParticleEnsemble(x.copy(), v.copy()), 0.05)
+    assert rel(e1.x, e1r.x) <= 1e-13 and rel(e1.v, e1r.v) <= 1e-13

@@ -81,16 +81,19 @@ def test_pic_step_guards_tickets_counter(m, nx):
         status = Guarded(2, dtype=torch.int64, fill=-1)
         hist = [Guarded(ring * p * nx), Guarded(ring * p * nx), Guarded(ring * p),
                 Guarded(ring * p)]
+        thist = Guarded(ring, dtype=torch.int64, fill=0)
         for k in range(steps):
             kick, kfull = (0.025, 0.0) if k == 0 else (0.05, 0.025)
             m.lib.call("picrom_pic_step", x.ptr, v.ptr, n, p, n, inst.data_ptr(), nx, d,
                        c.khat.data_ptr(), c.stencil.data_ptr(), phi.ptr, 0.05, kick, kfull, k,
                        counter.ptr, ring, p, hist[0].ptr, hist[1].ptr, hist[2].ptr, hist[3].ptr,
-                       ws.ptr, status.ptr, s)
+                       thist.ptr, ws.ptr, status.ptr, s)
         torch.cuda.synchronize()
-        for b in [x, v, phi, ws, counter, status] + hist:
+        for b in [x, v, phi, ws, counter, status, thist] + hist:
             assert b.intact()
         assert int(counter.t[0]) == steps and int(counter.t[1]) == 0
+        th = thist.t.cpu().numpy()
+        assert np.all(th > 0)                 # every ring row stamped by its step's last solve
         assert int(status.t[0]) == -1
         assert bool(torch.isfinite(phi.t).all()) and bool(torch.isfinite(x.t).all())
         outs.append([b.t.cpu().numpy() for b in [x, v, phi] + hist])

@@ -172,14 +172,40 @@ def test_reduced_run_with_hyper_reduction(m):
     params = np.stack([np.linspace(0.03, 0.06, 6), np.linspace(0.8, 1.0, 6)], axis=1)
     kw = dict(basis_dim=4, subsample=4, window=2, deim_dim=8, deim_period=2, deim_update=3,
               dt=0.01)
-    h = orl.run_reduced(osys, params, x0, v0, num_steps=8, energy_stride=1, **kw)
+    h = orl.run_reduced(osys, params, x0, v0, num_steps=8, energy_stride=1, decomp_stride=2, **kw)
     rec = m.driver.run_reduced(gsys, params, x0, v0, t_final=0.08, energy_stride=1,
-                               decomp_stride=10**9, **kw)
+                               decomp_stride=2, **kw)
     assert rec.hyper_engaged and h.hyper_engaged
     for a, b in zip(rec.deim_indices, h.deim_indices):
         np.testing.assert_array_equal(a, b)
     ee_o = np.asarray(h.electric)
     assert np.max(np.abs(rec.electric_energy - ee_o) / np.abs(ee_o)) <= 1e-9
+    # Hamiltonian-error decomposition at decomp_stride (driver.py:229-246):
+    # differences of O(|H|) energies, compared at 1e-10 |H|
+    np.testing.assert_allclose(rec.decomp_times, h.decomp_times)
+    assert len(rec.decomp_times) >= 2
+    hscale = np.linalg.norm(np.asarray(h.kinetic[-1]) + np.asarray(h.electric[-1]))
+    for key in ("dh_total", "dh_coeff", "dh_coeff_dd"):
+        np.testing.assert_allclose(getattr(rec, key), getattr(h, key), rtol=0, atol=1e-10 * hscale)
+    assert rec.dmd_imag_defect >= 0.0 and rec.timers is not None
+    assert rec.s_conds.shape == rec.fp_iterations.shape == (8,)
+
+
+def test_reduced_run_decomposition_per_instance(m):
+    """decomp_stride on per-instance meshes (C4's layout): the device
+    hyper_hamiltonian (per-column mesh, mass and weight scaling) vs the oracle."""
+    u, z, osys, gsys, x0, v0, lengths = _setup(m, 2, True, n=3000, p=6, nx=16, nb=4, seed=8)
+    params = np.stack([2 * np.pi / lengths, np.linspace(0.03, 0.06, 6)], axis=1)
+    kw = dict(basis_dim=4, subsample=4, window=2, deim_dim=8, deim_period=2, deim_update=3,
+              dt=0.01)
+    h = orl.run_reduced(osys, params, x0, v0, num_steps=7, energy_stride=1, decomp_stride=3, **kw)
+    rec = m.driver.run_reduced(gsys, params, x0, v0, t_final=0.07, energy_stride=1,
+                               decomp_stride=3, **kw)
+    np.testing.assert_array_equal(rec.fp_iterations, np.asarray(h.fp_iterations))
+    np.testing.assert_allclose(rec.decomp_times, h.decomp_times)
+    hscale = np.linalg.norm(np.asarray(h.kinetic[-1]) + np.asarray(h.electric[-1]))
+    for key in ("dh_total", "dh_coeff", "dh_coeff_dd"):
+        np.testing.assert_allclose(getattr(rec, key), getattr(h, key), rtol=0, atol=1e-10 * hscale)
 
 
 @pytest.mark.parametrize("d", [2, 3])
