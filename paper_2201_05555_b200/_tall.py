@@ -23,6 +23,14 @@ from .errors import ConfigurationError
 
 _WS = {}
 
+# set by parallel.row_sharded(): Gram results are partial sums over this
+# rank's rows and are all-reduced before use (None: single process)
+reduce_hook = None
+
+
+def _reduced(out):
+    return reduce_hook(out) if reduce_hook is not None else out
+
 
 def _ws(rows, width):
     need = int(_lib.query("picrom_rom_workspace_bytes", int(rows), 1, 1, 1))
@@ -57,7 +65,7 @@ def gram(blocks):
               _arr(C.c_int, [int(t.stride(0)) for t, _ in blocks]),
               _arr(C.c_int, widths), _arr(C.c_int, [int(bool(j)) for _, j in blocks]),
               rows, out.data_ptr(), _ws(rows, W).data_ptr(), dev.stream_handle())
-    return out.cpu().numpy()
+    return _reduced(out).cpu().numpy()
 
 
 def gram_tasks(blocks, tasks):
@@ -75,7 +83,7 @@ def gram_tasks(blocks, tasks):
               len(tasks), _arr(C.c_int, [int(i) for i, _ in tasks]),
               _arr(C.c_int, [int(j) for _, j in tasks]),
               rows, out.data_ptr(), _ws(rows, W).data_ptr(), dev.stream_handle())
-    return out.cpu().numpy()
+    return _reduced(out).cpu().numpy()
 
 
 def combine(terms, out=None, accumulate=False):

@@ -29,7 +29,7 @@ import torch
 from . import _device as dev
 from . import _lib, _tall
 from . import hyper as hyp
-from .errors import DivergenceError, EvaluationError, StepFailureError
+from .errors import ConfigurationError, DivergenceError, EvaluationError, StepFailureError
 from .fem import ChargeConfig, PoissonOperator, build_mesh
 from .fullorder import VlasovSystem
 from .reduction import (
@@ -105,8 +105,23 @@ class _Cols:
         return None if self.dev is None else self.dev.data_ptr()
 
 
+def _partial_inst(inst):
+    """Instance table of a row shard: the background bg*h is added by the
+    background owner only (rho partials of all ranks sum to rho)."""
+    from . import parallel
+    sh = parallel.active()
+    if sh is None or sh.background_owner():
+        return inst
+    loc = inst.clone()
+    loc.view(-1, dev.INST_STRIDE)[:, 3] = 0.0           # I_BGH
+    return loc
+
+
 def _field_device(system, ud, z, cols, want_energy=False, status=None):
-    """phi (p', nx) [, energy (p')] of X_r = U_X z on the device."""
+    """phi (p', nx) [, energy (p')] of X_r = U_X z on the device.  Row-sharded
+    (parallel.row_sharded): the local charge partial is all-reduced before the
+    replicated Poisson solve."""
+    from . import parallel
     N2, n = ud.shape
     N = N2 // 2
     p = z.shape[1]
@@ -118,10 +133,21 @@ def _field_device(system, ud, z, cols, want_energy=False, status=None):
     phi = torch.empty((p, nx), dtype=torch.float64, device="cuda")
     energy = torch.empty(p, dtype=torch.float64, device="cuda") if want_energy else None
     st = status if status is not None else dev.new_status()
+    s = dev.stream_handle()
+    sh = parallel.active()
+    if sh is None or sh.world == 1:
+        _lib.call("picrom_rom_field", ud.data_ptr(), N, n, zd.data_ptr(), p, p, cols.ptr,
+                  inst.data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(), phi.data_ptr(),
+                  None, dev.ptr(energy), _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(), s)
+        return zd, inst, phi, energy, st
+    rho = torch.empty((p, nx), dtype=torch.float64, device="cuda")
     _lib.call("picrom_rom_field", ud.data_ptr(), N, n, zd.data_ptr(), p, p, cols.ptr,
-              inst.data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(), phi.data_ptr(),
-              None, dev.ptr(energy), _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(),
-              dev.stream_handle())
+              _partial_inst(inst).data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(), None,
+              rho.data_ptr(), None, _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(), s)
+    parallel.allreduce_sum(rho)
+    col_inst = inst if cols.dev is None else inst[torch.from_numpy(cols.host.astype(np.int64)).cuda()]
+    _lib.call("picrom_poisson", rho.data_ptr(), p, nx, d, col_inst.data_ptr(), c.khat.data_ptr(),
+              c.stencil.data_ptr(), phi.data_ptr(), dev.ptr(energy), s)
     return zd, inst, phi, energy, st
 
 
@@ -180,7 +206,8 @@ def exact_gradients_device(system, ud, z, cols=None, harvest=True):
               proj[0].data_ptr(), proj[1].data_ptr(), p, dev.ptr(lam), e.data_ptr(), p,
               _rom_ws(N, p, n, mesh.num_cells).data_ptr(), st.data_ptr(), dev.stream_handle())
     _raise_eval(st, p)
-    ph = proj.cpu().numpy()
+    from . import parallel
+    ph = parallel.allreduce_sum(proj).cpu().numpy()      # U^T E partials (sharded runs)
     return DeviceGradient(ud, z, e, ph[0], ph[1]), phi, lam
 
 
@@ -203,6 +230,8 @@ def make_full_stage(system):
     """Warm-up coefficient gradient U_mid^T F(U_mid z) on all columns (driver.py:79-89):
     g(z) = U_X^T E(U_X z) + (U_V^T U_V) z, E by the fused rom_field/rom_gather
     passes, the Gram once per stage."""
+
+    from . import parallel
 
     def factory(u_mid):
         N = u_mid.shape[0] // 2
@@ -232,12 +261,17 @@ def make_full_stage(system):
             zd.copy_(bufs["z_h"], non_blocking=True)
             st.fill_(-1)
             sh = dev.stream_handle()
-            _lib.call("picrom_rom_field", u_mid.data_ptr(), N, n, zd.data_ptr(), p, p, None,
-                      bufs["inst"].data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(),
-                      phi.data_ptr(), None, None, bufs["ws"].data_ptr(), st.data_ptr(), sh)
+            if parallel.active() is None or parallel.active().world == 1:
+                _lib.call("picrom_rom_field", u_mid.data_ptr(), N, n, zd.data_ptr(), p, p, None,
+                          bufs["inst"].data_ptr(), nx, d, c.khat.data_ptr(),
+                          c.stencil.data_ptr(), phi.data_ptr(), None, None,
+                          bufs["ws"].data_ptr(), st.data_ptr(), sh)
+            else:
+                phi.copy_(_field_device(system, u_mid, z, _Cols(None, p), status=st)[2])
             _lib.call("picrom_rom_gather", u_mid.data_ptr(), N, n, zd.data_ptr(), p, p, None,
                       bufs["inst"].data_ptr(), nx, d, phi.data_ptr(), 0, gout.data_ptr(), p,
                       None, None, 0, bufs["ws"].data_ptr(), st.data_ptr(), sh)
+            parallel.allreduce_sum(gout)                  # U_X^T E partials (sharded runs)
             out_h = bufs["out_h"]
             out_h[:n * p].copy_(gout.reshape(-1), non_blocking=True)
             out_h[n * p:].copy_(st.view(torch.float64), non_blocking=True)
@@ -297,7 +331,7 @@ def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_di
                 deim_update, dt, t_final, svd_tol_dmd=1e-5, fp_tol=1e-9, fp_max_iter=100,
                 hyper_reduction=True, printed_subset_variant=False, printed_deim_ranking=False,
                 energy_stride=10, snapshot_stride=None, decomp_stride=50, record_snapshots=True,
-                timers=None, u0=None, z0=None):
+                timers=None, u0=None, z0=None, sharding=None):
     """Reduced-order run over all parameter columns (driver.py:117-274).
 
     U lives on the device for the whole run; Z and every small matrix on the
@@ -306,9 +340,24 @@ def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_di
     threads for the run: the n x n / window-size algebra gains nothing from
     more, and idle OpenBLAS threads spinning on 16 cores slowed every host
     step (profiles/r01b: the 420 x 420 DEIM eigh 48 -> 8 ms, argmax round
-    trips 3x)."""
+    trips 3x).
+
+    ``sharding`` (parallel.RowSharding, under torchrun): this rank advances
+    the particle rows [lo, hi) of U (u0 may be the global basis or the local
+    rows); every N-row product is all-reduced, Z and the records are
+    replicated, the snapshot bases hold the local rows.  No hyper-reduction
+    in the sharded mode (the DEIM window and greedy are not sharded)."""
     from threadpoolctl import threadpool_limits
-    with threadpool_limits(limits=4, user_api="blas"):
+
+    from . import parallel
+    if sharding is not None:
+        if hyper_reduction:
+            raise ConfigurationError("row-sharded reduced runs support hyper_reduction=False only")
+        if u0 is None:
+            u0, z0 = complex_svd_basis(x0, v0, basis_dim)
+        if u0.shape[0] == 2 * sharding.N:
+            u0 = sharding.local_u(u0 if isinstance(u0, torch.Tensor) else np.asarray(u0))
+    with threadpool_limits(limits=4, user_api="blas"), parallel.row_sharded(sharding):
         return _run_reduced(system, params, x0, v0, basis_dim=basis_dim, subsample=subsample,
                             window=window, deim_dim=deim_dim, deim_period=deim_period,
                             deim_update=deim_update, dt=dt, t_final=t_final,
