@@ -68,6 +68,23 @@ def gram(blocks):
     return _reduced(out).cpu().numpy()
 
 
+def cross_gram(a_blocks, b_blocks):
+    """A^T B (host numpy, wa x wb) for A = column concatenation of a_blocks and
+    B of b_blocks (tall device blocks, (tensor, jswap) pairs), picrom_cross_gram."""
+    blocks = [(t if t.is_contiguous() else t.contiguous(), j) for t, j in a_blocks + b_blocks]
+    rows = blocks[0][0].shape[0]
+    widths = [int(t.shape[1]) for t, _ in blocks]
+    wa = sum(widths[:len(a_blocks)])
+    wb = sum(widths[len(a_blocks):])
+    out = torch.empty((wa, wb), dtype=torch.float64, device="cuda")
+    _lib.call("picrom_cross_gram", len(blocks), len(a_blocks),
+              _arr(C.c_void_p, [t.data_ptr() for t, _ in blocks]),
+              _arr(C.c_int, [int(t.stride(0)) for t, _ in blocks]),
+              _arr(C.c_int, widths), _arr(C.c_int, [int(bool(j)) for _, j in blocks]),
+              rows, out.data_ptr(), _ws(rows, wa + wb).data_ptr(), dev.stream_handle())
+    return _reduced(out).cpu().numpy()
+
+
 def gram_tasks(blocks, tasks):
     """Selected block products of gram(blocks): tasks = [(i, j), ...] -> numpy (W x W)
     with block (i, j) = B_i^T B_j for each task (other entries unspecified)."""

@@ -331,7 +331,7 @@ def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_di
                 deim_update, dt, t_final, svd_tol_dmd=1e-5, fp_tol=1e-9, fp_max_iter=100,
                 hyper_reduction=True, printed_subset_variant=False, printed_deim_ranking=False,
                 energy_stride=10, snapshot_stride=None, decomp_stride=50, record_snapshots=True,
-                timers=None, u0=None, z0=None, sharding=None):
+                timers=None, u0=None, z0=None, sharding=None, init="host"):
     """Reduced-order run over all parameter columns (driver.py:117-274).
 
     U lives on the device for the whole run; Z and every small matrix on the
@@ -341,6 +341,11 @@ def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_di
     more, and idle OpenBLAS threads spinning on 16 cores slowed every host
     step (profiles/r01b: the 420 x 420 DEIM eigh 48 -> 8 ms, argmax round
     trips 3x).
+
+    ``init``: "host" (default) computes the initial basis by the reference's
+    LAPACK complex SVD (bit-identical U, Z); "device" by
+    reduction.complex_svd_basis_device (Hermitian Gram on the GPU: the same
+    basis up to a phase per singular vector, ~100x faster at C3).
 
     ``sharding`` (parallel.RowSharding, under torchrun): this rank advances
     the particle rows [lo, hi) of U (u0 may be the global basis or the local
@@ -367,20 +372,23 @@ def run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_di
                             printed_deim_ranking=printed_deim_ranking,
                             energy_stride=energy_stride, snapshot_stride=snapshot_stride,
                             decomp_stride=decomp_stride, record_snapshots=record_snapshots,
-                            timers=timers, u0=u0, z0=z0)
+                            timers=timers, u0=u0, z0=z0, init=init)
 
 
 def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_dim, deim_period,
                  deim_update, dt, t_final, svd_tol_dmd, fp_tol, fp_max_iter, hyper_reduction,
                  printed_subset_variant, printed_deim_ranking, energy_stride, snapshot_stride,
-                 decomp_stride, record_snapshots, timers, u0, z0):
+                 decomp_stride, record_snapshots, timers, u0, z0, init="host"):
     from .diagnostics import PhaseTimers
     params = np.asarray(params, dtype=float)
     num_steps = int(round(t_final / dt))
     snap_stride = (max(1, int(snapshot_stride)) if snapshot_stride is not None
                    else max(1, num_steps // 40))
     timers = timers or PhaseTimers()
-    if u0 is None:
+    if u0 is None and init == "device":
+        from .reduction import complex_svd_basis_device
+        u, z = complex_svd_basis_device(x0, v0, basis_dim)
+    elif u0 is None:
         u, z = complex_svd_basis(x0, v0, basis_dim, device=True)
     else:
         u = u0 if isinstance(u0, torch.Tensor) else torch.from_numpy(np.asarray(u0)).to("cuda")

@@ -38,7 +38,7 @@ from .errors import ConfigurationError, StepFailureError
 __all__ = [
     "jmul", "jrmul", "complex_svd_basis", "reconstruct", "orthosymplectic_residuals", "SMatrix",
     "select_parameter_subset", "basis_velocity", "retraction", "tangent_velocity", "fixed_point",
-    "prk2_step", "PRKResult",
+    "prk2_step", "PRKResult", "complex_svd_basis_device",
 ]
 
 
@@ -122,6 +122,52 @@ def complex_svd_basis(x, v, n, device=False):
     if device:
         return torch.from_numpy(u).to("cuda"), z
     return u, z
+
+
+def complex_svd_basis_device(x, v, n):
+    """Device initial basis: the ortho-symplectic U of complex_svd_basis
+    (reduction.py:56-76) from the p x p Hermitian Gram of A = x + i v instead of
+    a host SVD of the N x p complex matrix (11 s of LAPACK at C3).
+
+      A^H A = (X^T X + V^T V) + i (X^T V - V^T X)   one N-row Gram of [X, V]
+      A^H A W = W Sigma^2                            p x p Hermitian eigensolve (host)
+      A W_k Sigma_k^-1 = Phi + i Psi                 two N-row combines
+      Z = U^T [x; v]                                 one N-row cross Gram
+
+    Singular vectors are defined up to a phase per vector: the host LAPACK
+    path and this one agree up to a per-column rotation of (Phi_j, Psi_j)
+    (an ortho-symplectic change of reduced coordinates, under which U Z and
+    every reduced quantity are invariant); tests compare modulo that phase.
+    Returns (U (2N x n) CUDA tensor, Z (n x p) host)."""
+    from scipy.linalg import eigh
+    if n % 2 or n < 2:
+        raise ConfigurationError(f"basis dimension must be even and >= 2, got {n}")
+    xd, _ = _tall_in(x if not isinstance(x, np.ndarray) or x.ndim == 2 else np.atleast_2d(x.T).T)
+    vd, _ = _tall_in(v if not isinstance(v, np.ndarray) or v.ndim == 2 else np.atleast_2d(v.T).T)
+    N, p = xd.shape
+    half = n // 2
+    if half > min(N, p):
+        raise ConfigurationError(f"rank {half} complex basis needs at least {half} snapshots")
+    xx = _tall.gram([(xd, False)])
+    vv = _tall.gram([(vd, False)])
+    xv = _tall.cross_gram([(xd, False)], [(vd, False)])
+    herm = (xx + vv) + 1j * (xv - xv.T)
+    lam, w = eigh(herm)
+    order = np.argsort(lam)[::-1][:half]
+    lam, w = lam[order], w[:, order]
+    sig = np.sqrt(np.clip(lam, 0.0, None))
+    wr, wi = w.real / sig, w.imag / sig
+    phi = _tall.combine([(xd, wr, False), (vd, -wi, False)])          # Re(A W / sigma)
+    psi = _tall.combine([(xd, wi, False), (vd, wr, False)])           # Im(A W / sigma)
+    u = torch.empty((2 * N, n), dtype=torch.float64, device="cuda")
+    u[:N, :half] = phi
+    u[:N, half:] = -psi
+    u[N:, :half] = psi
+    u[N:, half:] = phi
+    # Z = U_X^T x + U_V^T v (two N-row cross Grams)
+    zx = _tall.cross_gram([(u[:N], False)], [(xd, False)])
+    zv = _tall.cross_gram([(u[N:], False)], [(vd, False)])
+    return u, zx + zv
 
 
 def reconstruct(u, z):

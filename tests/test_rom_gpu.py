@@ -290,3 +290,38 @@ def test_host_result_views_keep_their_buffer(m):
     # the potential solves the Poisson problem of the recorded charge
     phi = m.fem.PoissonOperator(sysm.mesh).solve(rec.charge_history[-1])
     assert rel(phi, rec.potential_history[-1]) <= 1e-12
+
+
+def _align_phases(u, ref, n):
+    """Rotate each (Phi_j, Psi_j) pair of u onto ref's phase (complex
+    singular vectors are defined up to e^{i theta})."""
+    N = u.shape[0] // 2
+    h = n // 2
+    a = u[:N, :h] + 1j * u[N:, :h]
+    b = ref[:N, :h] + 1j * ref[N:, :h]
+    ph = np.exp(1j * np.angle(np.einsum("ij,ij->j", np.conj(a), b)))
+    a = a * ph
+    out = np.empty_like(u)
+    out[:N, :h], out[N:, :h] = a.real, a.imag
+    out[:N, h:], out[N:, h:] = -a.imag, a.real
+    return out
+
+
+@pytest.mark.parametrize("N,p,n", [(20_000, 16, 6), (200_000, 128, 20)])
+def test_device_complex_svd_basis(m, N, p, n):
+    """complex_svd_basis_device (Hermitian Gram + eigensolve + combines) equals the
+    host LAPACK basis modulo the per-vector phase: U <= 1e-12 after phase
+    alignment, U Z (the reconstruction) and U^T U directly."""
+    rng = np.random.default_rng(N)
+    ks = rng.uniform(0.4, 0.6, p)
+    x = np.stack([rng.uniform(0, 2 * np.pi / k, N) for k in ks], axis=1)
+    v = rng.standard_normal((N, p))
+    u_h, z_h = m.red.complex_svd_basis(x, v, n)
+    u_d, z_d = m.red.complex_svd_basis_device(x, v, n)
+    u_d = u_d.cpu().numpy()
+    ua = _align_phases(u_d, u_h, n)
+    assert rel(ua, u_h) <= 1e-12
+    assert rel(u_d @ z_d, u_h @ z_h) <= 1e-12
+    assert np.abs(u_d.T @ u_d - np.eye(n)).max() <= 1e-13
+    o, s_ = m.red.orthosymplectic_residuals(u_d)
+    assert o <= 1e-13 and s_ <= 1e-13

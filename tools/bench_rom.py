@@ -88,6 +88,13 @@ def measure(config="C3", n=0, steps=5, warmup=2, e2e=True, cpu=True):
     from paper_2201_05555_b200.reduction import complex_svd_basis
     u0, z0 = complex_svd_basis(x0, v0, nb)
     init_s = time.perf_counter() - t0
+    from paper_2201_05555_b200.reduction import complex_svd_basis_device
+    complex_svd_basis_device(x0[:1000], v0[:1000], nb)          # warm the kernels
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    complex_svd_basis_device(x0, v0, nb)
+    torch.cuda.synchronize()
+    init_dev_s = time.perf_counter() - t0
     kw = dict(basis_dim=nb, subsample=sub, window=window, deim_dim=ex.get("deim_dim", 8),
               deim_period=ex.get("deim_period", 3), deim_update=ex.get("deim_update", 2), dt=w.dt,
               t_final=total * w.dt, hyper_reduction=hyper, energy_stride=10**9,
@@ -126,6 +133,10 @@ def measure(config="C3", n=0, steps=5, warmup=2, e2e=True, cpu=True):
         "dmd_ranks": rec.dmd_ranks[-steps:].tolist(),
         "ortho_residual_last": float(rec.ortho_residuals[-1]),
         "generation_s": gen_s, "init_csvd_s": init_s,
+        "init_csvd_device_s": init_dev_s,
+        "init_note": "initial basis: host LAPACK complex SVD (reference path, used for the run) vs "
+                     "reduction.complex_svd_basis_device (Hermitian Gram on the GPU, same basis up to "
+                     "a phase per singular vector; host (N, p) arrays uploaded inside the timing)",
     }
     if e2e:
         del u0d
