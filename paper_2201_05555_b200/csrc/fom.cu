@@ -4,6 +4,7 @@
 // Reference: /root/reference/pkg/src/picrom/fem.py and fullorder.py (see the
 // per-function citations in include/picrom_b200.h).  Design notes: DESIGN.md.
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -146,7 +147,11 @@ static int grid_for(long long n, int p, int occ) {
   // stragglers, ~7 us at C2, profiles/r02 timeline) -- when it idles <= 1/16
   // of the slots
   if (p <= g) {
-    const long long m = g / p;
+    long long m = g / p;
+#ifdef PICROM_CLUSTER_MAXM
+    m = std::min<long long>(m, PICROM_CLUSTER_MAXM);     // dev variant: cluster-sized grids
+    g = m * p;
+#endif
     if ((g - m * p) * 16 <= g) g = m * p;
   }
   return (int)g;
@@ -227,6 +232,8 @@ struct StepArgs {
   // fused solve (LEAPFROG): the last CTA finishing an instance solves it
   int fuse_solve;
   unsigned int* inst_done;   // p tickets (zeroed; left zeroed)
+  int cluster_m;             // > 0: the m CTAs of an instance form one thread-block
+                             // cluster; partial rows go through DSMEM, rank 0 solves
 };
 
 #ifdef PICROM_EXP_TIMING
@@ -358,7 +365,8 @@ __device__ __forceinline__ int kh_pad(int r) { return r + (r >> 2); }
 // in shared memory; crow_pre >= 0: the step counter value already read.
 __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int ntickets,
                            size_t avail, const double* kh_pre = nullptr,
-                           const double* stn_pre = nullptr, long long crow_pre = -1) {
+                           const double* stn_pre = nullptr, long long crow_pre = -1,
+                           bool rho_ready = false, double kin_ready = 0.0) {
   const int nx = a.nx;
   double* rho = sm;                      // nx (phi overwrites it after the circulant)
   double* kh = rho + nx;                 // khat, padded (kh_pad)
@@ -379,7 +387,10 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
   double* energy_out = a.energy_out ? a.energy_out + row * a.hist_stride_e : nullptr;
   double* kin_out = a.kin_out ? a.kin_out + row * a.hist_stride_e : nullptr;
 
-  if (a.seg_dense > 0) {
+  if (rho_ready) {
+    // rho already assembled in sm[0, nx) by the caller (cluster path)
+    if (kin_out && tid == 0) kin_out[j] = 0.5 * kin_ready;
+  } else if (a.seg_dense > 0) {
     const double qw = ip[I_QW], bgh = ip[I_BGH];
     for (int nd = tid; nd < nx; nd += blockDim.x) {
       const double s = ordered_sum(a.seg_hist + (size_t)j * nx + nd, (size_t)a.p * nx, a.seg_dense);
@@ -596,6 +607,14 @@ constexpr int kFixNT = PICROM_FIX_NT;
 constexpr int kFixMinB = PICROM_FIX_MINB;
 constexpr int kFixU = PICROM_FIX_U;
 constexpr int kFixChunk = 32767;
+
+// per-instance thread-block clusters in the fused step (DSMEM reduction to
+// the solving CTA) where the grid is instance-aligned
+#ifdef PICROM_NO_CLUSTER
+constexpr bool kUseCluster = false;
+#else
+constexpr bool kUseCluster = true;
+#endif
 
 // programmatic dependent launch between consecutive leapfrog steps: off --
 // with two instance groups pipelined on separate streams it cost 2-3 us per
@@ -1002,8 +1021,11 @@ step_kernel(StepArgs a, SolveArgs sa) {
 #ifdef PICROM_EXP_NOHIST
     if (false)
 #endif
+    // cluster path: the CTA's row stays in its own smem (the coefficient
+    // region, free after the particle loop) for rank 0 to read over DSMEM
+    double* seg_out = (MODE == MODE_LEAPFROG && a.cluster_m > 0) ? coef : a.seg_hist + (size_t)seg * nx;
     if constexpr (FIX) {
-      for (int nd = tid; nd < nx; nd += NT) a.seg_hist[(size_t)seg * nx + nd] = acc[nd] + fold_limbs(nd);
+      for (int nd = tid; nd < nx; nd += NT) seg_out[nd] = acc[nd] + fold_limbs(nd);
     } else
     for (int nd = tid; nd < nx; nd += NT) {
       double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1017,13 +1039,48 @@ step_kernel(StepArgs a, SolveArgs sa) {
             if (hh + u < H) s8[u] += rowp[(hh + u + nd) & (H - 1)];
         }
       }
-      a.seg_hist[(size_t)seg * nx + nd] =
-          ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+      seg_out[nd] = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     }
     TSTAMP(2, MODE == MODE_LEAPFROG && j == 0 && seg_hi == a.n);
     TL(5);
     if constexpr (MODE == MODE_LEAPFROG) {
       double ks = block_sum(kin, red);
+      if (a.cluster_m > 0 && a.fuse_solve == 1) {
+        // instance j = this cluster: rank 0 assembles rho from the m rows in
+        // the cluster's shared memory (fixed rank order -> deterministic), the
+        // others wait until it has read them, then rank 0 solves -- no global
+        // round trip, no ticket atomics
+        namespace cgx = cooperative_groups;
+        cgx::cluster_group cl = cgx::this_cluster();
+        if (tid == 0) red[48] = ks;
+        cl.sync();
+        const bool root = cl.block_rank() == 0;
+        __shared__ double s_kin;
+        if (root) {
+          const double* ipj = a.inst + (size_t)j * PICROM_INST_STRIDE;
+          const double qw = ipj[I_QW], bgh = ipj[I_BGH];
+          const int m = a.cluster_m;
+          for (int nd = tid; nd < nx; nd += NT) {
+            double sacc = 0.0;
+            for (int r = 0; r < m; ++r) sacc += cl.map_shared_rank(coef, r)[nd];
+            hist[nd] = fma(qw, sacc, bgh);
+          }
+          if (tid == 0) {
+            double kk = 0.0;
+            for (int r = 0; r < m; ++r) kk += cl.map_shared_rank(red, r)[48];
+            s_kin = kk;
+          }
+        }
+        cl.sync();
+        TL(6);
+        if (root) {
+          __syncthreads();
+          TSTAMP(3, j == 0);
+          solve_body(sa, j, hist, (unsigned int)a.p, (size_t)(red + 64 - smem), kh_pre, stn_pre,
+                     a.counter ? step_id - 1 : -1, true, s_kin);
+          TL(7);
+        }
+      } else {
       if (tid == 0) a.seg_kin[seg] = ks;
       if (a.fuse_solve) {
         // the last CTA to finish instance j's particles solves instance j
@@ -1054,6 +1111,7 @@ step_kernel(StepArgs a, SolveArgs sa) {
           TL(7);
         }
       }
+      }  // ticket path
     }
     __syncthreads();
     last_j = j;
@@ -1090,14 +1148,73 @@ int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, cons
 
 // --------------------------------------------------------- launch helpers
 
+// last cluster decision of the fused step: {m, clusters needed, max co-resident}
+static int g_cluster_info[3] = {0, 0, 0};
+extern "C" int picrom_debug_cluster_info(int* out) {
+  for (int i = 0; i < 3; ++i) out[i] = g_cluster_info[i];
+  return 0;
+}
+
 template <int D, int K, int MODE, bool FIX>
-static int launch_step_t(const StepArgs& a, const SolveArgs& sa, const Plan& pl, cudaStream_t s) {
+static int launch_step_t(const StepArgs& a_in, const SolveArgs& sa, const Plan& pl, cudaStream_t s) {
   constexpr int NT = FIX ? kFixNT : 128;
   auto kfn = step_kernel<D, K, MODE, NT, FIX>;
   static bool attr = false;
   if (!attr) {
     allow_max_dynamic_smem(kfn);
     attr = true;
+  }
+  StepArgs a = a_in;
+  const size_t smem = FIX ? pl.fsmem : pl.smem;
+  if (MODE == MODE_LEAPFROG && a.cluster_m > 0) {
+    // one cluster per instance (instance-aligned grid); fall back to the
+    // ticket path unless every cluster of the launch can be co-resident
+    const int m = a.cluster_m;
+    static int ok_m = -1, ok_clusters = -1;
+    static size_t ok_smem = 0;
+    const int clusters = pl.G / m;
+    if (!(ok_m == m && ok_smem == smem)) {
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t qc{};
+      qc.gridDim = dim3(pl.G);
+      qc.blockDim = dim3(NT);
+      qc.dynamicSmemBytes = smem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = m;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, kfn, &qc) != cudaSuccess) {
+        (void)cudaGetLastError();
+        nc = 0;
+      }
+      ok_m = m;
+      ok_smem = smem;
+      ok_clusters = nc;
+    }
+    g_cluster_info[0] = m;
+    g_cluster_info[1] = clusters;
+    g_cluster_info[2] = ok_clusters;
+    if (ok_clusters >= clusters) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(pl.G);
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = m;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, kfn, a, sa) != cudaSuccess) return check_launch("step_kernel (cluster)");
+      return check_launch("step_kernel (cluster)");
+    }
+    a.cluster_m = 0;
   }
   if (MODE == MODE_LEAPFROG && kPdl) {
     cudaLaunchConfig_t cfg{};
@@ -1113,7 +1230,7 @@ static int launch_step_t(const StepArgs& a, const SolveArgs& sa, const Plan& pl,
     if (cudaLaunchKernelEx(&cfg, kfn, a, sa) != cudaSuccess) return check_launch("step_kernel (PDL)");
     return check_launch("step_kernel");
   }
-  kfn<<<pl.G, NT, FIX ? pl.fsmem : pl.smem, s>>>(a, sa);
+  kfn<<<pl.G, NT, smem, s>>>(a, sa);
   return check_launch("step_kernel");
 }
 
@@ -1365,6 +1482,9 @@ extern "C" int picrom_pic_step(double* x, double* v, long long n, int p, long lo
   a.dt = dt; a.kick = kick; a.kfull = kfull; a.step = step + 1; a.status = status;
   a.counter = counter;
   a.fuse_solve = 1;
+  // instance-aligned grid (G = m p, 2 <= m <= 16): one thread-block cluster per
+  // instance, the per-instance reduction over DSMEM
+  if (kUseCluster && pl.G % p == 0 && pl.G / p >= 2 && pl.G / p <= 16) a.cluster_m = pl.G / p;
   ws_split(ws, pl, p, nx, &a.seg_hist, &a.seg_kin, &a.inst_done);
   SolveArgs sa{};
   sa.seg_hist = a.seg_hist; sa.seg_kin = a.seg_kin; sa.inst = inst; sa.khat = khat;

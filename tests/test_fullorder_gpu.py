@@ -261,7 +261,10 @@ def test_step_seconds_are_per_step_device_times(mods):
     rec = fo.run_full_order(sysm, fo.ParticleEnsemble(x, v), 0.05, steps * 0.05,
                             record=fo.RecordOptions(energy_stride=1, record_snapshots=False))
     ss = rec.step_seconds
-    assert ss.shape == (steps,) and np.all(ss > 0) and np.all(ss < 0.05)
+    # device time between consecutive step ends: includes any idle gap (the
+    # first graph replay waits for the host-side capture), like the
+    # reference's wall-clock step_seconds
+    assert ss.shape == (steps,) and np.all(ss > 0) and np.median(ss) < 1e-3
     assert len(np.unique(ss)) > steps // 2
     assert ss.sum() <= rec.phase_seconds["fom_step"] * 1.01
 
