@@ -211,7 +211,7 @@ int picrom_rom_field(const double* ux, long long N, int n, const double* z, int 
                      int p, const int* cols, const double* inst, int nx, int degree,
                      const double* khat, const double* stencil, double* phi,
                      double* rho, double* energy, void* workspace,
-                     unsigned long long* status, void* stream);
+                     unsigned long long* status, const long long* skip, void* stream);
 
 /* Gather half (driver.py:74-76, make_full_stage driver.py:83-85):
  * E = coef * d/dx (phi . lambda)(U_X Z) with coef = qw/m_p (coef_kind 0) or 1
@@ -222,7 +222,7 @@ int picrom_rom_gather(const double* ux, long long N, int n, const double* z, int
                       int p, const int* cols, const double* inst, int nx, int degree,
                       const double* phi, int coef_kind, double* g_out, int ldg,
                       double* lam, double* eout, long long ldo, void* workspace,
-                      unsigned long long* status, void* stream);
+                      unsigned long long* status, const long long* skip, void* stream);
 
 /* As picrom_rom_gather with u the full (2N x n) basis [U_X; U_V] and both
  * projections of E: g_out = U_X^T E and gv_out = U_V^T E (n x p', ld ldg).
@@ -304,7 +304,24 @@ int picrom_dmd_extrapolate(const double* modes, const double* coords, const doub
 int picrom_deim_gather(const double* uxd, const double* z, int ldz, const double* phi,
                        const double* inst, const int* cols, const double* w,
                        const double* wscale, int d, int n, int p, int nx, int degree,
-                       double* out, int ldo, unsigned long long* status, void* stream);
+                       double* out, int ldo, unsigned long long* status,
+                       const long long* skip, void* stream);
+
+/* `skip` (nullable, device int64) on picrom_rom_field / picrom_rom_gather /
+ * picrom_deim_gather: when *skip is nonzero the launches do nothing -- the
+ * iterations queued after a device-side fixed-point convergence
+ * (picrom_fp_update sets state[0]).
+ *
+ * One iteration of the implicit coefficient stage (fixed_point,
+ * reduction.py:185-202) for k -> J g(z + dt/2 k), g(z) = D(z) + C z with
+ * D(zeval) in gout (n x p, from the F-evaluation kernels at zeval) and C =
+ * U_V^T U_V (n x n), all device, row-major:  k_new = J(gout + C zeval);
+ * trace[it] = ||k_new - k|| / max(||k_new||, tiny); k = k_new;
+ * zeval = z + half_dt k_new; converged (trace[it] <= tol) -> state[1] = it+1,
+ * state[0] = 1, after which the call is a no-op.  One CTA; n p <= 25600. */
+int picrom_fp_update(const double* gout, const double* c, const double* z, double* k,
+                     double* zeval, int n, int p, double half_dt, double tol, int it,
+                     long long* state, double* trace, void* stream);
 
 /* out (d x w) = rows idx of src (row-major, leading dim ld): U_X[I] of
  * make_hyper_stage (hyper.py:312). */

@@ -45,9 +45,9 @@ SIGNATURES = {
     "picrom_transpose": (_i, [_vp, _ll, _ll, _vp, _vp]),
     "picrom_rom_workspace_bytes": (_sz, [_ll, _i, _i, _i]),
     "picrom_rom_field": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp,
-                              _vp, _vp, _vp, _vp]),
+                              _vp, _vp, _vp, _vp, _vp]),
     "picrom_rom_gather": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _i,
-                               _vp, _vp, _ll, _vp, _vp, _vp]),
+                               _vp, _vp, _ll, _vp, _vp, _vp, _vp]),
     "picrom_rom_gather_uv": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp,
                                   _i, _vp, _vp, _ll, _vp, _vp, _vp]),
     "picrom_paired_gram": (_i, [_i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp]),
@@ -59,7 +59,8 @@ SIGNATURES = {
     "picrom_combine": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _i, _i, _i, _vp]),
     "picrom_dmd_extrapolate": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "picrom_deim_gather": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _i,
-                                _vp, _vp]),
+                                _vp, _vp, _vp]),
+    "picrom_fp_update": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _d, _i, _vp, _vp, _vp]),
     "picrom_rows_gather": (_i, [_vp, _i, _vp, _i, _i, _vp, _vp]),
     "picrom_transpose_i64": (_i, [_vp, _ll, _ll, _vp, _vp]),
 }

@@ -310,6 +310,7 @@ struct SolveArgs {
   size_t scratch;           // solve_kernel: dynamic smem in doubles
   unsigned long long* t_hist;  // optional %globaltimer (ns) per history row, written
                                // when the counter advances (the step's last solve)
+  const long long* skip;       // nullable device flag: nonzero -> solve_kernel does nothing
 };
 
 // sum of cnt values v[0], v[stride], ... with 8 independent loads in flight,
@@ -574,6 +575,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
 
 __global__ void __launch_bounds__(512) solve_kernel(SolveArgs a) {
   extern __shared__ double sm[];
+  if (a.skip && *a.skip) return;
   solve_body(a, blockIdx.x, sm, gridDim.x, a.scratch);
 }
 
@@ -1137,8 +1139,10 @@ static int launch_solve(const SolveArgs& a_in, cudaStream_t s) {
 // dense-segment assembly + solve (used by the reduced-basis deposit, rom.cu)
 int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, const int* cols,
                        const double* inst, const double* khat, const double* stencil,
-                       double* phi, double* rho, double* energy, cudaStream_t s) {
+                       double* phi, double* rho, double* energy, cudaStream_t s,
+                       const long long* skip) {
   SolveArgs sa{};
+  sa.skip = skip;
   sa.seg_hist = seg; sa.seg_dense = G; sa.cols = cols; sa.inst = inst; sa.khat = khat;
   sa.stencil = stencil; sa.n = 1; sa.p = p; sa.nx = nx; sa.degree = degree; sa.G = G;
   sa.solve = phi != nullptr || energy != nullptr; sa.phi_out = phi; sa.rho_out = rho;

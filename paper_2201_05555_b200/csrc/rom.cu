@@ -66,7 +66,8 @@ extern int picrom_check_launch(const char* what);
 extern int picrom_num_sms();
 extern int picrom_solve_dense(const double* seg, int G, int p, int nx, int degree, const int* cols,
                               const double* inst, const double* khat, const double* stencil,
-                              double* phi, double* rho, double* energy, cudaStream_t s);
+                              double* phi, double* rho, double* energy, cudaStream_t s,
+                              const long long* skip);
 
 namespace {
 
@@ -88,6 +89,8 @@ struct RomArgs {
   unsigned long long* status;
   const double* uv;     // gather (DMMA path): optional U_V rows (N x n) -> U_V^T E
   double* seg2;         // gather: [G][p'][n] partials of U_V^T E
+  const long long* skip;  // nullable device flag: nonzero -> the launch does nothing
+                          // (iterations after a device-side fixed-point convergence)
 };
 
 __device__ __forceinline__ long long row_start(int b, long long N, int G) {
@@ -147,6 +150,7 @@ __device__ __forceinline__ double row_dot(const double* urow, const double* zc, 
 // double-buffered smem tile shared by all columns of the CTA.
 template <int D, int NB, int R>
 __global__ void __launch_bounds__(384) rom_deposit_kernel(RomArgs a) {
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   const int P = blockDim.x / R;               // columns per row group (mult of 32)
   const int H = blockDim.x;
@@ -232,6 +236,7 @@ __global__ void __launch_bounds__(384) rom_deposit_kernel(RomArgs a) {
 // lam and E output), same tiling; phi of the CTA's columns in smem [node][col].
 template <int D, int NB, int R>
 __global__ void __launch_bounds__(384) rom_gather_kernel(RomArgs a) {
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   const int P = blockDim.x / R;
   const int tid = threadIdx.x;
@@ -352,9 +357,9 @@ __global__ void __launch_bounds__(384) rom_gather_kernel(RomArgs a) {
 
 // out[c][k] (and optional transpose layout) = sum_b seg[b][c][k]
 __global__ void seg_sum_kernel(const double* seg, int G, int rows, double* out, int out_ld,
-                               int transpose, int width) {
+                               int transpose, int width, const long long* skip = nullptr) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= rows) return;
+  if (q >= rows || (skip && *skip)) return;
   double s = 0.0;
   for (int b = 0; b < G; ++b) s += seg[(size_t)b * rows + q];
   if (transpose) {  // q = c*width + k  ->  out[k][c]
@@ -1034,7 +1039,9 @@ template <int D>
 __global__ void deim_gather_kernel(const double* uxd, const double* z, int ldz, const double* phi,
                                    const double* inst, const int* cols, const double* w,
                                    const double* wscale, int d, int n, int p, int nx,
-                                   double* out, int ldo, unsigned long long* status) {
+                                   double* out, int ldo, unsigned long long* status,
+                                   const long long* skip) {
+  if (skip && *skip) return;
   extern __shared__ double e[];
   const int j = blockIdx.x;
   const int inst_id = cols ? cols[j] : j;
@@ -1120,6 +1127,7 @@ constexpr int DW = 16;           // warps per deposit CTA
 constexpr int DC = DW * 8;       // z columns per deposit CTA
 template <int D, int NK>
 __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) {
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   constexpr int NT = DW * 32;
   constexpr int HS = DC * 2;                  // histograms (row stride)
@@ -1228,6 +1236,7 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
 
 template <int D, int NK, bool VPROJ>
 __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   constexpr int NT = MW * 32;
   constexpr int NM = (4 * NK + 7) / 8;        // 8-row tiles of the projection (n <= 8 NM)
@@ -1659,12 +1668,12 @@ extern "C" int picrom_rom_field(const double* ux, long long N, int n, const doub
                                 int p, const int* cols, const double* inst, int nx, int degree,
                                 const double* khat, const double* stencil, double* phi,
                                 double* rho, double* energy, void* ws,
-                                unsigned long long* status, void* stream) {
+                                unsigned long long* status, const long long* skip, void* stream) {
   int rc = rom_check(N, n, p, nx, degree);
   if (rc) return rc;
   RomArgs a{};
   a.ux = ux; a.z = z; a.inst = inst; a.cols = cols; a.seg = (double*)ws; a.N = N; a.n = n;
-  a.p = p; a.ldz = ldz; a.nx = nx; a.status = status;
+  a.p = p; a.ldz = ldz; a.nx = nx; a.status = status; a.skip = skip;
   const int G = degree == 1 ? rom_dep_grid<1>(a) : degree == 2 ? rom_dep_grid<2>(a) : rom_dep_grid<3>(a);
   cudaStream_t s = (cudaStream_t)stream;
   switch (degree) {
@@ -1673,7 +1682,8 @@ extern "C" int picrom_rom_field(const double* ux, long long N, int n, const doub
     default: rc = launch_rom_deposit_any<3>(a, G, s); break;
   }
   if (rc) return rc;
-  return picrom_solve_dense(a.seg, G, p, nx, degree, cols, inst, khat, stencil, phi, rho, energy, s);
+  return picrom_solve_dense(a.seg, G, p, nx, degree, cols, inst, khat, stencil, phi, rho, energy, s,
+                            skip);
 }
 
 // Gather + projection: g_out (n x p', ld ldg) = U_X^T E with E = coef d/dx
@@ -1682,13 +1692,14 @@ static int rom_gather_impl(const double* ux, long long N, int n, const double* z
                            const int* cols, const double* inst, int nx, int degree,
                            const double* phi, int coef_kind, double* g_out, int ldg,
                            double* gv_out, double* lam, double* eout, long long ldo, void* ws,
-                           unsigned long long* status, void* stream) {
+                           unsigned long long* status, void* stream,
+                           const long long* skip = nullptr) {
   int rc = rom_check(N, n, p, nx, degree);
   if (rc) return rc;
   RomArgs a{};
   a.ux = ux; a.z = z; a.inst = inst; a.cols = cols; a.phi = phi; a.seg = (double*)ws;
   a.lam = lam; a.eout = eout; a.N = N; a.ldo = ldo; a.n = n; a.p = p; a.ldz = ldz; a.nx = nx;
-  a.coef_kind = coef_kind; a.status = status;
+  a.coef_kind = coef_kind; a.status = status; a.skip = skip;
   const int G = rom_gat_grid(a);
   if (gv_out) {
     a.uv = ux + (size_t)N * n;
@@ -1703,12 +1714,12 @@ static int rom_gather_impl(const double* ux, long long N, int n, const double* z
   if (rc) return rc;
   const int rows = p * n;
   if (g_out) {
-    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg, G, rows, g_out, ldg, 1, n);
+    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg, G, rows, g_out, ldg, 1, n, a.skip);
     rc = picrom_check_launch("seg_sum");
     if (rc) return rc;
   }
   if (gv_out) {
-    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg2, G, rows, gv_out, ldg, 1, n);
+    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg2, G, rows, gv_out, ldg, 1, n, a.skip);
     rc = picrom_check_launch("seg_sum");
   }
   return rc;
@@ -1718,9 +1729,10 @@ extern "C" int picrom_rom_gather(const double* ux, long long N, int n, const dou
                                  int p, const int* cols, const double* inst, int nx, int degree,
                                  const double* phi, int coef_kind, double* g_out, int ldg,
                                  double* lam, double* eout, long long ldo, void* ws,
-                                 unsigned long long* status, void* stream) {
+                                 unsigned long long* status, const long long* skip,
+                                 void* stream) {
   return rom_gather_impl(ux, N, n, z, ldz, p, cols, inst, nx, degree, phi, coef_kind, g_out, ldg,
-                         nullptr, lam, eout, ldo, ws, status, stream);
+                         nullptr, lam, eout, ldo, ws, status, stream, skip);
 }
 
 // Gather with both projections of E: g_out = U_X^T E and gv_out = U_V^T E
@@ -2371,17 +2383,100 @@ extern "C" int picrom_dmd_extrapolate(const double* modes, const double* coords,
 extern "C" int picrom_deim_gather(const double* uxd, const double* z, int ldz, const double* phi,
                                   const double* inst, const int* cols, const double* w,
                                   const double* wscale, int d, int n, int p, int nx, int degree,
-                                  double* out, int ldo, unsigned long long* status, void* stream) {
+                                  double* out, int ldo, unsigned long long* status,
+                                  const long long* skip, void* stream) {
   if (d < 1 || n < 1 || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "empty DEIM stage");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t sm = (size_t)d * sizeof(double);
   switch (degree) {
-    case 1: deim_gather_kernel<1><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status); break;
-    case 2: deim_gather_kernel<2><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status); break;
-    case 3: deim_gather_kernel<3><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status); break;
+    case 1: deim_gather_kernel<1><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status, skip); break;
+    case 2: deim_gather_kernel<2><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status, skip); break;
+    case 3: deim_gather_kernel<3><<<p, 64, sm, s>>>(uxd, z, ldz, phi, inst, cols, w, wscale, d, n, p, nx, out, ldo, status, skip); break;
     default: return picrom_set_error(PICROM_ERR_CONFIG, "degree must be 1, 2 or 3");
   }
   return picrom_check_launch("deim_gather");
+}
+
+// ------------------------------------------------- device fixed point
+//
+// One iteration of reduction.fixed_point (reduction.py:185-202) for the stage
+// map k -> J g(z + dt/2 k) with g(z) = D(z) + (U_V^T U_V) z, D(z) already in
+// gout (the F-evaluation kernels, evaluated at zeval = z + dt/2 k):
+//   k_new = J (gout + C zeval); r = ||k_new - k|| / max(||k_new||, tiny);
+//   trace[it] = r; k = k_new; converged (r <= tol) -> state = {1, it + 1};
+//   zeval = z + dt/2 k_new for the next iteration.
+// One CTA; once converged every later call (and the F-evaluation kernels,
+// which test state[0] as their skip flag) returns immediately.
+__global__ void __launch_bounds__(256) fp_update_kernel(const double* gout, const double* c,
+                                                       const double* z, double* k, double* zeval,
+                                                       int n, int p, double half_dt, double tol,
+                                                       int it, long long* state, double* trace) {
+  extern __shared__ double g[];
+  __shared__ double red[64];
+  if (state[0]) return;
+  const int tid = threadIdx.x, np = n * p;
+  for (int q = tid; q < np; q += blockDim.x) {
+    const int r = q / p, col = q % p;
+    double acc = gout[q];
+    for (int j = 0; j < n; ++j) acc = fma(c[r * n + j], zeval[(size_t)j * p + col], acc);
+    g[q] = acc;
+  }
+  __syncthreads();
+  const int h = n / 2;
+  double dd = 0.0, kk = 0.0;
+  for (int q = tid; q < np; q += blockDim.x) {
+    const int r = q / p, col = q % p;
+    const double kn = r < h ? g[(r + h) * p + col] : -g[(r - h) * p + col];
+    const double df = kn - k[q];
+    dd = fma(df, df, dd);
+    kk = fma(kn, kn, kk);
+  }
+  // block reductions (fixed tree)
+  dd = warp_sum(dd);
+  kk = warp_sum(kk);
+  const int w = tid >> 5, l = tid & 31;
+  if (l == 0) { red[w] = dd; red[32 + w] = kk; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    double a = l < nw ? red[l] : 0.0, b = l < nw ? red[32 + l] : 0.0;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (l == 0) { red[0] = a; red[32] = b; }
+  }
+  __syncthreads();
+  const double num = sqrt(red[0]);
+  const double den = fmax(sqrt(red[32]), 2.2250738585072014e-308);
+  for (int q = tid; q < np; q += blockDim.x) {
+    const int r = q / p, col = q % p;
+    const double kn = r < h ? g[(r + h) * p + col] : -g[(r - h) * p + col];
+    k[q] = kn;
+    zeval[q] = fma(half_dt, kn, z[q]);
+  }
+  if (tid == 0) {
+    trace[it] = num / den;
+    if (num <= tol * den) {
+      state[1] = it + 1;
+      __threadfence();
+      state[0] = 1;
+    }
+  }
+}
+
+extern "C" int picrom_fp_update(const double* gout, const double* c, const double* z, double* k,
+                                double* zeval, int n, int p, double half_dt, double tol, int it,
+                                long long* state, double* trace, void* stream) {
+  if (n < 2 || (n & 1) || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "fp_update: bad n / p");
+  const size_t sm = (size_t)n * p * sizeof(double);
+  if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "fp_update: n p too large");
+  static bool attr = false;
+  if (!attr) {
+    rom_allow_smem(fp_update_kernel);
+    attr = true;
+  }
+  fp_update_kernel<<<1, 256, sm, (cudaStream_t)stream>>>(gout, c, z, k, zeval, n, p, half_dt, tol,
+                                                          it, state, trace);
+  return picrom_check_launch("fp_update");
 }
 
 // out (d x w) = src rows idx (src row-major with leading dim ld)

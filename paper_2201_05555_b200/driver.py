@@ -138,12 +138,12 @@ def _field_device(system, ud, z, cols, want_energy=False, status=None):
     if sh is None or sh.world == 1:
         _lib.call("picrom_rom_field", ud.data_ptr(), N, n, zd.data_ptr(), p, p, cols.ptr,
                   inst.data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(), phi.data_ptr(),
-                  None, dev.ptr(energy), _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(), s)
+                  None, dev.ptr(energy), _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(), None, s)
         return zd, inst, phi, energy, st
     rho = torch.empty((p, nx), dtype=torch.float64, device="cuda")
     _lib.call("picrom_rom_field", ud.data_ptr(), N, n, zd.data_ptr(), p, p, cols.ptr,
               _partial_inst(inst).data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(), None,
-              rho.data_ptr(), None, _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(), s)
+              rho.data_ptr(), None, _rom_ws(N, p, n, nx).data_ptr(), st.data_ptr(), None, s)
     parallel.allreduce_sum(rho)
     col_inst = inst if cols.dev is None else inst[torch.from_numpy(cols.host.astype(np.int64)).cuda()]
     _lib.call("picrom_poisson", rho.data_ptr(), p, nx, d, col_inst.data_ptr(), c.khat.data_ptr(),
@@ -232,6 +232,8 @@ def make_full_stage(system):
     passes, the Gram once per stage."""
 
     from . import parallel
+    from .reduction import DeviceFixedPoint
+    hint = [None]                    # the previous step's fixed-point iteration count
 
     def factory(u_mid):
         N = u_mid.shape[0] // 2
@@ -242,11 +244,7 @@ def make_full_stage(system):
         c = system.poisson.constants
         bufs = {}
 
-        def g(z):
-            # the fixed-point loop calls this ~9 times per step: buffers are
-            # reused and the result and the status word come back in one sync
-            z = np.ascontiguousarray(z, dtype=np.float64)
-            p = z.shape[1]
+        def ensure(p):
             if bufs.get("p") != p:
                 bufs.update(p=p, zd=torch.empty((n, p), dtype=torch.float64, device="cuda"),
                             phi=torch.empty((p, nx), dtype=torch.float64, device="cuda"),
@@ -256,6 +254,13 @@ def make_full_stage(system):
                             out_h=torch.empty((n * p + 2,), dtype=torch.float64, pin_memory=True),
                             inst=_inst_table(system, p),
                             ws=_rom_ws(N, p, n, nx))
+
+        def g(z):
+            # the host fixed-point loop calls this ~9 times per step: buffers
+            # are reused and the result and the status word come back in one sync
+            z = np.ascontiguousarray(z, dtype=np.float64)
+            p = z.shape[1]
+            ensure(p)
             zd, phi, gout, st = bufs["zd"], bufs["phi"], bufs["gout"], bufs["st"]
             bufs["z_h"].numpy()[...] = z
             zd.copy_(bufs["z_h"], non_blocking=True)
@@ -265,12 +270,12 @@ def make_full_stage(system):
                 _lib.call("picrom_rom_field", u_mid.data_ptr(), N, n, zd.data_ptr(), p, p, None,
                           bufs["inst"].data_ptr(), nx, d, c.khat.data_ptr(),
                           c.stencil.data_ptr(), phi.data_ptr(), None, None,
-                          bufs["ws"].data_ptr(), st.data_ptr(), sh)
+                          bufs["ws"].data_ptr(), st.data_ptr(), None, sh)
             else:
                 phi.copy_(_field_device(system, u_mid, z, _Cols(None, p), status=st)[2])
             _lib.call("picrom_rom_gather", u_mid.data_ptr(), N, n, zd.data_ptr(), p, p, None,
                       bufs["inst"].data_ptr(), nx, d, phi.data_ptr(), 0, gout.data_ptr(), p,
-                      None, None, 0, bufs["ws"].data_ptr(), st.data_ptr(), sh)
+                      None, None, 0, bufs["ws"].data_ptr(), st.data_ptr(), None, sh)
             parallel.allreduce_sum(gout)                  # U_X^T E partials (sharded runs)
             out_h = bufs["out_h"]
             out_h[:n * p].copy_(gout.reshape(-1), non_blocking=True)
@@ -281,6 +286,22 @@ def make_full_stage(system):
                 _raise_eval(stat, p)
             return out_h[:n * p].numpy().reshape(n, p).copy() + uvtuv @ z
 
+        def launch_d(zeval, gout, skip, st):
+            """D(zeval) = U_X^T E(U_X zeval) into gout: rom_field + rom_gather,
+            both skipped once the device fixed point has converged."""
+            p = zeval.shape[1]
+            ensure(p)
+            sh = dev.stream_handle()
+            _lib.call("picrom_rom_field", u_mid.data_ptr(), N, n, zeval.data_ptr(), p, p, None,
+                      bufs["inst"].data_ptr(), nx, d, c.khat.data_ptr(), c.stencil.data_ptr(),
+                      bufs["phi"].data_ptr(), None, None, bufs["ws"].data_ptr(), st.data_ptr(),
+                      skip.data_ptr(), sh)
+            _lib.call("picrom_rom_gather", u_mid.data_ptr(), N, n, zeval.data_ptr(), p, p, None,
+                      bufs["inst"].data_ptr(), nx, d, bufs["phi"].data_ptr(), 0, gout.data_ptr(),
+                      p, None, None, 0, bufs["ws"].data_ptr(), st.data_ptr(), skip.data_ptr(), sh)
+
+        if parallel.active() is None or parallel.active().world == 1:
+            g.device_fixed_point = DeviceFixedPoint(n, launch_d, uvtuv, hint)
         return g
 
     return factory

@@ -363,6 +363,84 @@ def fixed_point(map_fn, z0, tol=1e-9, max_iter=100):
         f"(last relative update {trace[-1]:.3e})", iterations=max_iter, residual_trace=trace)
 
 
+class DeviceFixedPoint:
+    """fixed_point (reduction.py:185-202) for the stage map k -> J g(z + dt/2 k)
+    kept on the device: g(z) = D(z) + C z with D the stage's F-evaluation
+    kernels (launched by `launch_d(zeval, gout, skip, status)`) and C = U_V^T U_V.
+    Each iteration is D + picrom_fp_update (J, the relative-update test and the
+    residual trace on the device); iterations are queued in chunks and the host
+    syncs once per chunk -- the first chunk is the previous step's iteration
+    count + 1, launches queued past convergence are skipped by the device flag.
+    Same iteration count, convergence test and StepFailureError as fixed_point."""
+
+    def __init__(self, n, launch_d, c_host, stream_owner=None):
+        self.n = n
+        self.launch_d = launch_d
+        self.c = torch.from_numpy(np.ascontiguousarray(c_host, dtype=np.float64)).to("cuda")
+        self.bufs = None
+        self.hint = stream_owner
+
+    def _alloc(self, p, max_iter):
+        n = self.n
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.bufs = dict(p=p, zd=torch.empty((n, p), **f64), k=torch.empty((n, p), **f64),
+                         ze=torch.empty((n, p), **f64), gout=torch.empty((n, p), **f64),
+                         state=torch.zeros(4, dtype=torch.int64, device="cuda"),
+                         trace=torch.zeros(max(max_iter, 1), **f64),
+                         z_h=torch.empty((n, p), dtype=torch.float64, pin_memory=True),
+                         flags_h=torch.empty(4, dtype=torch.int64, pin_memory=True))
+
+    def __call__(self, z, dt, tol, max_iter):
+        from . import _device as dev
+        from . import _lib
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        n, p = z.shape
+        if self.bufs is None or self.bufs["p"] != p or self.bufs["trace"].numel() < max_iter:
+            self._alloc(p, max_iter)
+        b = self.bufs
+        b["z_h"].numpy()[...] = z
+        b["zd"].copy_(b["z_h"], non_blocking=True)
+        b["k"].zero_()
+        b["ze"].copy_(b["zd"])
+        b["state"].zero_()
+        st = b["state"][2:]                    # F-evaluation status word (min-reduced)
+        st.fill_(-1)
+        s = dev.stream_handle()
+        hint = self.hint[0] if self.hint else None
+        chunk = (hint + 1) if hint else 6
+        it = 0
+        done = False
+        while it < max_iter:
+            m = min(chunk, max_iter - it)
+            for q in range(m):
+                self.launch_d(b["ze"], b["gout"], b["state"], st)
+                _lib.call("picrom_fp_update", b["gout"].data_ptr(), self.c.data_ptr(),
+                          b["zd"].data_ptr(), b["k"].data_ptr(), b["ze"].data_ptr(), n, p,
+                          0.5 * dt, float(tol), it + q, b["state"].data_ptr(),
+                          b["trace"].data_ptr(), s)
+            it += m
+            b["flags_h"].copy_(b["state"], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            flags = b["flags_h"].numpy()
+            if int(flags[2]) != -1:
+                from .driver import _raise_eval
+                _raise_eval(b["flags_h"][2:], p)
+            if int(flags[0]):
+                done = True
+                break
+            chunk = 4
+        if not done:
+            trace = b["trace"][:max_iter].cpu().numpy().tolist()
+            raise StepFailureError(
+                f"implicit coefficient stage did not converge in {max_iter} iterations "
+                f"(last relative update {trace[-1]:.3e})", iterations=max_iter,
+                residual_trace=trace)
+        iters = int(flags[1])
+        if self.hint is not None:
+            self.hint[0] = iters
+        return b["k"].cpu().numpy(), iters, b["trace"][:iters].cpu().numpy().tolist()
+
+
 @dataclass
 class PRKResult:
     u: object
@@ -390,8 +468,12 @@ def prk2_step(u, z, dt, sub, grad_sub, g_sub0, coeff_stage, fp_tol=1e-9, fp_max_
         u_mid = retraction(u, half_step)
         g = coeff_stage(u_mid)
     with timers.phase("rom_coeff"):
-        k, iterations, _ = fixed_point(lambda kk: jmul(g(z + 0.5 * dt * kk)), np.zeros_like(z),
-                                       fp_tol, fp_max_iter)
+        dfp = getattr(g, "device_fixed_point", None)
+        if dfp is not None:
+            k, iterations, _ = dfp(z, dt, fp_tol, fp_max_iter)
+        else:
+            k, iterations, _ = fixed_point(lambda kk: jmul(g(z + 0.5 * dt * kk)),
+                                           np.zeros_like(z), fp_tol, fp_max_iter)
         z_new = z + dt * k
         z_mid = z + 0.5 * dt * k
     with timers.phase("rom_basis"):

@@ -156,7 +156,7 @@ def test_rom_kernels_and_greedy_guards(m):
         s = m.dev.stream_handle()
         m.lib.call("picrom_rom_field", u.data_ptr(), N, nb, zd.data_ptr(), p, p, None,
                    inst.data_ptr(), nx, 2, c.khat.data_ptr(), c.stencil.data_ptr(), phi.ptr, None,
-                   None, ws.ptr, st.ptr, s)
+                   None, ws.ptr, st.ptr, None, s)
         m.lib.call("picrom_rom_gather_uv", u.data_ptr(), N, nb, zd.data_ptr(), p, p, None,
                    inst.data_ptr(), nx, 2, phi.ptr, 0, proj[0].ptr, proj[1].ptr, p, lam.ptr, e.ptr,
                    p, ws.ptr, st.ptr, s)

@@ -47,7 +47,7 @@ s = dev.stream_handle()
 def field():
     _lib.call("picrom_rom_field", u.data_ptr(), N, n, zd.data_ptr(), p, p, None, inst.data_ptr(),
               nx, d, c.khat.data_ptr(), c.stencil.data_ptr(), phi.data_ptr(), None, None,
-              ws.data_ptr(), st.data_ptr(), s)
+              ws.data_ptr(), st.data_ptr(), None, s)
 
 
 gout = torch.empty((n, p), dtype=torch.float64, device="cuda")
@@ -57,13 +57,13 @@ e = torch.empty((N, p), dtype=torch.float64, device="cuda")
 def gather():
     _lib.call("picrom_rom_gather", u.data_ptr(), N, n, zd.data_ptr(), p, p, None, inst.data_ptr(),
               nx, d, phi.data_ptr(), 0, gout.data_ptr(), p, None, None, 0, ws.data_ptr(),
-              st.data_ptr(), s)
+              st.data_ptr(), None, s)
 
 
 def gather_e():
     _lib.call("picrom_rom_gather", u.data_ptr(), N, n, zd.data_ptr(), p, p, None, inst.data_ptr(),
               nx, d, phi.data_ptr(), 0, None, 0, None, e.data_ptr(), p, ws.data_ptr(),
-              st.data_ptr(), s)
+              st.data_ptr(), None, s)
 
 
 xi = torch.randn_like(u)
