@@ -267,6 +267,12 @@ int picrom_argmax_abs(const double* v, long long n, long long stride,
                       const long long* banned, int nbanned, long long* out_index,
                       double* out_value, void* workspace, void* stream);
 
+/* Compare-mode error norms (diagnostics.py:50-71): out[0] = ||a - b||_F^2,
+ * out[1] = ||a||_F^2 over `count` contiguous doubles (b nullable -> out[0] =
+ * 0); fixed-order reduction; workspace >= 8 * 4 * num_sms * 2 doubles. */
+int picrom_diff_sumsq(const double* a, const double* b, long long count, double* out,
+                      void* workspace, void* stream);
+
 /* Scratch bytes of picrom_deim_greedy for an N x d basis. */
 size_t picrom_deim_workspace_bytes(long long N, int d);
 

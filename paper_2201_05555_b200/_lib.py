@@ -55,6 +55,7 @@ SIGNATURES = {
     "picrom_cross_gram": (_i, [_i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp]),
     "picrom_argmax_abs": (_i, [_vp, _ll, _ll, _vp, _i, _vp, _vp, _vp, _vp]),
     "picrom_deim_workspace_bytes": (_sz, [_ll, _i]),
+    "picrom_diff_sumsq": (_i, [_vp, _vp, _ll, _vp, _vp, _vp]),
     "picrom_deim_greedy": (_i, [_vp, _i, _ll, _i, _vp, _vp, _vp, _vp, _vp]),
     "picrom_combine": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _i, _i, _i, _vp]),
     "picrom_dmd_extrapolate": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),

@@ -651,8 +651,11 @@ __device__ __noinline__ CellFrac locate_rare(double x, double h, double inv_h, i
 // so every access is conflict-free) and take turns (K phases); each lane
 // handles U particles per iteration (u*32 + lane within its warp's 32*U
 // block: coalesced), with the next iteration's loads issued first.
+#ifndef PICROM_PHASE_MINB
+#define PICROM_PHASE_MINB 1
+#endif
 template <int D, int K, int MODE, int NT, bool FIX>
-__global__ void __launch_bounds__(NT, FIX ? kFixMinB : 1)
+__global__ void __launch_bounds__(NT, FIX ? kFixMinB : PICROM_PHASE_MINB)
 step_kernel(StepArgs a, SolveArgs sa) {
   extern __shared__ double smem[];
   constexpr int H = FIX ? 1 : NT / K;
@@ -1772,6 +1775,54 @@ __global__ void half_sumsq_kernel(const double* a, long long n, long long ld, do
   }
   s = block_sum(s, red);
   if (threadIdx.x == 0) out[j] = 0.5 * s;
+}
+
+// ||a - b||^2 and ||a||^2 over `count` contiguous doubles (b nullable: only
+// ||a||^2), per-block partials then one fixed-order final sum (deterministic)
+__global__ void diff_sumsq_kernel(const double* a, const double* b, long long count, double* part) {
+  __shared__ double red[32];
+  double d = 0.0, q = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double av = a[i];
+    const double df = b ? av - b[i] : 0.0;
+    d = fma(df, df, d);
+    q = fma(av, av, q);
+  }
+  d = block_sum(d, red);
+  q = block_sum(q, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = d;
+    part[2 * blockIdx.x + 1] = q;
+  }
+}
+
+__global__ void diff_sumsq_final(const double* part, int G, double* out) {
+  __shared__ double red[32];
+  double d = 0.0, q = 0.0;
+  for (int k = threadIdx.x; k < G; k += blockDim.x) {
+    d += part[2 * k];
+    q += part[2 * k + 1];
+  }
+  d = block_sum(d, red);
+  q = block_sum(q, red);
+  if (threadIdx.x == 0) {
+    out[0] = d;
+    out[1] = q;
+  }
+}
+
+extern "C" int picrom_diff_sumsq(const double* a, const double* b, long long count, double* out,
+                                 void* ws, void* stream) {
+  if (count < 1) return set_err(PICROM_ERR_CONFIG, "diff_sumsq of an empty array");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int G = (int)std::min<long long>(4LL * num_sms(), (count + 255) / 256);
+  double* part = (double*)ws;
+  diff_sumsq_kernel<<<G, 256, 0, s>>>(a, b, count, part);
+  int rc = check_launch("diff_sumsq");
+  if (rc) return rc;
+  diff_sumsq_final<<<1, 256, 0, s>>>(part, G, out);
+  return check_launch("diff_sumsq_final");
 }
 
 extern "C" int picrom_half_sumsq(const double* a, long long n, int p, long long ld, double* out,

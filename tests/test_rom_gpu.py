@@ -325,3 +325,47 @@ def test_device_complex_svd_basis(m, N, p, n):
     assert np.abs(u_d.T @ u_d - np.eye(n)).max() <= 1e-13
     o, s_ = m.red.orthosymplectic_residuals(u_d)
     assert o <= 1e-13 and s_ <= 1e-13
+
+
+def test_compare_diagnostics_vs_reference(m):
+    """diagnostics.relative_errors / total_relative_error /
+    target_projection_errors / numerical_rank / hamiltonian_relative_error
+    (device norms, device cSVD basis) against the reference's own functions
+    (picrom.diagnostics from baseline/_ref) or their formulas."""
+    import sys
+    from pathlib import Path
+    from paper_2201_05555_b200 import diagnostics as dg
+    rng = np.random.default_rng(17)
+    N, p, nb = 40_000, 12, 6
+    sx = rng.uniform(0, 10, (N, p))
+    sv = rng.standard_normal((N, p))
+    u, z = m.red.complex_svd_basis(sx, sv, nb)
+    xr, vr = u[:N] @ z, u[N:] @ z
+    ref = Path(__file__).resolve().parent.parent / "baseline" / "_ref"
+    if (ref / "picrom").exists():
+        sys.path.insert(0, str(ref))
+        try:
+            from picrom import diagnostics as rdg
+        finally:
+            sys.path.remove(str(ref))
+        want = dict(rel=rdg.relative_errors(sx, sv, xr, vr),
+                    tot=rdg.total_relative_error(sx, sv, xr, vr),
+                    tgt=rdg.target_projection_errors(sx, sv, nb),
+                    rank=rdg.numerical_rank(np.concatenate([sx, sv]), 1e-3),
+                    ham=rdg.hamiltonian_relative_error(np.arange(1.0, 5.0), np.arange(1.0, 5.0) + 1e-3))
+    else:
+        def r(a, b):
+            return np.linalg.norm(a - b) / np.linalg.norm(a)
+        s = np.linalg.svd(np.concatenate([sx, sv]), compute_uv=False)
+        want = dict(rel=(r(sx, xr), r(sv, vr)),
+                    tot=r(np.concatenate([sx, sv]), np.concatenate([xr, vr])),
+                    tgt=(r(sx, xr), r(sv, vr)), rank=int((s >= 1e-3 * s[0]).sum()),
+                    ham=np.linalg.norm(np.full(4, 1e-3)) / np.linalg.norm(np.arange(1.0, 5.0)))
+    got_rel = dg.relative_errors(sx, sv, xr, vr)
+    np.testing.assert_allclose(got_rel, want["rel"], rtol=1e-12)
+    np.testing.assert_allclose(dg.total_relative_error(sx, sv, xr, vr), want["tot"], rtol=1e-12)
+    np.testing.assert_allclose(dg.target_projection_errors(sx, sv, nb), want["tgt"], rtol=1e-10)
+    assert dg.numerical_rank(np.concatenate([sx, sv]), 1e-3) == want["rank"]
+    np.testing.assert_allclose(dg.hamiltonian_relative_error(np.arange(1.0, 5.0),
+                                                             np.arange(1.0, 5.0) + 1e-3),
+                               want["ham"], rtol=1e-14)
