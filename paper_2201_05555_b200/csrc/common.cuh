@@ -88,6 +88,29 @@ __device__ __forceinline__ void locate_fast(double x, double h, double inv_h, in
   i0 = __double2loint(t) & mask;
 }
 
+// locate() for a position already divided by h: the reduced-basis kernels
+// reconstruct s = U_X (z / h) directly (one DMMA chain, no division), so only
+// the floor remains -- by the 1.5*2^52 add; `rare` = |s| >= 2^51, non-finite,
+// or non-power-of-two nx (mask < 0), handled by locate_scaled_exact().
+__device__ __forceinline__ void locate_scaled(double s, int mask, int& i0, double& frac,
+                                              bool& rare) {
+  constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52
+  const double t = __dadd_rd(s, kMagic);
+  const double c = __dsub_rn(t, kMagic);
+  frac = __dsub_rn(s, c);
+  rare = !(fabs(s) < 0x1p51) || mask < 0;
+  i0 = __double2loint(t) & mask;
+}
+
+__device__ __forceinline__ void locate_scaled_exact(double s, int nx, double inv_nx, int& i0,
+                                                    double& frac) {
+  const double c = floor(s);
+  frac = __dsub_rn(s, c);
+  i0 = cell_mod(c, nx, inv_nx);
+}
+
+__device__ __forceinline__ int pow2_mask(int nx) { return (nx & (nx - 1)) == 0 ? nx - 1 : -1; }
+
 template <int D> struct Spline;
 
 // P1 hat functions -- fem.py:179-200 exactly (weights 1-f, f; gradient -1/h, 1/h)

@@ -1143,7 +1143,7 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
   const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
   const double h = ip[I_H], inv_h = ip[I_INVH];
   const double inv_nx = 1.0 / (double)nx;
-  const int mask = fast_mask(nx, h);
+  const int mask = pow2_mask(nx);
   // histogram of (column, t/2): bank = 2 cl + t/2 mod 16 -- distinct over the
   // 8 lanes of one phase in each half-warp
   const unsigned int hbase = smem_u32(hist + 2 * cl + (t >> 1));
@@ -1151,7 +1151,8 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
 #pragma unroll
   for (int ks = 0; ks < NK; ++ks) {
     const int k = ks * 4 + t;
-    za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+    // Z scaled by 1/h of the column: the reconstruct yields s = x / h directly
+    za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] * inv_h : 0.0;
   }
   for (int q = tid; q < nh * HS; q += NT) hist[q] = 0.0;
   const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
@@ -1188,7 +1189,7 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
         int cell;
         double f;
         bool rare;
-        locate_fast(x, h, inv_h, nx, mask, inv_nx, cell, f, rare);
+        locate_scaled(x, mask, cell, f, rare);
         if (act[e] && rare) {
           if (!isfinite(x)) {
             record_bad(a.status, 0, t0 + row, c, a.p);
@@ -1196,7 +1197,7 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
             cell = 0;
             f = 0.0;
           } else {
-            locate(x, h, inv_h, nx, inv_nx, cell, f);
+            locate_scaled_exact(x, nx, inv_nx, cell, f);
           }
         }
         Spline<D>::weights(f, w[e]);
@@ -1260,12 +1261,13 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
   const double h = ip[I_H], gi = ip[I_INVH], inv_h = gi;
   const double cf = a.coef_kind == 0 ? ip[I_GCOEF] : 1.0;
   const double inv_nx = 1.0 / (double)nx;
-  const int mask = fast_mask(nx, h);
+  const int mask = pow2_mask(nx);
   double za[NK], acc[NM][2], accv[NM][2];
 #pragma unroll
   for (int ks = 0; ks < NK; ++ks) {
     const int k = ks * 4 + t;
-    za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] : 0.0;
+    // Z scaled by 1/h of the column: the reconstruct yields s = x / h directly
+    za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] * inv_h : 0.0;
   }
 #pragma unroll
   for (int mt = 0; mt < NM; ++mt) acc[mt][0] = acc[mt][1] = accv[mt][0] = accv[mt][1] = 0.0;
@@ -1308,13 +1310,13 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
         int cell;
         double f;
         bool rare;
-        locate_fast(x, h, inv_h, nx, mask, inv_nx, cell, f, rare);
+        locate_scaled(x, mask, cell, f, rare);
         if (rare) {
           if (!isfinite(x)) {
             record_bad(a.status, 0, i, c, a.p);
             continue;
           }
-          locate(x, h, inv_h, nx, inv_nx, cell, f);
+          locate_scaled_exact(x, nx, inv_nx, cell, f);
         }
         double pv[D + 1];
 #pragma unroll
