@@ -319,7 +319,7 @@ __device__ __forceinline__ double ordered_sum(const double* v, size_t stride, in
   if (cnt > 16 && cnt <= 32) {   // one round of loads for up to 32 rows (C1: 48 rows, 2 parts)
     double t[32];
 #pragma unroll
-    for (int u = 0; u < 32; ++u) t[u] = u < cnt ? v[(size_t)u * stride] : 0.0;
+    for (int u = 0; u < 32; ++u) t[u] = u < cnt ? __ldcg(v + (size_t)u * stride) : 0.0;
     double acc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = (t[u] + t[u + 8]) + (t[u + 16] + t[u + 24]);
@@ -328,7 +328,7 @@ __device__ __forceinline__ double ordered_sum(const double* v, size_t stride, in
   if (cnt <= 16) {   // common case: every load in flight at once, same sum order
     double t[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) t[u] = u < cnt ? v[(size_t)u * stride] : 0.0;
+    for (int u = 0; u < 16; ++u) t[u] = u < cnt ? __ldcg(v + (size_t)u * stride) : 0.0;
     double acc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = t[u] + t[u + 8];
@@ -338,9 +338,9 @@ __device__ __forceinline__ double ordered_sum(const double* v, size_t stride, in
   int b = 0;
   for (; b + 8 <= cnt; b += 8) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] += v[(size_t)(b + u) * stride];
+    for (int u = 0; u < 8; ++u) acc[u] += __ldcg(v + (size_t)(b + u) * stride);
   }
-  for (int u = 0; b < cnt; ++b, ++u) acc[u] += v[(size_t)b * stride];
+  for (int u = 0; b < cnt; ++b, ++u) acc[u] += __ldcg(v + (size_t)b * stride);
   return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 }
 
@@ -431,7 +431,7 @@ __device__ void solve_body(const SolveArgs& a, int j, double* sm, unsigned int n
     }
     if (kin_out && tid < 32) {                   // warp-parallel, fixed lane tree
       double k = 0.0;
-      for (int b = tid; b < cnt; b += 32) k += a.seg_kin[b_lo + j + b];
+      for (int b = tid; b < cnt; b += 32) k += __ldcg(a.seg_kin + b_lo + j + b);
       k = warp_sum(k);
       if (tid == 0) kin_out[j] = 0.5 * k;
     }
@@ -1108,7 +1108,9 @@ step_kernel(StepArgs a, SolveArgs sa) {
 #else
         if (s_last && a.fuse_solve == 1) {
 #endif
+#ifndef PICROM_SOLVE_NOFENCE
           __threadfence();
+#endif
           TSTAMP(3, j == 0);
           // scratch = the histogram, coefficient and reduction smem (free now)
           solve_body(sa, j, hist, (unsigned int)a.p, (size_t)(red + 64 - smem),
