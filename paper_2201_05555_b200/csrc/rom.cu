@@ -1125,13 +1125,15 @@ __device__ __forceinline__ void recon_block(const double* tile, int rb, int rows
 // buys 16 resident warps instead of 8 (the kernel is latency-bound).
 constexpr int DW = 16;           // warps per deposit CTA
 constexpr int DC = DW * 8;       // z columns per deposit CTA
-template <int D, int NK>
+// EX: n == 4 NK exactly (C3/C4's n = 20): the basis width is a compile-time
+// constant, so the fragment bounds tests fold away and row offsets are shifts
+template <int D, int NK, bool EX>
 __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) {
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   constexpr int NT = DW * 32;
   constexpr int HS = DC * 2;                  // histograms (row stride)
-  const int n = a.n, nx = a.nx, nh = nx + D;
+  const int n = EX ? 4 * NK : a.n, nx = a.nx, nh = nx + D;
   double* ut = smem;                          // [2][TR * n]
   double* hist = ut + 2 * TR * n;             // [nh][HS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1235,26 +1237,30 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
   }
 }
 
-template <int D, int NK, bool VPROJ>
+template <int D, int NK, bool VPROJ, bool EX>
 __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   constexpr int NT = MW * 32;
   constexpr int NM = (4 * NK + 7) / 8;        // 8-row tiles of the projection (n <= 8 NM)
   constexpr int PS = MC + 1;                  // padded phi row (bank spread)
-  const int n = a.n, nx = a.nx;
+  const int n = EX ? 4 * NK : a.n, nx = a.nx;
   double* ut = smem;                          // [2][TR * n]
-  double* phs = ut + 2 * TR * n;              // [nx][PS]
-  double* vt = phs + nx * PS;                 // [2][TR * n] U_V rows (VPROJ)
+  // phi with D periodic ghost rows on each side: row r holds node (r - D) mod nx,
+  // so a particle's nodes cell + OFF + m need no wrap
+  double* phs = ut + 2 * TR * n;              // [nx + 2D][PS]
+  double* vt = phs + (nx + 6) * PS;           // [2][TR * n] U_V rows (VPROJ)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int cl = warp * 8 + g;
   const int c = blockIdx.y * MC + cl;
   const bool active = c < a.p;
   const int P_used = min(MC, a.p - blockIdx.y * MC);
-  for (int q = tid; q < nx * MC; q += NT) {
-    const int nd = q / MC, cc = q % MC;
-    phs[nd * PS + cc] = cc < P_used ? a.phi[(size_t)(blockIdx.y * MC + cc) * nx + nd] : 0.0;
+  for (int q = tid; q < (nx + 2 * D) * MC; q += NT) {
+    const int r = q / MC, cc = q % MC;
+    int nd = r - D;
+    nd = nd < 0 ? nd + nx : (nd >= nx ? nd - nx : nd);
+    phs[r * PS + cc] = cc < P_used ? a.phi[(size_t)(blockIdx.y * MC + cc) * nx + nd] : 0.0;
   }
   const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
   const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
@@ -1319,12 +1325,9 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
           locate_scaled_exact(x, nx, inv_nx, cell, f);
         }
         double pv[D + 1];
+        const double* pc = phs + (cell + Spline<D>::OFF + D) * PS + cl;
 #pragma unroll
-        for (int m = 0; m <= D; ++m) {
-          int nd = cell + Spline<D>::OFF + m;
-          nd = nd < 0 ? nd + nx : (nd >= nx ? nd - nx : nd);
-          pv[m] = phs[nd * PS + cl];
-        }
+        for (int m = 0; m <= D; ++m) pv[m] = pc[m * PS];
         double E;
         if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
           E = __dmul_rn(cf, __dadd_rn(__dmul_rn(-gi, pv[0]), __dmul_rn(gi, pv[1])));
@@ -1597,32 +1600,38 @@ static size_t mma_dep_smem(int n, int nx, int D) {
   return ((size_t)2 * TR * n + (size_t)(nx + D) * DC * 2) * sizeof(double);
 }
 static size_t mma_gat_smem(int n, int nx, bool vproj = false) {
-  return ((size_t)(vproj ? 4 : 2) * TR * n + (size_t)nx * (MC + 1)) * sizeof(double);
+  return ((size_t)(vproj ? 4 : 2) * TR * n + (size_t)(nx + 6) * (MC + 1)) * sizeof(double);
 }
 
-template <int D, int NK>
-static int launch_dep_mma_t(const RomArgs& a, int G, cudaStream_t s) {
-  auto kfn = rom_deposit_mma_kernel<D, NK>;
+template <int D, int NK, bool EX>
+static int launch_dep_mma_e(const RomArgs& a, int G, cudaStream_t s) {
+  auto kfn = rom_deposit_mma_kernel<D, NK, EX>;
   static bool attr = false;
   if (!attr) { rom_allow_smem(kfn); attr = true; }
   kfn<<<dim3(G, (a.p + DC - 1) / DC), DW * 32, mma_dep_smem(a.n, a.nx, D), s>>>(a);
   return picrom_check_launch("rom_deposit_mma_kernel");
 }
 template <int D, int NK>
-static int launch_gat_mma_t(const RomArgs& a, int G, cudaStream_t s) {
+static int launch_dep_mma_t(const RomArgs& a, int G, cudaStream_t s) {
+  return a.n == 4 * NK ? launch_dep_mma_e<D, NK, true>(a, G, s)
+                       : launch_dep_mma_e<D, NK, false>(a, G, s);
+}
+template <int D, int NK, bool VPROJ, bool EX>
+static int launch_gat_mma_e(const RomArgs& a, int G, cudaStream_t s) {
   const dim3 grid(G, (a.p + MC - 1) / MC);
-  if (a.uv) {
-    auto kfn = rom_gather_mma_kernel<D, NK, true>;
-    static bool attr = false;
-    if (!attr) { rom_allow_smem(kfn); attr = true; }
-    kfn<<<grid, MW * 32, mma_gat_smem(a.n, a.nx, true), s>>>(a);
-  } else {
-    auto kfn = rom_gather_mma_kernel<D, NK, false>;
-    static bool attr = false;
-    if (!attr) { rom_allow_smem(kfn); attr = true; }
-    kfn<<<grid, MW * 32, mma_gat_smem(a.n, a.nx, false), s>>>(a);
-  }
+  auto kfn = rom_gather_mma_kernel<D, NK, VPROJ, EX>;
+  static bool attr = false;
+  if (!attr) { rom_allow_smem(kfn); attr = true; }
+  kfn<<<grid, MW * 32, mma_gat_smem(a.n, a.nx, VPROJ), s>>>(a);
   return picrom_check_launch("rom_gather_mma_kernel");
+}
+template <int D, int NK>
+static int launch_gat_mma_t(const RomArgs& a, int G, cudaStream_t s) {
+  const bool ex = a.n == 4 * NK;
+  if (a.uv) return ex ? launch_gat_mma_e<D, NK, true, true>(a, G, s)
+                      : launch_gat_mma_e<D, NK, true, false>(a, G, s);
+  return ex ? launch_gat_mma_e<D, NK, false, true>(a, G, s)
+            : launch_gat_mma_e<D, NK, false, false>(a, G, s);
 }
 #define ROM_NK_DISPATCH(FN, D, A, G, S)                                              \
   (mma_nk(A.n) == 2 ? FN<D, 2>(A, G, S) : mma_nk(A.n) == 4 ? FN<D, 4>(A, G, S) :     \
