@@ -20,6 +20,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 #include <stdint.h>
 #include <stdlib.h>
@@ -1103,7 +1104,7 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
 }
 
 // X^T block: x0, x1 = X[rb + 2t (+1)][column g] from the staged U tile
-template <int NK>
+template <int NK, bool CHECK = true>
 __device__ __forceinline__ void recon_block(const double* tile, int rb, int rows, int n,
                                             const double* za, int g, int t, double& x0,
                                             double& x1) {
@@ -1113,7 +1114,7 @@ __device__ __forceinline__ void recon_block(const double* tile, int rb, int rows
 #pragma unroll
   for (int ks = 0; ks < NK; ++ks) {
     const int k = ks * 4 + t;
-    const double b = (ur < rows && k < n) ? tile[ur * n + k] : 0.0;
+    const double b = !CHECK || (ur < rows && k < n) ? tile[ur * n + k] : 0.0;
     dmma_f64(x0, x1, za[ks], b);
   }
 }
@@ -1303,14 +1304,19 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
     __syncthreads();
     const double* tile = ut + (tt & 1) * TR * n;
     const double* vtile = vt + (tt & 1) * TR * n;
-    for (int rb = 0; rb < rows; rb += 8) {
+    // full tiles (all but a CTA's last) run without row bounds tests; with an
+    // exact basis width (EX) no fragment test remains in the reconstruct
+    auto run_tile = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    const int nrows = FULL ? TR : rows;
+    for (int rb = 0; rb < nrows; rb += 8) {
       double xv[2], ev[2];
-      recon_block<NK>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
+      recon_block<NK, !(FULL && EX)>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         ev[e] = 0.0;
         const int row = rb + 2 * t + e;
-        if (!active || row >= rows) continue;
+        if (!active || (!FULL && row >= rows)) continue;
         const double x = xv[e];
         const long long i = t0 + row;
         int cell;
@@ -1367,19 +1373,22 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
 #pragma unroll
         for (int mt = 0; mt < NM; ++mt) {
           const int m = mt * 8 + g;
-          const double av = (ur < rows && m < n) ? tile[ur * n + m] : 0.0;
+          const double av = ((FULL || ur < rows) && m < n) ? tile[ur * n + m] : 0.0;
           dmma_f64(acc[mt][0], acc[mt][1], av, b);
         }
         if constexpr (VPROJ) {
 #pragma unroll
           for (int mt = 0; mt < NM; ++mt) {
             const int m = mt * 8 + g;
-            const double av = (ur < rows && m < n) ? vtile[ur * n + m] : 0.0;
+            const double av = ((FULL || ur < rows) && m < n) ? vtile[ur * n + m] : 0.0;
             dmma_f64(accv[mt][0], accv[mt][1], av, b);
           }
         }
       }
     }
+    };
+    if (rows == TR) run_tile(std::true_type{});
+    else run_tile(std::false_type{});
     __syncthreads();
   }
   // per-CTA partials seg[b][c][k]: lane holds basis m = 8 mt + g at columns 2t, 2t+1
