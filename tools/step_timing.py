@@ -1,6 +1,6 @@
 """Fused PIC step timing over (N, p, nx, degree) shapes (dev tool; select the
 library with PICROM_LIB).  Back-to-back steps between L2 flushes, CUDA events:
-    python tools/step_timing.py [steps]
+    python tools/step_timing.py [steps [groups,... [shape indices,...]]]
 Prints one line per shape: G pushes/s and the fraction of MEASURED_PEAKS hbm."""
 import json
 import sys
@@ -19,6 +19,8 @@ peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
     if (ROOT / "MEASURED_PEAKS.json").exists() else 6450.0
 shapes = [(250_000, 32, 128, 3), (250_000, 32, 512, 3), (4_000_000, 64, 512, 3),
           (4_000_000, 64, 128, 3), (1_000_000, 8, 64, 2), (250_000, 32, 64, 1)]
+if len(sys.argv) > 3:
+    shapes = [shapes[int(i)] for i in sys.argv[3].split(",")]
 flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 for (n, p, nx, d) in shapes:
   for groups in group_opts:
