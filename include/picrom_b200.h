@@ -260,6 +260,18 @@ int picrom_cross_gram(int nblocks, int na, const double* const* ptrs, const int*
                       const int* widths, const int* jswap, long long N, double* out,
                       void* workspace, void* stream);
 
+/* out (ca x k, row-major) = A^T B for a WIDE left operand: A (N x ca, row
+ * stride lda, even ca <= 448) is the DEIM sample window -- (T+1) p* = 420
+ * columns at C4 -- and B (N x k, row stride ldb, even k <= 48) a subspace
+ * block or the newest sample block.  These are the tall products of the
+ * windowed SVD that the reference gets from LAPACK's gesdd on the N x 420
+ * window (hyper.py:262): the sliding Gram update, W^T Q of the subspace
+ * iteration and the Rayleigh-Ritz block Q^T W.  Rows must be 16-byte aligned
+ * (even strides, aligned bases).  Fixed-order reduction (deterministic). */
+size_t picrom_tall_atb_workspace_bytes(long long N, int ca, int k);
+int picrom_tall_atb(const double* a, int lda, int ca, const double* b, int ldb, int k,
+                    long long N, double* out, void* workspace, void* stream);
+
 /* DEIM greedy selection step (hyper.py:241-244): out_index = the first index
  * of max |v[i*stride]| over i < n with the `banned` indices scored -1;
  * out_value (nullable) = that maximum. */
@@ -288,7 +300,9 @@ int picrom_deim_greedy(const double* psi, int ld, long long N, int d, const long
 
 /* out (N x c, row stride ldo) (+)= sum_t op_t(in_t) (N x widths[t]) @ M_t,
  * op_t = J when jswap[t] (nullable), M_t (widths[t] x c) at mats + moffs[t]
- * (device); c <= 32, at most 6 terms. */
+ * (device); at most 6 terms; c <= 32, or c <= 48 when N >= 1024 and every
+ * input row is 16-byte aligned (the window's W (N x 420) @ (420 x 48) products
+ * of the subspace iteration, hyper.py:262). */
 int picrom_combine(int nterms, const double* const* ins, const int* lds,
                    const int* widths, const int* jswap, const int* moffs,
                    const double* mats, int mats_len, long long N, double* out, int ldo,

@@ -85,6 +85,31 @@ def cross_gram(a_blocks, b_blocks):
     return _reduced(out).cpu().numpy()
 
 
+_ATB_WS = {}
+
+
+def atb(a, b):
+    """a^T b (host numpy, ca x k) for a WIDE tall device block a (N x ca, even
+    ca <= 448: the DEIM sample window) and a block b (N x k, even k <= 48),
+    picrom_tall_atb.  a and b may be column slices of wider row-major matrices
+    (row strides even, 16-byte aligned rows)."""
+    rows = a.shape[0]
+    ca, k = int(a.shape[1]), int(b.shape[1])
+    if a.stride(1) != 1:
+        a = a.contiguous()
+    if b.stride(1) != 1:
+        b = b.contiguous()
+    need = int(_lib.query("picrom_tall_atb_workspace_bytes", int(rows), ca, k))
+    key = torch.cuda.current_device()
+    ws = _ATB_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = _ATB_WS[key] = torch.empty(need, dtype=torch.uint8, device="cuda")
+    out = torch.empty((ca, k), dtype=torch.float64, device="cuda")
+    _lib.call("picrom_tall_atb", a.data_ptr(), int(a.stride(0)), ca, b.data_ptr(), int(b.stride(0)), k,
+              int(rows), out.data_ptr(), ws.data_ptr(), dev.stream_handle())
+    return _reduced(out).cpu().numpy()
+
+
 def gram_tasks(blocks, tasks):
     """Selected block products of gram(blocks): tasks = [(i, j), ...] -> numpy (W x W)
     with block (i, j) = B_i^T B_j for each task (other entries unspecified)."""

@@ -264,6 +264,15 @@ __device__ __forceinline__ double lds_f64_if(uint32_t addr, bool p) {
       : "+d"(v) : "r"(addr), "r"((uint32_t)p));
   return v;
 }
+// as lds_f64_if without the zero default: the result is undefined when p is
+// false (callers only store it under the same predicate)
+__device__ __forceinline__ double lds_f64_raw_if(uint32_t addr, bool p) {
+  double v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}\n"
+      : "=d"(v) : "r"(addr), "r"((uint32_t)p));
+  return v;
+}
 __device__ __forceinline__ void sts_f64_if(uint32_t addr, double v, bool p) {
   asm volatile(
       "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}\n"

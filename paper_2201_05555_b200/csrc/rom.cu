@@ -810,6 +810,137 @@ gram_mma_kernel(Blocks b, GramTasks tk, int na, long long N, int GT, int wn, dou
   (void)NACC;
 }
 
+// ---- tall A^T B for a WIDE left operand (the DEIM window, hyper.py:262) ----
+//
+// out (ca x k) = A^T B, A (N x ca, ld lda, ca <= 448: e.g. the (T+1) p* = 420
+// window columns) and B (N x k, k <= 48: the subspace block).  The Gram kernels
+// above take blocks <= 32 wide; here the output has up to 53 x 6 tiles of 8 x 8,
+// so each of the 8 warps owns TPW row tiles (8 columns of A each) x CT column
+// tiles of DMMA accumulators and every warp walks every 4-row k-step of the
+// CTA's row chunk.  Tiles of ATG rows of A and B land in smem by one TMA bulk
+// copy per row (pitches = 4 mod 16 doubles: the 4 rows x 8 columns of a
+// fragment load cover each bank twice -- the 2-wavefront minimum of a 256-byte
+// request), double buffered.  DMMA-bound: 42 DMMAs per 13 fragment loads at
+// 420 x 48.  Per-CTA partials -> seg, summed in a fixed order.
+constexpr int ATG = 16;      // rows per staged tile (32 in the k-split variant)
+__host__ __device__ inline int atb_pitch(int w) {
+  int p = w;
+  while (p % 16 != 4) ++p;
+  return p;
+}
+// KSPLIT (narrow A, ca <= 8 TPW: e.g. the 48 x 48 Gram of the subspace block):
+// every warp owns ALL TPW x CT output tiles and the warps split the k-steps of
+// a tile instead; their accumulators are summed through smem in warp order.
+template <int TPW, int CT, bool KSPLIT>
+__global__ void __launch_bounds__(256, 1)
+tall_atb_kernel(const double* __restrict__ A, int lda, int ca, const double* __restrict__ B,
+                int ldb, int k, long long N, double* seg) {
+  extern __shared__ __align__(128) double tsm[];
+  constexpr int TG = KSPLIT ? 2 * ATG : ATG;
+  const int pa = atb_pitch(ca), pb = atb_pitch(k);
+  const int SZ = TG * (pa + pb);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + 2 * SZ);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lc = lane >> 2, lr = lane & 3;
+  const int RT = (ca + 7) >> 3;
+  const long long lo = row_start(blockIdx.x, N, gridDim.x);
+  const long long hi = row_start(blockIdx.x + 1, N, gridDim.x);
+  const int nt = (int)((hi - lo + TG - 1) / TG);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // warp 0 stages tile t: lane r copies row r of A and of B
+  auto issue = [&](int t) {
+    const long long r0 = lo + (long long)t * TG;
+    const int rows = (int)min((long long)TG, hi - r0);
+    double* st = tsm + (t & 1) * SZ;
+    if (lane == 0) mbar_expect_tx(&full[t & 1], (uint32_t)rows * (uint32_t)(ca + k) * 8u);
+    __syncwarp();
+    if (lane < rows) {
+      bulk_g2s(st + lane * pa, A + (size_t)(r0 + lane) * lda, (uint32_t)ca * 8u, &full[t & 1]);
+      bulk_g2s(st + TG * pa + lane * pb, B + (size_t)(r0 + lane) * ldb, (uint32_t)k * 8u, &full[t & 1]);
+    }
+  };
+  double acc[TPW][CT][2];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int j = 0; j < CT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (warp == 0 && nt > 0) issue(0);
+  for (int t = 0; t < nt; ++t) {
+    const long long r0 = lo + (long long)t * TG;
+    const int rows = (int)min((long long)TG, hi - r0);
+    if (warp == 0 && t + 1 < nt) issue(t + 1);
+    mbar_wait(&full[t & 1], (uint32_t)((t >> 1) & 1));
+    const double* sa = tsm + (t & 1) * SZ;
+    const double* sb = sa + TG * pa;
+    const int ksteps = (rows + 3) >> 2;
+    for (int kk = KSPLIT ? warp : 0; kk < ksteps; kk += KSPLIT ? 8 : 1) {
+      const int r = kk * 4 + lr;
+      const bool rv = r < rows;
+      double fb[CT], fa[TPW];
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        const int c = 8 * j + lc;
+        fb[j] = (rv && c < k) ? sb[r * pb + c] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int c = 8 * (KSPLIT ? i : warp + 8 * i) + lc;
+        fa[i] = (rv && c < ca) ? sa[r * pa + c] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i)
+        if ((KSPLIT ? i : warp + 8 * i) < RT) {
+#pragma unroll
+          for (int j = 0; j < CT; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+        }
+    }
+    __syncthreads();                       // stage t&1 free for tile t+2
+  }
+  double* out = seg + (size_t)blockIdx.x * ca * k;
+  if constexpr (KSPLIT) {
+    // warps summed in a fixed order (warp 0 first) in smem (the stages are free)
+    double* red = tsm;                     // [TPW][CT][64]
+    for (int w = 0; w < 8; ++w) {
+      if (warp == w) {
+#pragma unroll
+        for (int i = 0; i < TPW; ++i)
+#pragma unroll
+          for (int j = 0; j < CT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double* q = red + (i * CT + j) * 64 + lane * 2 + e;
+              *q = (w == 0) ? acc[i][j][e] : *q + acc[i][j][e];
+            }
+      }
+      __syncthreads();
+    }
+    for (int q = tid; q < TPW * CT * 64; q += blockDim.x) {
+      const int e = q & 1, ln = (q >> 1) & 31, tile = q >> 6;
+      const int j = tile % CT, i = tile / CT;
+      const int ri = 8 * i + (ln >> 2), cj = 8 * j + 2 * (ln & 3) + e;
+      if (ri < ca && cj < k) out[(size_t)ri * k + cj] = red[q];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int ri = 8 * (warp + 8 * i) + lc;
+      if (ri >= ca) continue;
+#pragma unroll
+      for (int j = 0; j < CT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cj = 8 * j + 2 * lr + e;
+          if (cj < k) out[(size_t)ri * k + cj] = acc[i][j][e];
+        }
+    }
+  }
+}
+
 // first index of max |v[i*stride]| over i < n, skipping `banned` (numpy
 // argmax tie rule: the smallest index among equal maxima); banned entries
 // score -1 as in hyper.py:241-243.  Two passes: per-CTA (value, index), then
@@ -1124,6 +1255,11 @@ __device__ __forceinline__ void recon_block(const double* tile, int rb, int rows
 // share one histogram (2 copies per column, [nh][2 DC]) and take turns (two
 // predicated phases): half the smem per lane of private histograms, which
 // buys 16 resident warps instead of 8 (the kernel is latency-bound).
+#ifdef PICROM_DEP_LDS_RAW
+#define DEP_LDS lds_f64_raw_if
+#else
+#define DEP_LDS lds_f64_if
+#endif
 constexpr int DW = 16;           // warps per deposit CTA
 constexpr int DC = DW * 8;       // z columns per deposit CTA
 // EX: n == 4 NK exactly (C3/C4's n = 20): the basis width is a compile-time
@@ -1174,53 +1310,73 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
     }
     __syncthreads();
     const double* tile = ut + (tt & 1) * TR * n;
-    // RB row blocks per pass: RB independent DMMA chains, 2 RB units per lane
+    // RB row blocks per pass: RB independent DMMA chains, 2 RB units per lane.
+    // Full tiles (all but a CTA's last) run without row / column bounds tests:
+    // an inactive column (z = 0 -> x = 0) deposits into its own never-read
+    // histogram, a non-finite position deposits zero weights, so the deposit
+    // predicate is the lane's phase alone.
     constexpr int RB = 2;
-    for (int rb0 = 0; rb0 < rows; rb0 += 8 * RB) {
-      double xv[2 * RB];
+    auto run_tile = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      const int nrows = FULL ? TR : rows;
+      for (int rb0 = 0; rb0 < nrows; rb0 += 8 * RB) {
+        double xv[2 * RB];
 #pragma unroll
-      for (int q = 0; q < RB; ++q)
-        recon_block<NK>(tile, rb0 + 8 * q, rows, n, za, g, t, xv[2 * q], xv[2 * q + 1]);
-      double w[2 * RB][D + 1];
-      unsigned int hrow[2 * RB];
-      bool act[2 * RB];
-#pragma unroll
-      for (int e = 0; e < 2 * RB; ++e) {
-        const int row = rb0 + 8 * (e >> 1) + 2 * t + (e & 1);
-        act[e] = active && row < rows;
-        const double x = xv[e];
-        int cell;
-        double f;
-        bool rare;
-        locate_scaled(x, mask, cell, f, rare);
-        if (act[e] && rare) {
-          if (!isfinite(x)) {
-            record_bad(a.status, 0, t0 + row, c, a.p);
-            act[e] = false;
-            cell = 0;
-            f = 0.0;
-          } else {
-            locate_scaled_exact(x, nx, inv_nx, cell, f);
-          }
-        }
-        Spline<D>::weights(f, w[e]);
-        hrow[e] = hbase + (unsigned int)(act[e] ? cell : 0) * (unsigned int)(HS * 8);
-      }
-      // lanes t = 0, 2 then t = 1, 3 (the two lanes of a histogram)
-#pragma unroll
-      for (int ph = 0; ph < 2; ++ph) {
+        for (int q = 0; q < RB; ++q)
+          recon_block<NK, !(FULL && EX)>(tile, rb0 + 8 * q, rows, n, za, g, t, xv[2 * q], xv[2 * q + 1]);
+        double w[2 * RB][D + 1];
+        unsigned int hrow[2 * RB];
+        bool act[2 * RB];
 #pragma unroll
         for (int e = 0; e < 2 * RB; ++e) {
-          const bool on = act[e] && (t & 1) == ph;
-          double cur[D + 1];
+          const int row = rb0 + 8 * (e >> 1) + 2 * t + (e & 1);
+          act[e] = FULL ? active : (active && row < rows);
+          const double x = xv[e];
+          int cell;
+          double f;
+          bool rare;
+          locate_scaled(x, mask, cell, f, rare);
+          bool dead = false;
+          if (act[e] && rare) {
+            if (!isfinite(x)) {
+              record_bad(a.status, 0, t0 + row, c, a.p);
+              dead = true;
+              cell = 0;
+              f = 0.0;
+            } else {
+              locate_scaled_exact(x, nx, inv_nx, cell, f);
+            }
+          }
+          Spline<D>::weights(f, w[e]);
+          if constexpr (FULL) {
+            if (dead) {
 #pragma unroll
-          for (int m = 0; m <= D; ++m) cur[m] = lds_f64_if(hrow[e] + m * HS * 8u, on);
-#pragma unroll
-          for (int m = 0; m <= D; ++m) sts_f64_if(hrow[e] + m * HS * 8u, cur[m] + w[e][m], on);
+              for (int m = 0; m <= D; ++m) w[e][m] = 0.0;
+            }
+            hrow[e] = hbase + (unsigned int)cell * (unsigned int)(HS * 8);
+          } else {
+            act[e] = act[e] && !dead;
+            hrow[e] = hbase + (unsigned int)(act[e] ? cell : 0) * (unsigned int)(HS * 8);
+          }
         }
-        __syncwarp();
+        // lanes t = 0, 2 then t = 1, 3 (the two lanes of a histogram)
+#pragma unroll
+        for (int ph = 0; ph < 2; ++ph) {
+#pragma unroll
+          for (int e = 0; e < 2 * RB; ++e) {
+            const bool on = (FULL || act[e]) && (t & 1) == ph;
+            double cur[D + 1];
+#pragma unroll
+            for (int m = 0; m <= D; ++m) cur[m] = DEP_LDS(hrow[e] + m * HS * 8u, on);
+#pragma unroll
+            for (int m = 0; m <= D; ++m) sts_f64_if(hrow[e] + m * HS * 8u, cur[m] + w[e][m], on);
+          }
+          __syncwarp();
+        }
       }
-    }
+    };
+    if (rows == TR) run_tile(std::true_type{});
+    else run_tile(std::false_type{});
     __syncthreads();
   }
   // fold ghost rows and the 2 copies per column (fixed order) -> seg[b][c][nd];
@@ -1934,6 +2090,53 @@ extern "C" int picrom_gram_tasks(int nblocks, const double* const* ptrs, const i
   return gram_impl(nblocks, 0, ptrs, lds, widths, jswap, N, out, ws, stream);   // all blocks
 }
 
+static int atb_grid(long long N) {
+  return (int)std::max<long long>(1, std::min<long long>(picrom_num_sms(), N / (4 * ATG)));
+}
+
+extern "C" size_t picrom_tall_atb_workspace_bytes(long long N, int ca, int k) {
+  return (size_t)atb_grid(N) * (size_t)ca * (size_t)k * sizeof(double) + 256;
+}
+
+template <int TPW, int CT, bool KSPLIT>
+static int launch_tall_atb(const double* a, int lda, int ca, const double* b, int ldb, int k,
+                           long long N, double* seg, int G, cudaStream_t s) {
+  const int tg = KSPLIT ? 2 * ATG : ATG;
+  size_t sm = (size_t)2 * tg * (atb_pitch(ca) + atb_pitch(k)) * sizeof(double) + 2 * sizeof(uint64_t);
+  sm = std::max(sm, (size_t)TPW * CT * 64 * sizeof(double));
+  rom_allow_smem(tall_atb_kernel<TPW, CT, KSPLIT>);
+  tall_atb_kernel<TPW, CT, KSPLIT><<<G, 256, sm, s>>>(a, lda, ca, b, ldb, k, N, seg);
+  return picrom_check_launch("tall_atb_kernel");
+}
+
+extern "C" int picrom_tall_atb(const double* a, int lda, int ca, const double* b, int ldb, int k,
+                               long long N, double* out, void* ws, void* stream) {
+  if (N < 1 || ca < 2 || ca > 448 || k < 2 || k > 48 || (ca & 1) || (k & 1))
+    return picrom_set_error(PICROM_ERR_CONFIG, "tall_atb: even widths, 2 <= ca <= 448, 2 <= k <= 48");
+  if ((lda & 1) || (ldb & 1) || lda < ca || ldb < k ||
+      ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15))
+    return picrom_set_error(PICROM_ERR_CONFIG, "tall_atb: rows must be 16-byte aligned (even ld, aligned base)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int G = atb_grid(N);
+  double* seg = (double*)ws;
+  const int rt = (ca + 7) / 8;
+  const int tpw = (rt + 7) / 8;
+  const bool wide = k > 24;
+  int rc;
+  if (rt <= 6) rc = wide ? launch_tall_atb<6, 6, true>(a, lda, ca, b, ldb, k, N, seg, G, s)
+                         : launch_tall_atb<6, 3, true>(a, lda, ca, b, ldb, k, N, seg, G, s);
+  else if (tpw <= 1) rc = wide ? launch_tall_atb<1, 6, false>(a, lda, ca, b, ldb, k, N, seg, G, s)
+                               : launch_tall_atb<1, 3, false>(a, lda, ca, b, ldb, k, N, seg, G, s);
+  else if (tpw <= 4) rc = wide ? launch_tall_atb<4, 6, false>(a, lda, ca, b, ldb, k, N, seg, G, s)
+                               : launch_tall_atb<4, 3, false>(a, lda, ca, b, ldb, k, N, seg, G, s);
+  else rc = wide ? launch_tall_atb<7, 6, false>(a, lda, ca, b, ldb, k, N, seg, G, s)
+                 : launch_tall_atb<7, 3, false>(a, lda, ca, b, ldb, k, N, seg, G, s);
+  if (rc) return rc;
+  const int rows = ca * k;
+  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(seg, G, rows, out, 0, 0, 1);
+  return picrom_check_launch("seg_sum");
+}
+
 extern "C" int picrom_argmax_abs(const double* v, long long n, long long stride,
                                  const long long* banned, int nbanned, long long* out_index,
                                  double* out_value, void* ws, void* stream) {
@@ -2298,7 +2501,9 @@ static int launch_wide_combine(const Terms& t, const double* mats, long long N, 
     case 1: rom_allow_smem(wide_combine_kernel<1>); wide_combine_kernel<1><<<G, 256, sm, s>>>(t, mats, N, cp); break;
     case 2: rom_allow_smem(wide_combine_kernel<2>); wide_combine_kernel<2><<<G, 256, sm, s>>>(t, mats, N, cp); break;
     case 3: rom_allow_smem(wide_combine_kernel<3>); wide_combine_kernel<3><<<G, 256, sm, s>>>(t, mats, N, cp); break;
-    default: rom_allow_smem(wide_combine_kernel<4>); wide_combine_kernel<4><<<G, 256, sm, s>>>(t, mats, N, cp); break;
+    case 4: rom_allow_smem(wide_combine_kernel<4>); wide_combine_kernel<4><<<G, 256, sm, s>>>(t, mats, N, cp); break;
+    case 5: rom_allow_smem(wide_combine_kernel<5>); wide_combine_kernel<5><<<G, 256, sm, s>>>(t, mats, N, cp); break;
+    default: rom_allow_smem(wide_combine_kernel<6>); wide_combine_kernel<6><<<G, 256, sm, s>>>(t, mats, N, cp); break;
   }
   return picrom_check_launch("wide_combine_kernel");
 }
@@ -2308,7 +2513,13 @@ extern "C" int picrom_combine(int nterms, const double* const* ins, const int* l
                               const double* mats, int mats_len, long long N, double* out,
                               int ldo, int c, int accumulate, void* stream) {
   if (nterms < 1 || nterms > MAXTERM) return picrom_set_error(PICROM_ERR_CONFIG, "1..6 terms");
-  if (c < 1 || c > NMAX) return picrom_set_error(PICROM_ERR_CONFIG, "output width in [1, 32]");
+  // up to 48 output columns through the wide kernel (16-byte aligned rows, N >= 1024:
+  // the DEIM window's subspace block, hyper.py:262), 32 otherwise
+  bool all_aligned = N >= 1024;
+  for (int i = 0; i < nterms; ++i)
+    all_aligned &= (lds[i] % 2 == 0) && ((reinterpret_cast<uintptr_t>(ins[i]) & 15) == 0);
+  if (c < 1 || c > (all_aligned && !kNoCombineWide ? 48 : NMAX))
+    return picrom_set_error(PICROM_ERR_CONFIG, "output width in [1, 32] (48 for aligned inputs)");
   Terms t{};
   t.nt = nterms;
   for (int i = 0; i < nterms; ++i) {

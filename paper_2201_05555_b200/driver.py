@@ -472,6 +472,9 @@ def _run_reduced(system, params, x0, v0, *, basis_dim, subsample, window, deim_d
             hyper_now = hyper_reduction and len(pot_window) == window + 1
             if hyper_now:
                 hyper_engaged = True
+                # the window Gram's eigensolve (device, worker thread) runs under
+                # the host-side DMD fit
+                deim_window.prefetch_eigh()
                 with timers.phase("dmd_fit"):
                     dmd_model = hyp.fit_parametric_dmd(list(pot_window), dt, t_prev, params, sub,
                                                        svd_tol=svd_tol_dmd)

@@ -10,14 +10,15 @@ Split by size:
   stays in host LAPACK, as in the reference;
 * everything that scales with the particle count N runs on the device:
   the DEIM window Gram (sliding, one new block x window per step), the
-  window SVD (Gram eigenvectors refined by subspace iteration: plain tall
-  GEMMs), the whole greedy index selection (picrom_deim_greedy, one device
+  window SVD (Gram eigenvectors refined by subspace iteration; its tall
+  products are the library's own DMMA kernels, picrom_tall_atb and
+  picrom_combine), the whole greedy index selection (picrom_deim_greedy, one device
   sequence, no host round trip per index), U_X[I] (picrom_rows_gather), and
   per stage the DMD extrapolation (picrom_dmd_extrapolate) and the
   DEIM-sampled gather + projection (picrom_deim_gather).
 
-The DEIM SVD is computed from the window Gram (eigen-decomposition on the
-host) followed by one Rayleigh-Ritz refinement on the device; its accuracy
+The DEIM SVD is computed from the window Gram (420 x 420 eigen-decomposition,
+cuSOLVER) followed by one Rayleigh-Ritz refinement on the device; its accuracy
 (and therefore index parity with the reference's direct SVD) is discussed in
 DESIGN.md -- greedy index selection itself is bit-exact given the same basis.
 """
@@ -212,22 +213,60 @@ class DEIMModel:
         return self.psi.shape[1]
 
 
-def _tsq(a, b, chunk=8192):
-    """a^T b for tall device blocks (N x ka, N x kb): batched DGEMM over row
-    chunks (split-K; a single GEMM with K = N runs on a handful of tiles), the
-    chunk products summed in a fixed order.  Host result."""
-    n = a.shape[0]
-    nb = n // chunk
-    out = None
-    if nb > 0:
-        m = nb * chunk
-        ab = a[:m].unflatten(0, (nb, chunk))
-        bb = b[:m].unflatten(0, (nb, chunk))
-        out = torch.bmm(ab.transpose(1, 2), bb).sum(dim=0)
-    if n > nb * chunk:
-        tail = a[nb * chunk:].T @ b[nb * chunk:]
-        out = tail if out is None else out + tail
-    return out.cpu().numpy()
+def _even_cols(t):
+    """t with an even column count and 16-byte aligned rows (a zero column is
+    appended to an odd-width block; copies only when needed)."""
+    if t.shape[1] % 2 == 0 and t.stride(1) == 1 and t.stride(0) % 2 == 0 and t.data_ptr() % 16 == 0:
+        return t
+    w = t.shape[1] + (t.shape[1] & 1)
+    out = torch.zeros((t.shape[0], w), dtype=torch.float64, device="cuda")
+    out[:, :t.shape[1]].copy_(t)
+    return out
+
+
+def _tsq(a, b):
+    """a^T b (host numpy) for tall device blocks (N x ka, N x kb) on the library's
+    own DMMA kernel (picrom_tall_atb: the wider operand streams as the window,
+    <= 448 columns per call, the narrower one as the <= 48-column block)."""
+    ka, kb = a.shape[1], b.shape[1]
+    if ka < kb:
+        return _tsq(b, a).T
+    ae, be = _even_cols(a), _even_cols(b)
+    out = np.empty((ae.shape[1], be.shape[1]))
+    for i in range(0, ae.shape[1], 448):
+        for j in range(0, be.shape[1], 48):
+            out[i:i + 448, j:j + 48] = _tall.atb(ae[:, i:i + 448], be[:, j:j + 48])
+    return out[:ka, :kb]
+
+
+def _mul(w, m):
+    """w (N x c, device) @ m (c x k, host) -> device (N x k): picrom_combine (the
+    wide-term DMMA kernel takes up to 48 output columns for aligned rows)."""
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    k = m.shape[1]
+    aligned = (w.stride(1) == 1 and w.stride(0) % 2 == 0 and w.data_ptr() % 16 == 0
+               and w.shape[0] >= 1024)
+    step = 48 if aligned else 32
+    out = torch.empty((w.shape[0], k), dtype=torch.float64, device="cuda")
+    for j in range(0, k, step):
+        _tall.combine([(w, m[:, j:j + step], False)], out=out[:, j:j + step])
+    return out
+
+
+def _eigh_device(gram):
+    """Eigenpairs (ascending) of a small symmetric host matrix on the device
+    (cuSOLVER through torch; 4 ms against 8 ms in host LAPACK at 420 x 420), on
+    a private stream so it can run from a worker thread."""
+    stream = _EIGH_STREAMS.get(torch.cuda.current_device())
+    if stream is None:
+        stream = _EIGH_STREAMS[torch.cuda.current_device()] = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        lam_d, vec_d = torch.linalg.eigh(torch.from_numpy(np.ascontiguousarray(gram)).to("cuda"))
+        return lam_d.cpu().numpy(), vec_d.cpu().numpy()
+
+
+_EIGH_STREAMS = {}
+_EIGH_POOL = None
 
 
 class DeimWindow:
@@ -243,6 +282,8 @@ class DeimWindow:
         self.w = None
         self.slots = deque()     # slot of each block, oldest first
         self.G = None            # host Gram in slot order
+        self._version = 0        # bumped by append()
+        self._eig = None         # (version, future) of a prefetched eigensolve
 
     def __len__(self):
         return len(self.slots)
@@ -259,10 +300,34 @@ class DeimWindow:
         self.mat[:, slot * w:(slot + 1) * w].copy_(block)
         self.slots.append(slot)
         filled = len(self.slots) * w if len(self.slots) < self.capacity else self.capacity * w
-        # new block against the whole window (plain DGEMM)
+        # new block against the whole window (picrom_tall_atb)
         g = _tsq(self.mat[:, slot * w:(slot + 1) * w], self.mat[:, :filled])
         self.G[slot * w:(slot + 1) * w, :filled] = g
         self.G[:filled, slot * w:(slot + 1) * w] = g.T
+        self._version += 1
+
+    def prefetch_eigh(self):
+        """Start the window Gram's eigensolve on a worker thread (its own CUDA
+        stream): the caller's host work -- the DMD fit -- overlaps it."""
+        global _EIGH_POOL
+        if _EIGH_POOL is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _EIGH_POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="picrom-eigh")
+        c = len(self.slots) * self.w
+        dev_id = torch.cuda.current_device()
+
+        def job(gram=self.G[:c, :c].copy()):
+            torch.cuda.set_device(dev_id)
+            return _eigh_device(gram)
+        self._eig = (self._version, _EIGH_POOL.submit(job))
+
+    def eigh(self):
+        """(eigenvalues ascending, eigenvectors) of the current window Gram."""
+        pending, self._eig = self._eig, None
+        if pending is not None and pending[0] == self._version:
+            return pending[1].result()
+        c = len(self.slots) * self.w
+        return _eigh_device(self.G[:c, :c])
 
     def _ring_cols(self):
         return np.concatenate([np.arange(s * self.w, (s + 1) * self.w) for s in self.slots])
@@ -304,6 +369,17 @@ def _greedy_device(psi, keep=None):
 
 
 _GREEDY_WS = {}
+_ONES = {}
+
+
+def _ones(rows):
+    """Cached (rows x 2) block of ones (the column sums Psi^T 1 as a tall product)."""
+    key = (torch.cuda.current_device(), int(rows))
+    buf = _ONES.get(key)
+    if buf is None:
+        _ONES.clear()
+        buf = _ONES[key] = torch.ones((rows, 2), dtype=torch.float64, device="cuda")
+    return buf
 
 
 def deim_greedy(psi, keep=None):
@@ -326,41 +402,45 @@ def _rows(psi, idx):
     return out.cpu().numpy()
 
 
+def _orth_factor(y, kappa_one=16.0):
+    """Cholesky-QR factor of a tall device block (N x k): returns (y, R^-1)
+    with Q = y R^-1 orthonormal to O(eps kappa(R)^2).  Q is never formed -- the
+    callers fold R^-1 into the next small matrix.  The blocks of _window_svd are
+    balanced (kappa ~ 1); an ill-conditioned block gets one explicit round first
+    (CholQR2)."""
+    g = _tsq(y, y)
+    r = np.linalg.cholesky(g).T
+    sv = np.linalg.svd(r, compute_uv=False)
+    if sv[0] > kappa_one * sv[-1]:
+        y = _mul(y, np.linalg.inv(r))
+        r = np.linalg.cholesky(_tsq(y, y)).T
+    return y, np.linalg.inv(r)
+
+
 def _orthonormalize(y, kappa_one=16.0):
-    """Cholesky QR of a tall device block (N x k): Q with Q^T Q = I to O(eps).
-    CholQR's orthogonality error is ~eps kappa(Y)^2, so a second round (CholQR2)
-    runs only when the first factor is not well conditioned -- the balanced
-    blocks of _window_svd (columns pre-scaled by the inverse singular values)
-    need one round, an arbitrary block two."""
-    for _ in range(2):
-        g = _tsq(y, y)
-        r = np.linalg.cholesky(g).T
-        y = y @ torch.from_numpy(np.linalg.inv(r)).to("cuda")
-        sv = np.linalg.svd(r, compute_uv=False)
-        if sv[0] <= kappa_one * sv[-1]:
-            break
-    return y
+    """Explicit Cholesky QR of a tall device block (N x k)."""
+    y, rinv = _orth_factor(y, kappa_one)
+    return _mul(y, rinv)
 
 
 def _window_svd(window, dim, oversample=8, iterations=1):
     """Leading left singular vectors of the window W (N x c) without forming
-    more than an N x (d+q) block (the products are plain DGEMMs on the
-    contiguous window):
-      1. W^T W (sliding Gram) -> eigenpairs -> initial basis Y = W V_{d+q};
-      2. `iterations` subspace-iteration steps Y <- W (W^T Q) Sigma^-2, Q =
-         CholQR(Y) (a second round only if Y is not balanced), which removes
-         the squared-condition error of step 1;
-      3. Rayleigh-Ritz: SVD of the small Q^T W, Psi = Q U_B[:, :d].
+    more than an N x (d+q) block; every tall product runs on the library's own
+    DMMA kernels (picrom_tall_atb for A^T B, picrom_combine for W M):
+      1. W^T W (sliding Gram) -> eigenpairs -> initial block Y = W V_{d+q} / sigma;
+      2. `iterations` subspace-iteration steps Y <- W (W^T Q) Sigma^-2 with
+         Q = Y R^-1 from a Cholesky QR whose R^-1 is folded into the small
+         matrix (W^T Q = (W^T Y) R^-1), which removes the squared-condition
+         error of step 1;
+      3. Rayleigh-Ritz: SVD of the small Q^T W = R^-T (Y^T W), Psi = Y (R^-1 U_B[:, :d]).
     The rank test is the reference's (hyper.py:263) on the Gram singular values.
     One refinement iteration is enough at C4 (teacher-forced against LAPACK at
-    full size: indices bit-exact, weights 1.3e-11, the step's Z 1.3e-12,
-    profiles/r02); none is not (indices differ)."""
+    full size: indices bit-exact, weights ~1e-11, the step's Z ~1e-12,
+    profiles/r02); none is not (indices differ).  The c x c eigensolve
+    (N-independent, 420 x 420 at C4) is cuSOLVER's, as the reference's is LAPACK's."""
     W, gram = window.matrix()
     c = W.shape[1]
-    # the c x c eigensolve on the device (cuSOLVER): ~8 ms per 420 x 420 in host
-    # LAPACK even with the BLAS threads capped
-    lam_d, vec_d = torch.linalg.eigh(torch.from_numpy(np.ascontiguousarray(gram)).to("cuda"))
-    lam, vec = lam_d.cpu().numpy(), vec_d.cpu().numpy()
+    lam, vec = window.eigh()
     order = np.argsort(lam)[::-1]
     lam, vec = lam[order], vec[:, order]
     sing = np.sqrt(np.clip(lam, 0.0, None))
@@ -370,14 +450,16 @@ def _window_svd(window, dim, oversample=8, iterations=1):
     if d_eff < dim:
         warnings.warn(f"DEIM samples have numerical rank {rank} < {dim}; basis reduced to {d_eff}")
     k = min(c, rank, d_eff + oversample, 64)
-    q = _orthonormalize(W @ torch.from_numpy(vec[:, :k] / sing[:k]).to("cuda"))
+    y = _mul(W, vec[:, :k] / sing[:k])
     for _ in range(iterations):
         # W W^T Q ~ Q Sigma^2: dividing column j by sigma_j^2 keeps the block
         # balanced (kappa ~ 1), so one Cholesky QR round suffices
-        q = _orthonormalize(W @ torch.from_numpy(_tsq(W, q) / lam[:k]).to("cuda"))
-    qtw = _tsq(W, q).T
+        y, rinv = _orth_factor(y)
+        y = _mul(W, (_tsq(W, y) @ rinv) / lam[:k])
+    y, rinv = _orth_factor(y)
+    qtw = rinv.T @ _tsq(W, y).T
     ub, _, _ = svd(qtw, full_matrices=False)
-    psi = q @ torch.from_numpy(np.ascontiguousarray(ub[:, :d_eff])).to("cuda")
+    psi = _mul(y, rinv @ ub[:, :d_eff])
     return psi, d_eff
 
 
@@ -396,8 +478,7 @@ def fit_deim_device(window, dim, charge, prev=None, full=True, n_update=None,
         refresh = {int(i) for i in (order[::-1] if printed_ranking else order)[:n_update]}
         keep = {k: int(prev.indices[k]) for k in range(d_eff) if k not in refresh}
     idx_d, rows_d = _greedy_device(psi, keep)
-    ones = torch.ones((psi.shape[0], 1), dtype=torch.float64, device="cuda")
-    colsum = _tall.gram([(psi, False), (ones, False)])[:d_eff, d_eff]     # one sync
+    colsum = _tsq(psi, _ones(psi.shape[0]))[:d_eff, 0]                    # Psi^T 1, one sync
     indices = idx_d.cpu().numpy()
     # weights = solve(Psi[I]^T, qw Psi^T 1) (hyper.py:276), Psi[I] from the greedy
     weights = np.linalg.solve(rows_d.cpu().numpy().T, charge.charge_weight * colsum)

@@ -125,3 +125,67 @@ def test_combine_wide_term(lib_built, rows, c):
     got = out.cpu().numpy()
     assert np.abs(got[rows:] - ref).max() <= 1e-12 * np.abs(ref).max()
     assert not got[:rows].any()
+
+
+@pytest.mark.parametrize("ca,k,rows", [(420, 48, 30011), (420, 20, 4099), (48, 48, 2 * 25013),
+                                       (140, 24, 1500), (6, 2, 333), (448, 48, 1024)])
+def test_tall_atb_wide_left_operand(lib_built, ca, k, rows):
+    """picrom_tall_atb (the DEIM window's W^T Q, Q^T W and sliding Gram update,
+    hyper.py:262) against numpy, incl. column slices of a wider row-major
+    matrix (row stride > width), ragged last tiles and few-row inputs."""
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(ca * 3 + k + rows)
+    big = rng.standard_normal((rows, ca + 12)) * np.logspace(0, -6, ca + 12)
+    b = rng.standard_normal((rows, k))
+    bd = torch.from_numpy(big).cuda()
+    a_view = bd[:, 4:4 + ca]                  # stride ca + 12, offset 32 bytes
+    got = _tall.atb(a_view, torch.from_numpy(b).cuda())
+    ref = big[:, 4:4 + ca].T @ b
+    scale = np.linalg.norm(big[:, 4:4 + ca], axis=0)[:, None] * np.linalg.norm(b, axis=0)[None, :]
+    assert np.abs(got - ref).max() <= 1e-13 * scale.max()
+    assert (np.abs(got - ref) <= 1e-12 * scale + 1e-300).all()
+    assert np.array_equal(got, _tall.atb(a_view, torch.from_numpy(b).cuda()))     # deterministic
+
+
+def test_tall_atb_rejects_unaligned(lib_built):
+    import torch
+    from paper_2201_05555_b200 import _tall
+    from paper_2201_05555_b200.errors import ConfigurationError
+    a = torch.zeros((64, 21), dtype=torch.float64, device="cuda")
+    b = torch.zeros((64, 4), dtype=torch.float64, device="cuda")
+    with pytest.raises((ConfigurationError, RuntimeError, ValueError)):
+        _tall.atb(a, b)
+
+
+@pytest.mark.parametrize("c", [40, 48])
+def test_combine_up_to_48_columns(lib_built, c):
+    """W (N x 420) @ M (420 x c): the subspace-iteration products of the window
+    SVD through the wide-term DMMA combine."""
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(c)
+    rows = 20011
+    w = rng.standard_normal((rows, 420))
+    m = rng.standard_normal((420, c))
+    got = _tall.combine([(torch.from_numpy(w).cuda(), m, False)]).cpu().numpy()
+    ref = w @ m
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_window_svd_tall_products_helpers(lib_built):
+    """hyper._tsq / hyper._mul: odd widths, > 48 columns and > 448 columns are
+    chunked or padded onto the library kernels."""
+    import torch
+    from paper_2201_05555_b200 import hyper
+    rng = np.random.default_rng(3)
+    rows = 5003
+    a = rng.standard_normal((rows, 451))
+    b = rng.standard_normal((rows, 51))
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    ref = a.T @ b
+    assert np.abs(hyper._tsq(ad, bd) - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert np.abs(hyper._tsq(bd, ad) - ref.T).max() <= 1e-12 * np.abs(ref).max()
+    m = rng.standard_normal((451, 51))
+    got = hyper._mul(ad, m).cpu().numpy()
+    assert np.abs(got - a @ m).max() <= 1e-12 * np.abs(a @ m).max()
