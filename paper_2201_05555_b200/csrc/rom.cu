@@ -822,7 +822,7 @@ gram_mma_kernel(Blocks b, GramTasks tk, int na, long long N, int GT, int wn, dou
 // fragment load cover each bank twice -- the 2-wavefront minimum of a 256-byte
 // request), double buffered.  DMMA-bound: 42 DMMAs per 13 fragment loads at
 // 420 x 48.  Per-CTA partials -> seg, summed in a fixed order.
-constexpr int ATG = 16;      // rows per staged tile (32 in the k-split variant)
+constexpr int ATG = 16;      // rows per staged tile (64 in the k-split variant)
 __host__ __device__ inline int atb_pitch(int w) {
   int p = w;
   while (p % 16 != 4) ++p;
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(256, 1)
 tall_atb_kernel(const double* __restrict__ A, int lda, int ca, const double* __restrict__ B,
                 int ldb, int k, long long N, double* seg) {
   extern __shared__ __align__(128) double tsm[];
-  constexpr int TG = KSPLIT ? 2 * ATG : ATG;
+  constexpr int TG = KSPLIT ? 4 * ATG : ATG;
   const int pa = atb_pitch(ca), pb = atb_pitch(k);
   const int SZ = TG * (pa + pb);
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm + 2 * SZ);
@@ -859,9 +859,9 @@ tall_atb_kernel(const double* __restrict__ A, int lda, int ca, const double* __r
     double* st = tsm + (t & 1) * SZ;
     if (lane == 0) mbar_expect_tx(&full[t & 1], (uint32_t)rows * (uint32_t)(ca + k) * 8u);
     __syncwarp();
-    if (lane < rows) {
-      bulk_g2s(st + lane * pa, A + (size_t)(r0 + lane) * lda, (uint32_t)ca * 8u, &full[t & 1]);
-      bulk_g2s(st + TG * pa + lane * pb, B + (size_t)(r0 + lane) * ldb, (uint32_t)k * 8u, &full[t & 1]);
+    for (int r = lane; r < rows; r += 32) {
+      bulk_g2s(st + r * pa, A + (size_t)(r0 + r) * lda, (uint32_t)ca * 8u, &full[t & 1]);
+      bulk_g2s(st + TG * pa + r * pb, B + (size_t)(r0 + r) * ldb, (uint32_t)k * 8u, &full[t & 1]);
     }
   };
   double acc[TPW][CT][2];
@@ -1264,19 +1264,23 @@ constexpr int DW = 16;           // warps per deposit CTA
 constexpr int DC = DW * 8;       // z columns per deposit CTA
 // EX: n == 4 NK exactly (C3/C4's n = 20): the basis width is a compile-time
 // constant, so the fragment bounds tests fold away and row offsets are shifts
-template <int D, int NK, bool EX>
-__global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) {
+// DWT warps per CTA: DW for wide column sets; 4 (32 columns, several CTAs per
+// SM) for the few subsample columns of the hyper-reduced model (C4: p* = 20),
+// where a 128-column CTA would idle 5/6 of its lanes
+template <int D, int NK, bool EX, int DWT>
+__global__ void __launch_bounds__(DWT * 32, DWT == DW ? 1 : 4) rom_deposit_mma_kernel(RomArgs a) {
+  constexpr int DCT = DWT * 8;
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
-  constexpr int NT = DW * 32;
-  constexpr int HS = DC * 2;                  // histograms (row stride)
+  constexpr int NT = DWT * 32;
+  constexpr int HS = DCT * 2;                  // histograms (row stride)
   const int n = EX ? 4 * NK : a.n, nx = a.nx, nh = nx + D;
   double* ut = smem;                          // [2][TR * n]
   double* hist = ut + 2 * TR * n;             // [nh][HS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int cl = warp * 8 + g;
-  const int c = blockIdx.y * DC + cl;
+  const int c = blockIdx.y * DCT + cl;
   const bool active = c < a.p;
   const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
   const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
@@ -1382,7 +1386,7 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
   // fold ghost rows and the 2 copies per column (fixed order) -> seg[b][c][nd];
   // consecutive threads take consecutive columns of one node (one 16-byte
   // load of both copies: conflict-free)
-  const int P_used = min(DC, a.p - blockIdx.y * DC);
+  const int P_used = min(DCT, a.p - blockIdx.y * DCT);
   for (int q = tid; q < P_used * nx; q += NT) {
     const int nd = q / P_used, cc = q % P_used;
     double s = 0.0;
@@ -1390,17 +1394,20 @@ __global__ void __launch_bounds__(DW * 32, 1) rom_deposit_mma_kernel(RomArgs a) 
       const double2 v = *reinterpret_cast<const double2*>(hist + rr * HS + 2 * cc);
       s += v.x + v.y;
     }
-    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * DC + cc) * nx + nd] = s;
+    a.seg[((size_t)blockIdx.x * a.p + blockIdx.y * DCT + cc) * nx + nd] = s;
   }
 }
 
-template <int D, int NK, bool VPROJ, bool EX>
-__global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
+// MWT warps per CTA: MW, or 4 (32 columns) for the few subsample columns of the
+// hyper-reduced model (see rom_deposit_mma_kernel)
+template <int D, int NK, bool VPROJ, bool EX, int MWT>
+__global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
+  constexpr int MCT = MWT * 8;
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
-  constexpr int NT = MW * 32;
+  constexpr int NT = MWT * 32;
   constexpr int NM = (4 * NK + 7) / 8;        // 8-row tiles of the projection (n <= 8 NM)
-  constexpr int PS = MC + 1;                  // padded phi row (bank spread)
+  constexpr int PS = MCT + 1;                  // padded phi row (bank spread)
   const int n = EX ? 4 * NK : a.n, nx = a.nx;
   double* ut = smem;                          // [2][TR * n]
   // phi with D periodic ghost rows on each side: row r holds node (r - D) mod nx,
@@ -1410,14 +1417,14 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int cl = warp * 8 + g;
-  const int c = blockIdx.y * MC + cl;
+  const int c = blockIdx.y * MCT + cl;
   const bool active = c < a.p;
-  const int P_used = min(MC, a.p - blockIdx.y * MC);
-  for (int q = tid; q < (nx + 2 * D) * MC; q += NT) {
-    const int r = q / MC, cc = q % MC;
+  const int P_used = min(MCT, a.p - blockIdx.y * MCT);
+  for (int q = tid; q < (nx + 2 * D) * MCT; q += NT) {
+    const int r = q / MCT, cc = q % MCT;
     int nd = r - D;
     nd = nd < 0 ? nd + nx : (nd >= nx ? nd - nx : nd);
-    phs[r * PS + cc] = cc < P_used ? a.phi[(size_t)(blockIdx.y * MC + cc) * nx + nd] : 0.0;
+    phs[r * PS + cc] = cc < P_used ? a.phi[(size_t)(blockIdx.y * MCT + cc) * nx + nd] : 0.0;
   }
   const int inst_id = active ? (a.cols ? a.cols[c] : c) : 0;
   const double* ip = a.inst + (size_t)inst_id * PICROM_INST_STRIDE;
@@ -1553,7 +1560,7 @@ __global__ void __launch_bounds__(MW * 32) rom_gather_mma_kernel(RomArgs a) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int m = mt * 8 + g;
-      const int col = blockIdx.y * MC + warp * 8 + 2 * t + e;
+      const int col = blockIdx.y * MCT + warp * 8 + 2 * t + e;
       if (m < n && col < a.p) {
         a.seg[((size_t)blockIdx.x * a.p + col) * n + m] = acc[mt][e];
         if constexpr (VPROJ) a.seg2[((size_t)blockIdx.x * a.p + col) * n + m] = accv[mt][e];
@@ -1692,7 +1699,8 @@ combine_mma_kernel(Terms t, MmaTerms mt, const double* mats, long long N) {
 }
 
 extern "C" size_t picrom_rom_workspace_bytes(long long N, int p, int n, int nx) {
-  const size_t G = (size_t)std::max(rom_grid(N), rom_grid_mma(N, p, kGatherMmaPerSm));
+  size_t G = (size_t)std::max(rom_grid(N), rom_grid_mma(N, p, kGatherMmaPerSm));
+  G = std::max(G, (size_t)picrom_num_sms() * 4);      // narrow-deposit grid (kDepNarrowPerSm)
   const size_t dep = G * p * nx;
   const size_t gat = 2 * G * p * n;        // U_X^T E and U_V^T E partials
   const size_t gram = (size_t)gram_grid(N) * 256 * 256;
@@ -1761,16 +1769,26 @@ static int launch_rom_gather(const RomArgs& a, int G, cudaStream_t s) {
 
 // DMMA path: k-steps NK = ceil(n / 4) rounded up to {2, 4, 5, 8}
 static int mma_nk(int n) { return n <= 8 ? 2 : n <= 16 ? 4 : n <= 20 ? 5 : 8; }
-static size_t mma_dep_smem(int n, int nx, int D) {
-  return ((size_t)2 * TR * n + (size_t)(nx + D) * DC * 2) * sizeof(double);
+static size_t mma_dep_smem(int n, int nx, int D, int dwt = DW) {
+  return ((size_t)2 * TR * n + (size_t)(nx + D) * dwt * 8 * 2) * sizeof(double);
 }
-static size_t mma_gat_smem(int n, int nx, bool vproj = false) {
-  return ((size_t)(vproj ? 4 : 2) * TR * n + (size_t)(nx + 6) * (MC + 1)) * sizeof(double);
+// few columns (the hyper-reduced model's subsample): 4-warp deposit CTAs, 4 per SM
+constexpr int kDepNarrowCols = 32;
+constexpr int kDepNarrowPerSm = 4;
+static size_t mma_gat_smem(int n, int nx, bool vproj = false, int mwt = MW) {
+  return ((size_t)(vproj ? 4 : 2) * TR * n + (size_t)(nx + 6) * (mwt * 8 + 1)) * sizeof(double);
 }
 
 template <int D, int NK, bool EX>
 static int launch_dep_mma_e(const RomArgs& a, int G, cudaStream_t s) {
-  auto kfn = rom_deposit_mma_kernel<D, NK, EX>;
+  if (a.p <= kDepNarrowCols) {
+    auto kfn = rom_deposit_mma_kernel<D, NK, EX, 4>;
+    static bool attr = false;
+    if (!attr) { rom_allow_smem(kfn); attr = true; }
+    kfn<<<dim3(G, 1), 4 * 32, mma_dep_smem(a.n, a.nx, D, 4), s>>>(a);
+    return picrom_check_launch("rom_deposit_mma_kernel");
+  }
+  auto kfn = rom_deposit_mma_kernel<D, NK, EX, DW>;
   static bool attr = false;
   if (!attr) { rom_allow_smem(kfn); attr = true; }
   kfn<<<dim3(G, (a.p + DC - 1) / DC), DW * 32, mma_dep_smem(a.n, a.nx, D), s>>>(a);
@@ -1783,8 +1801,15 @@ static int launch_dep_mma_t(const RomArgs& a, int G, cudaStream_t s) {
 }
 template <int D, int NK, bool VPROJ, bool EX>
 static int launch_gat_mma_e(const RomArgs& a, int G, cudaStream_t s) {
+  if (a.p <= kDepNarrowCols) {
+    auto kfn = rom_gather_mma_kernel<D, NK, VPROJ, EX, 4>;
+    static bool attr = false;
+    if (!attr) { rom_allow_smem(kfn); attr = true; }
+    kfn<<<dim3(G, 1), 4 * 32, mma_gat_smem(a.n, a.nx, VPROJ, 4), s>>>(a);
+    return picrom_check_launch("rom_gather_mma_kernel");
+  }
   const dim3 grid(G, (a.p + MC - 1) / MC);
-  auto kfn = rom_gather_mma_kernel<D, NK, VPROJ, EX>;
+  auto kfn = rom_gather_mma_kernel<D, NK, VPROJ, EX, MW>;
   static bool attr = false;
   if (!attr) { rom_allow_smem(kfn); attr = true; }
   kfn<<<grid, MW * 32, mma_gat_smem(a.n, a.nx, VPROJ), s>>>(a);
@@ -1806,6 +1831,8 @@ static int launch_gat_mma_t(const RomArgs& a, int G, cudaStream_t s) {
 template <int D>
 static int rom_dep_grid(const RomArgs& a) {
   if (!rom_use_mma() || mma_dep_smem(a.n, a.nx, D) > 220 * 1024) return rom_grid(a.N);
+  if (a.p <= kDepNarrowCols)
+    return (int)std::min<long long>((long long)picrom_num_sms() * kDepNarrowPerSm, std::max<long long>(1, a.N / 64));
   const int tiles = (a.p + DC - 1) / DC;
   return (int)std::min<long long>(std::max(1, picrom_num_sms() / tiles), std::max<long long>(1, a.N / 64));
 }
@@ -1815,6 +1842,8 @@ static int launch_rom_deposit_any(const RomArgs& a, int G, cudaStream_t s) {
   return ROM_NK_DISPATCH(launch_dep_mma_t, D, a, G, s);
 }
 static int rom_gat_grid(const RomArgs& a) {
+  if (rom_use_mma() && a.p <= kDepNarrowCols)     // 4-warp CTAs, 4 per SM
+    return (int)std::min<long long>((long long)picrom_num_sms() * kDepNarrowPerSm, std::max<long long>(1, a.N / 64));
   if (a.uv) return rom_grid_mma(a.N, a.p, 2);     // 94 registers: 2 CTAs per SM
   if (!rom_use_mma() || mma_gat_smem(a.n, a.nx) > 200 * 1024) return rom_grid(a.N);
   return rom_grid_mma(a.N, a.p, kGatherMmaPerSm);
@@ -2101,7 +2130,7 @@ extern "C" size_t picrom_tall_atb_workspace_bytes(long long N, int ca, int k) {
 template <int TPW, int CT, bool KSPLIT>
 static int launch_tall_atb(const double* a, int lda, int ca, const double* b, int ldb, int k,
                            long long N, double* seg, int G, cudaStream_t s) {
-  const int tg = KSPLIT ? 2 * ATG : ATG;
+  const int tg = KSPLIT ? 4 * ATG : ATG;
   size_t sm = (size_t)2 * tg * (atb_pitch(ca) + atb_pitch(k)) * sizeof(double) + 2 * sizeof(uint64_t);
   sm = std::max(sm, (size_t)TPW * CT * 64 * sizeof(double));
   rom_allow_smem(tall_atb_kernel<TPW, CT, KSPLIT>);

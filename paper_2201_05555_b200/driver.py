@@ -186,8 +186,11 @@ class DeviceGradient:
 
     def dense(self):
         N = self.u.shape[0] // 2
-        zd = torch.from_numpy(self.z).to("cuda")
-        return torch.cat([self.e, self.u[N:] @ zd], dim=0)
+        out = torch.empty((2 * N, self.z.shape[1]), dtype=torch.float64, device="cuda")
+        out[:N].copy_(self.e)
+        for j in range(0, self.z.shape[1], 32):              # U_V z, 32 columns per combine
+            _tall.combine([(self.u[N:], self.z[:, j:j + 32], False)], out=out[N:, j:j + 32])
+        return out
 
 
 def exact_gradients_device(system, ud, z, cols=None, harvest=True):

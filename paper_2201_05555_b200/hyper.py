@@ -472,8 +472,7 @@ def fit_deim_device(window, dim, charge, prev=None, full=True, n_update=None,
     keep = None
     if (not full and prev is not None and prev.dim == d_eff and n_update is not None
             and n_update < d_eff):
-        both = _tall.gram([(psi, False), (prev.psi, False)])
-        align = np.abs(np.diag(both[:d_eff, d_eff:]))
+        align = np.abs(np.diag(_tsq(psi, prev.psi)))
         order = np.argsort(align)
         refresh = {int(i) for i in (order[::-1] if printed_ranking else order)[:n_update]}
         keep = {k: int(prev.indices[k]) for k in range(d_eff) if k not in refresh}

@@ -37,9 +37,9 @@ def wrap(mod, name, label=None):
     setattr(mod, name, w)
 
 
-for mod, names in ((hyper, ["_window_svd", "_orthonormalize", "_tsq", "_greedy_device", "_rows",
+for mod, names in ((hyper, ["_window_svd", "_orth_factor", "_tsq", "_mul", "svd", "_greedy_device", "_rows",
                             "fit_parametric_dmd", "fit_deim_device", "make_hyper_stage_device"]),
-                   (hyper.DeimWindow, ["append"]),
+                   (hyper.DeimWindow, ["append", "eigh"]),
                    (driver, ["exact_gradients_device", "prk2_step", "orthosymplectic_residuals"]),
                    (reduction, ["basis_velocity", "retraction", "tangent_velocity", "SMatrix"]),
                    (reduction.DeviceFixedPoint, ["__call__"])):
