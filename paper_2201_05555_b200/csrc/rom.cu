@@ -834,10 +834,13 @@ __host__ __device__ inline int atb_pitch(int w) {
 template <int TPW, int CT, bool KSPLIT>
 __global__ void __launch_bounds__(256, 1)
 tall_atb_kernel(const double* __restrict__ A, int lda, int ca, const double* __restrict__ B,
-                int ldb, int k, long long N, double* seg) {
+                int ldb, int k, long long N, double* seg, int pa, int pb) {
   extern __shared__ __align__(128) double tsm[];
   constexpr int TG = KSPLIT ? 4 * ATG : ATG;
-  const int pa = atb_pitch(ca), pb = atb_pitch(k);
+  // smem pitches: atb_pitch (per-row copies), or the natural width of a
+  // row-contiguous operand (pa == ca == lda: ONE bulk copy per tile -- the
+  // k-split variant's tiles are small, 2 x 64 row copies of 384 bytes would
+  // cost more than its DMMAs)
   const int SZ = TG * (pa + pb);
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm + 2 * SZ);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -859,9 +862,17 @@ tall_atb_kernel(const double* __restrict__ A, int lda, int ca, const double* __r
     double* st = tsm + (t & 1) * SZ;
     if (lane == 0) mbar_expect_tx(&full[t & 1], (uint32_t)rows * (uint32_t)(ca + k) * 8u);
     __syncwarp();
-    for (int r = lane; r < rows; r += 32) {
-      bulk_g2s(st + r * pa, A + (size_t)(r0 + r) * lda, (uint32_t)ca * 8u, &full[t & 1]);
-      bulk_g2s(st + TG * pa + r * pb, B + (size_t)(r0 + r) * ldb, (uint32_t)k * 8u, &full[t & 1]);
+    if (pa == ca && lda == ca) {
+      if (lane == 0) bulk_g2s(st, A + (size_t)r0 * lda, (uint32_t)rows * (uint32_t)ca * 8u, &full[t & 1]);
+    } else {
+      for (int r = lane; r < rows; r += 32)
+        bulk_g2s(st + r * pa, A + (size_t)(r0 + r) * lda, (uint32_t)ca * 8u, &full[t & 1]);
+    }
+    if (pb == k && ldb == k) {
+      if (lane == 0) bulk_g2s(st + TG * pa, B + (size_t)r0 * ldb, (uint32_t)rows * (uint32_t)k * 8u, &full[t & 1]);
+    } else {
+      for (int r = lane; r < rows; r += 32)
+        bulk_g2s(st + TG * pa + r * pb, B + (size_t)(r0 + r) * ldb, (uint32_t)k * 8u, &full[t & 1]);
     }
   };
   double acc[TPW][CT][2];
@@ -1584,7 +1595,10 @@ int rom_grid_mma(long long N, int p, int per_sm) {
   long long g = std::max(1LL, (long long)picrom_num_sms() * per_sm / tiles);
   return (int)std::min<long long>(g, std::max<long long>(1, N / 64));
 }
-constexpr int kGatherMmaPerSm = 3;   // 79 registers x 256 threads: 3 CTAs per SM
+#ifndef PICROM_GATHER_PER_SM
+#define PICROM_GATHER_PER_SM 3
+#endif
+constexpr int kGatherMmaPerSm = PICROM_GATHER_PER_SM;   // CTAs per SM of the gather wave (3 measured best)
 
 // kernel-path switches are compile time only (tools/build_variant.py -D...),
 // never environment-dependent: the DMMA F-evaluation kernels are the default
@@ -2131,10 +2145,12 @@ template <int TPW, int CT, bool KSPLIT>
 static int launch_tall_atb(const double* a, int lda, int ca, const double* b, int ldb, int k,
                            long long N, double* seg, int G, cudaStream_t s) {
   const int tg = KSPLIT ? 4 * ATG : ATG;
-  size_t sm = (size_t)2 * tg * (atb_pitch(ca) + atb_pitch(k)) * sizeof(double) + 2 * sizeof(uint64_t);
+  const int pa = (KSPLIT && lda == ca) ? ca : atb_pitch(ca);
+  const int pb = (KSPLIT && ldb == k) ? k : atb_pitch(k);
+  size_t sm = (size_t)2 * tg * (pa + pb) * sizeof(double) + 2 * sizeof(uint64_t);
   sm = std::max(sm, (size_t)TPW * CT * 64 * sizeof(double));
   rom_allow_smem(tall_atb_kernel<TPW, CT, KSPLIT>);
-  tall_atb_kernel<TPW, CT, KSPLIT><<<G, 256, sm, s>>>(a, lda, ca, b, ldb, k, N, seg);
+  tall_atb_kernel<TPW, CT, KSPLIT><<<G, 256, sm, s>>>(a, lda, ca, b, ldb, k, N, seg, pa, pb);
   return picrom_check_launch("tall_atb_kernel");
 }
 
@@ -2411,9 +2427,9 @@ extern "C" int picrom_deim_greedy(const double* psi, int ld, long long N, int d,
 // Combine with a wide term (a_t > 32, e.g. the N x p' field block E times a
 // p' x n matrix in the basis velocity): A streams from global straight into
 // DMMA fragments (lane (g, t) reads row g, column 4 ks + t: every 32-byte
-// sector read once), M sits in smem with a pitch = 4 mod 16 (conflict-free B
-// fragments), and a warp owns 32 rows = 4 row blocks x TBO column tiles of
-// independent accumulators.
+// sector read once), M sits in smem with a pitch = 1 mod 4 (conflict-free B
+// fragments under the permuted k order), and a warp owns 16 rows = 2 row
+// blocks x TBO column tiles of independent accumulators.
 constexpr int WRB = 2;          // 8-row blocks per warp chunk
 template <int TBO>
 __global__ void __launch_bounds__(256, 2) wide_combine_kernel(Terms t, const double* mats,
@@ -2520,8 +2536,12 @@ static int launch_wide_combine(const Terms& t, const double* mats, long long N, 
   int K = 0;
   for (int i = 0; i < t.nt; ++i) K += (t.a[i] + 3) & ~3;
   const int tbo = (t.c + 7) / 8;
-  int cp = 8 * tbo;
-  while (cp % 16 != 4) ++cp;
+  // M pitch = 1 mod 4: with the permuted k order a lane (g, tq) reads M row
+  // 4 tq + ks, so the four tq groups must land 4 double-banks apart (4 tq cp =
+  // 4 tq mod 16) -- each bank twice, the 2-wavefront minimum of a 256-byte
+  // request (a pitch = 4 mod 16 put all four groups on the same banks: ncu
+  // counted 74 % of the kernel's smem wavefronts as conflicts)
+  const int cp = 8 * tbo + 1;
   const size_t sm = (size_t)K * cp * sizeof(double);
   if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
   const long long chunks = (N + 8 * WRB - 1) / (8 * WRB);
