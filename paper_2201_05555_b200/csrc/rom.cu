@@ -2430,11 +2430,15 @@ extern "C" int picrom_deim_greedy(const double* psi, int ld, long long N, int d,
 // sector read once), M sits in smem with a pitch = 1 mod 4 (conflict-free B
 // fragments under the permuted k order), and a warp owns 16 rows = 2 row
 // blocks x TBO column tiles of independent accumulators.
-constexpr int WRB = 2;          // 8-row blocks per warp chunk
+// WRB 8-row blocks per warp chunk: 2, or 4 for the 40/48-column outputs (their M
+// fills the smem of a whole SM, so one CTA per SM may use 255 registers: twice
+// the independent DMMA chains per B-fragment load)
+template <int TBO> __host__ __device__ constexpr int wide_wrb() { return TBO >= 5 ? 4 : 2; }
 template <int TBO>
-__global__ void __launch_bounds__(256, 2) wide_combine_kernel(Terms t, const double* mats,
+__global__ void __launch_bounds__(256, TBO >= 5 ? 1 : 2) wide_combine_kernel(Terms t, const double* mats,
                                                            long long N, int cp) {
   extern __shared__ __align__(16) double wsm[];
+  constexpr int WRB = wide_wrb<TBO>();
   int koff[MAXTERM + 1];
   koff[0] = 0;
   for (int i = 0; i < t.nt; ++i) koff[i + 1] = koff[i] + ((t.a[i] + 3) & ~3);
@@ -2544,8 +2548,10 @@ static int launch_wide_combine(const Terms& t, const double* mats, long long N, 
   const int cp = 8 * tbo + 1;
   const size_t sm = (size_t)K * cp * sizeof(double);
   if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "combine matrices too large");
+  const int WRB = tbo >= 5 ? 4 : 2;
   const long long chunks = (N + 8 * WRB - 1) / (8 * WRB);
-  const int G = (int)std::max<long long>(1, std::min<long long>(2LL * picrom_num_sms(), (chunks + 7) / 8));
+  const long long per_sm = tbo >= 5 ? 1 : 2;      // resident CTAs (one wave: M is staged once per CTA)
+  const int G = (int)std::max<long long>(1, std::min<long long>(per_sm * picrom_num_sms(), (chunks + 7) / 8));
   switch (tbo) {
     case 1: rom_allow_smem(wide_combine_kernel<1>); wide_combine_kernel<1><<<G, 256, sm, s>>>(t, mats, N, cp); break;
     case 2: rom_allow_smem(wide_combine_kernel<2>); wide_combine_kernel<2><<<G, 256, sm, s>>>(t, mats, N, cp); break;
