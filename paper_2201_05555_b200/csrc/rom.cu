@@ -1342,20 +1342,55 @@ __global__ void __launch_bounds__(DWT * 32, DWT == DW ? 1 : 4) rom_deposit_mma_k
         double w[2 * RB][D + 1];
         unsigned int hrow[2 * RB];
         bool act[2 * RB];
+        if constexpr (FULL) {
+          // straight-line common path: all elements located with no per-element
+          // branch, rare inputs fixed up behind one warp vote
+          int cell[2 * RB];
+          double f[2 * RB];
+          bool rare[2 * RB], any_rare = false;
+#pragma unroll
+          for (int e = 0; e < 2 * RB; ++e) {
+            act[e] = true;
+            locate_scaled(xv[e], mask, cell[e], f[e], rare[e]);
+            any_rare |= rare[e];
+          }
+          if (__any_sync(0xffffffffu, any_rare)) {
+#pragma unroll
+            for (int e = 0; e < 2 * RB; ++e) {
+              if (!(rare[e] && active)) continue;
+              if (!isfinite(xv[e])) {
+                record_bad(a.status, 0, t0 + rb0 + 8 * (e >> 1) + 2 * t + (e & 1), c, a.p);
+                cell[e] = 0;
+                f[e] = 0.0;
+                act[e] = false;
+              } else {
+                locate_scaled_exact(xv[e], nx, inv_nx, cell[e], f[e]);
+              }
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 2 * RB; ++e) {
+            Spline<D>::weights(f[e], w[e]);
+            if (!act[e]) {                 // non-finite position: deposits nothing
+#pragma unroll
+              for (int m = 0; m <= D; ++m) w[e][m] = 0.0;
+            }
+            hrow[e] = hbase + (unsigned int)cell[e] * (unsigned int)(HS * 8);
+          }
+        } else {
 #pragma unroll
         for (int e = 0; e < 2 * RB; ++e) {
           const int row = rb0 + 8 * (e >> 1) + 2 * t + (e & 1);
-          act[e] = FULL ? active : (active && row < rows);
+          act[e] = active && row < rows;
           const double x = xv[e];
           int cell;
           double f;
           bool rare;
           locate_scaled(x, mask, cell, f, rare);
-          bool dead = false;
           if (act[e] && rare) {
             if (!isfinite(x)) {
               record_bad(a.status, 0, t0 + row, c, a.p);
-              dead = true;
+              act[e] = false;
               cell = 0;
               f = 0.0;
             } else {
@@ -1363,16 +1398,8 @@ __global__ void __launch_bounds__(DWT * 32, DWT == DW ? 1 : 4) rom_deposit_mma_k
             }
           }
           Spline<D>::weights(f, w[e]);
-          if constexpr (FULL) {
-            if (dead) {
-#pragma unroll
-              for (int m = 0; m <= D; ++m) w[e][m] = 0.0;
-            }
-            hrow[e] = hbase + (unsigned int)cell * (unsigned int)(HS * 8);
-          } else {
-            act[e] = act[e] && !dead;
-            hrow[e] = hbase + (unsigned int)(act[e] ? cell : 0) * (unsigned int)(HS * 8);
-          }
+          hrow[e] = hbase + (unsigned int)(act[e] ? cell : 0) * (unsigned int)(HS * 8);
+        }
         }
         // lanes t = 0, 2 then t = 1, 3 (the two lanes of a histogram)
 #pragma unroll
@@ -1486,11 +1513,72 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
     for (int rb = 0; rb < nrows; rb += 8) {
       double xv[2], ev[2];
       recon_block<NK, !(FULL && EX)>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
+      // field (and optional harvest) of one located element; cfe = the column's
+      // coefficient, or 0 for an element that must contribute nothing
+      auto eval_at = [&](int cell, double f, double cfe, long long i, bool store) {
+        double pv[D + 1];
+        const double* pc = phs + (cell + Spline<D>::OFF + D) * PS + cl;
+#pragma unroll
+        for (int m = 0; m <= D; ++m) pv[m] = pc[m * PS];
+        double E;
+        if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
+          E = __dmul_rn(cfe, __dadd_rn(__dmul_rn(-gi, pv[0]), __dmul_rn(gi, pv[1])));
+        } else {
+          double dw[D + 1];
+          Spline<D>::dweights(f, gi, dw);
+          double sacc = 0.0;
+#pragma unroll
+          for (int m = 0; m <= D; ++m) sacc = fma(dw[m], pv[m], sacc);
+          E = cfe * sacc;
+        }
+        if (store && a.eout) a.eout[(size_t)i * a.ldo + c] = E;
+        if (store && a.lam) {
+          double lv;
+          if constexpr (D == 1) {
+            lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
+          } else {
+            double w[D + 1];
+            Spline<D>::weights(f, w);
+            lv = 0.0;
+#pragma unroll
+            for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
+          }
+          a.lam[(size_t)i * a.ldo + c] = lv;
+        }
+        return E;
+      };
+      if constexpr (FULL) {
+        // straight-line common path: both elements located and evaluated with no
+        // per-element branch; rare inputs are fixed up behind one warp vote.  An
+        // inactive column (z = 0 -> x = 0) reads its zero-filled phi column.
+        int cell[2];
+        double f[2], cfe[2] = {cf, cf};
+        bool rare[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) locate_scaled(xv[e], mask, cell[e], f[e], rare[e]);
+        if (__any_sync(0xffffffffu, rare[0] || rare[1])) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (!(rare[e] && active)) continue;
+            if (!isfinite(xv[e])) {
+              record_bad(a.status, 0, t0 + rb + 2 * t + e, c, a.p);
+              cell[e] = 0;
+              f[e] = 0.0;
+              cfe[e] = 0.0;
+            } else {
+              locate_scaled_exact(xv[e], nx, inv_nx, cell[e], f[e]);
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          ev[e] = eval_at(cell[e], f[e], cfe[e], t0 + rb + 2 * t + e, active);
+      } else {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         ev[e] = 0.0;
         const int row = rb + 2 * t + e;
-        if (!active || (!FULL && row >= rows)) continue;
+        if (!active || row >= rows) continue;
         const double x = xv[e];
         const long long i = t0 + row;
         int cell;
@@ -1504,36 +1592,8 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
           }
           locate_scaled_exact(x, nx, inv_nx, cell, f);
         }
-        double pv[D + 1];
-        const double* pc = phs + (cell + Spline<D>::OFF + D) * PS + cl;
-#pragma unroll
-        for (int m = 0; m <= D; ++m) pv[m] = pc[m * PS];
-        double E;
-        if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
-          E = __dmul_rn(cf, __dadd_rn(__dmul_rn(-gi, pv[0]), __dmul_rn(gi, pv[1])));
-        } else {
-          double dw[D + 1];
-          Spline<D>::dweights(f, gi, dw);
-          double sacc = 0.0;
-#pragma unroll
-          for (int m = 0; m <= D; ++m) sacc = fma(dw[m], pv[m], sacc);
-          E = cf * sacc;
-        }
-        ev[e] = E;
-        if (a.eout) a.eout[(size_t)i * a.ldo + c] = E;
-        if (a.lam) {
-          double lv;
-          if constexpr (D == 1) {
-            lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
-          } else {
-            double w[D + 1];
-            Spline<D>::weights(f, w);
-            lv = 0.0;
-#pragma unroll
-            for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
-          }
-          a.lam[(size_t)i * a.ldo + c] = lv;
-        }
+        ev[e] = eval_at(cell, f, cf, i, true);
+      }
       }
       // projection: acc (basis m = 8 mt + g, columns 2t, 2t+1) += U_blk^T E_blk;
       // B fragment E[rb + 4 ks + t][column g] lives in lane 4 g + 2 ks + t/2
