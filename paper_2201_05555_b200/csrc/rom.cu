@@ -1330,7 +1330,10 @@ __global__ void __launch_bounds__(DWT * 32, DWT == DW ? 1 : 4) rom_deposit_mma_k
     // an inactive column (z = 0 -> x = 0) deposits into its own never-read
     // histogram, a non-finite position deposits zero weights, so the deposit
     // predicate is the lane's phase alone.
-    constexpr int RB = 2;
+#ifndef PICROM_DEP_RB
+#define PICROM_DEP_RB 2
+#endif
+    constexpr int RB = PICROM_DEP_RB;
     auto run_tile = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
       const int nrows = FULL ? TR : rows;

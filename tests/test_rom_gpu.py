@@ -82,6 +82,20 @@ def test_exact_gradients_vs_oracle(m, d, per_instance):
     assert rel(g_stage, o_stage) <= 1e-12
 
 
+@pytest.mark.parametrize("p", [20, 33, 70, 130])
+def test_exact_gradients_column_tilings(m, p):
+    """The F-evaluation kernels pick their CTA shape from the column count: 4-warp
+    / 32-column CTAs for p' <= 32 (the hyper-reduced subsample), 16-warp deposit
+    and 8-warp gather CTAs above, with partly filled and multiple column tiles;
+    full and ragged row tiles (N not a multiple of 64)."""
+    u, z, osys, gsys, *_ = _setup(m, 2, True, n=2500, p=p, nx=32, nb=8, seed=p)
+    og, ophi, olam = orl.exact_gradients(osys, u, z)
+    gg, gphi, glam = m.driver.exact_gradients(gsys, u, z)
+    assert rel(gphi, ophi) <= 1e-12
+    assert rel(gg, og) <= 1e-12
+    assert rel(glam, olam) <= 1e-12
+
+
 def test_reduced_run_no_hyper_vs_reference(m, g):
     L, nx = float(g["length"]), int(g["nx"])
     mesh = m.fem.build_mesh(L, nx)
