@@ -1238,6 +1238,10 @@ __global__ void deim_gather_kernel(const double* uxd, const double* z, int ldz, 
 // pipe on B200 (profiles/r01b/fp64_peak.log: 37.2 vs 36.4 TF/s, 30.8 mixed):
 // the gain is issue slots -- 5 DMMA per 64 units instead of 1280 DFMA.
 constexpr int MW = 8;            // warps per CTA
+#ifndef PICROM_GATHER_PER_SM
+#define PICROM_GATHER_PER_SM 3
+#endif
+constexpr int kGatherMmaPerSm = PICROM_GATHER_PER_SM;   // CTAs per SM of the gather wave (3 measured best)
 constexpr int MC = MW * 8;       // z columns per CTA
 
 __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
@@ -1442,7 +1446,7 @@ __global__ void __launch_bounds__(DWT * 32, DWT == DW ? 1 : 4) rom_deposit_mma_k
 // MWT warps per CTA: MW, or 4 (32 columns) for the few subsample columns of the
 // hyper-reduced model (see rom_deposit_mma_kernel)
 template <int D, int NK, bool VPROJ, bool EX, int MWT>
-__global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
+__global__ void __launch_bounds__(MWT * 32, MWT == MW ? (VPROJ ? 2 : kGatherMmaPerSm) : 4) rom_gather_mma_kernel(RomArgs a) {
   constexpr int MCT = MWT * 8;
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
@@ -1473,7 +1477,9 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
   const double cf = a.coef_kind == 0 ? ip[I_GCOEF] : 1.0;
   const double inv_nx = 1.0 / (double)nx;
   const int mask = pow2_mask(nx);
-  double za[NK], acc[NM][2], accv[NM][2];
+  // acc / accv: projections of even row blocks; acc1 / accv1: odd row blocks of
+  // full tiles (two independent DMMA chains per lane), summed at the end
+  double za[NK], acc[NM][2], accv[NM][2], acc1[NM][2], accv1[NM][2];
 #pragma unroll
   for (int ks = 0; ks < NK; ++ks) {
     const int k = ks * 4 + t;
@@ -1481,7 +1487,10 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
     za[ks] = (active && k < n) ? a.z[(size_t)k * a.ldz + c] * inv_h : 0.0;
   }
 #pragma unroll
-  for (int mt = 0; mt < NM; ++mt) acc[mt][0] = acc[mt][1] = accv[mt][0] = accv[mt][1] = 0.0;
+  for (int mt = 0; mt < NM; ++mt) {
+    acc[mt][0] = acc[mt][1] = accv[mt][0] = accv[mt][1] = 0.0;
+    acc1[mt][0] = acc1[mt][1] = accv1[mt][0] = accv1[mt][1] = 0.0;
+  }
   const long long lo = row_start(blockIdx.x, a.N, gridDim.x);
   const long long hi = row_start(blockIdx.x + 1, a.N, gridDim.x);
   const int ntiles = (int)((hi - lo + TR - 1) / TR);
@@ -1513,58 +1522,89 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
     auto run_tile = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
     const int nrows = FULL ? TR : rows;
-    for (int rb = 0; rb < nrows; rb += 8) {
-      double xv[2], ev[2];
-      recon_block<NK, !(FULL && EX)>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
-      // field (and optional harvest) of one located element; cfe = the column's
-      // coefficient, or 0 for an element that must contribute nothing
-      auto eval_at = [&](int cell, double f, double cfe, long long i, bool store) {
-        double pv[D + 1];
-        const double* pc = phs + (cell + Spline<D>::OFF + D) * PS + cl;
+    // field (and optional harvest) of one located element; cfe = the column's
+    // coefficient, or 0 for an element that must contribute nothing
+    auto eval_at = [&](int cell, double f, double cfe, long long i, bool store) {
+      double pv[D + 1];
+      const double* pc = phs + (cell + Spline<D>::OFF + D) * PS + cl;
 #pragma unroll
-        for (int m = 0; m <= D; ++m) pv[m] = pc[m * PS];
-        double E;
-        if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
-          E = __dmul_rn(cfe, __dadd_rn(__dmul_rn(-gi, pv[0]), __dmul_rn(gi, pv[1])));
+      for (int m = 0; m <= D; ++m) pv[m] = pc[m * PS];
+      double E;
+      if constexpr (D == 1) {   // coef * ((-g)*phi0 + g*phi1): driver.py:74-75 order
+        E = __dmul_rn(cfe, __dadd_rn(__dmul_rn(-gi, pv[0]), __dmul_rn(gi, pv[1])));
+      } else {
+        double dw[D + 1];
+        Spline<D>::dweights(f, gi, dw);
+        double sacc = 0.0;
+#pragma unroll
+        for (int m = 0; m <= D; ++m) sacc = fma(dw[m], pv[m], sacc);
+        E = cfe * sacc;
+      }
+      if (store && a.eout) a.eout[(size_t)i * a.ldo + c] = E;
+      if (store && a.lam) {
+        double lv;
+        if constexpr (D == 1) {
+          lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
         } else {
-          double dw[D + 1];
-          Spline<D>::dweights(f, gi, dw);
-          double sacc = 0.0;
+          double w[D + 1];
+          Spline<D>::weights(f, w);
+          lv = 0.0;
 #pragma unroll
-          for (int m = 0; m <= D; ++m) sacc = fma(dw[m], pv[m], sacc);
-          E = cfe * sacc;
+          for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
         }
-        if (store && a.eout) a.eout[(size_t)i * a.ldo + c] = E;
-        if (store && a.lam) {
-          double lv;
-          if constexpr (D == 1) {
-            lv = __dadd_rn(__dmul_rn(__dsub_rn(1.0, f), pv[0]), __dmul_rn(f, pv[1]));
-          } else {
-            double w[D + 1];
-            Spline<D>::weights(f, w);
-            lv = 0.0;
+        a.lam[(size_t)i * a.ldo + c] = lv;
+      }
+      return E;
+    };
+    // projection of one row block: accp (basis m = 8 mt + g, columns 2t, 2t+1)
+    // += U_blk^T E_blk; B fragment E[rb + 4 ks + t][column g] lives in lane
+    // 4 g + 2 ks + t/2
+    auto project = [&](int rb, const double* ev, double (*accp)[2], double (*accvp)[2]) {
 #pragma unroll
-            for (int m = 0; m <= D; ++m) lv = fma(w[m], pv[m], lv);
+      for (int ks = 0; ks < 2; ++ks) {
+        const int src = g * 4 + 2 * ks + (t >> 1);
+        const double s0 = __shfl_sync(0xffffffffu, ev[0], src);
+        const double s1 = __shfl_sync(0xffffffffu, ev[1], src);
+        const double b = (t & 1) ? s1 : s0;
+        const int ur = rb + 4 * ks + t;
+#pragma unroll
+        for (int mt = 0; mt < NM; ++mt) {
+          const int m = mt * 8 + g;
+          const double av = ((FULL || ur < rows) && m < n) ? tile[ur * n + m] : 0.0;
+          dmma_f64(accp[mt][0], accp[mt][1], av, b);
+        }
+        if constexpr (VPROJ) {
+#pragma unroll
+          for (int mt = 0; mt < NM; ++mt) {
+            const int m = mt * 8 + g;
+            const double av = ((FULL || ur < rows) && m < n) ? vtile[ur * n + m] : 0.0;
+            dmma_f64(accvp[mt][0], accvp[mt][1], av, b);
           }
-          a.lam[(size_t)i * a.ldo + c] = lv;
         }
-        return E;
-      };
-      if constexpr (FULL) {
-        // straight-line common path: both elements located and evaluated with no
-        // per-element branch; rare inputs are fixed up behind one warp vote.  An
-        // inactive column (z = 0 -> x = 0) reads its zero-filled phi column.
-        int cell[2];
-        double f[2], cfe[2] = {cf, cf};
-        bool rare[2];
+      }
+    };
+    if constexpr (FULL) {
+      // two row blocks per pass: two independent reconstruct chains and two
+      // accumulator sets; straight-line common path (all four elements located
+      // and evaluated with no per-element branch), rare inputs fixed up behind
+      // one warp vote.  An inactive column (z = 0 -> x = 0) reads its
+      // zero-filled phi column.
+      static_assert(TR % 16 == 0, "full tiles are walked two row blocks at a time");
+      for (int rb = 0; rb < TR; rb += 16) {
+        double xv[4], ev[4];
+        recon_block<NK, !EX>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
+        recon_block<NK, !EX>(tile, rb + 8, rows, n, za, g, t, xv[2], xv[3]);
+        int cell[4];
+        double f[4], cfe[4] = {cf, cf, cf, cf};
+        bool rare[4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) locate_scaled(xv[e], mask, cell[e], f[e], rare[e]);
-        if (__any_sync(0xffffffffu, rare[0] || rare[1])) {
+        for (int e = 0; e < 4; ++e) locate_scaled(xv[e], mask, cell[e], f[e], rare[e]);
+        if (__any_sync(0xffffffffu, (rare[0] || rare[1]) || (rare[2] || rare[3]))) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
+          for (int e = 0; e < 4; ++e) {
             if (!(rare[e] && active)) continue;
             if (!isfinite(xv[e])) {
-              record_bad(a.status, 0, t0 + rb + 2 * t + e, c, a.p);
+              record_bad(a.status, 0, t0 + rb + 8 * (e >> 1) + 2 * t + (e & 1), c, a.p);
               cell[e] = 0;
               f[e] = 0.0;
               cfe[e] = 0.0;
@@ -1574,9 +1614,15 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
           }
         }
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          ev[e] = eval_at(cell[e], f[e], cfe[e], t0 + rb + 2 * t + e, active);
-      } else {
+        for (int e = 0; e < 4; ++e)
+          ev[e] = eval_at(cell[e], f[e], cfe[e], t0 + rb + 8 * (e >> 1) + 2 * t + (e & 1), active);
+        project(rb, ev, acc, accv);
+        project(rb + 8, ev + 2, acc1, accv1);
+      }
+    } else {
+    for (int rb = 0; rb < nrows; rb += 8) {
+      double xv[2], ev[2];
+      recon_block<NK, true>(tile, rb, rows, n, za, g, t, xv[0], xv[1]);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         ev[e] = 0.0;
@@ -1597,31 +1643,8 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
         }
         ev[e] = eval_at(cell, f, cf, i, true);
       }
-      }
-      // projection: acc (basis m = 8 mt + g, columns 2t, 2t+1) += U_blk^T E_blk;
-      // B fragment E[rb + 4 ks + t][column g] lives in lane 4 g + 2 ks + t/2
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int src = g * 4 + 2 * ks + (t >> 1);
-        const double s0 = __shfl_sync(0xffffffffu, ev[0], src);
-        const double s1 = __shfl_sync(0xffffffffu, ev[1], src);
-        const double b = (t & 1) ? s1 : s0;
-        const int ur = rb + 4 * ks + t;
-#pragma unroll
-        for (int mt = 0; mt < NM; ++mt) {
-          const int m = mt * 8 + g;
-          const double av = ((FULL || ur < rows) && m < n) ? tile[ur * n + m] : 0.0;
-          dmma_f64(acc[mt][0], acc[mt][1], av, b);
-        }
-        if constexpr (VPROJ) {
-#pragma unroll
-          for (int mt = 0; mt < NM; ++mt) {
-            const int m = mt * 8 + g;
-            const double av = ((FULL || ur < rows) && m < n) ? vtile[ur * n + m] : 0.0;
-            dmma_f64(accv[mt][0], accv[mt][1], av, b);
-          }
-        }
-      }
+      project(rb, ev, acc, accv);
+    }
     }
     };
     if (rows == TR) run_tile(std::true_type{});
@@ -1636,8 +1659,8 @@ __global__ void __launch_bounds__(MWT * 32) rom_gather_mma_kernel(RomArgs a) {
       const int m = mt * 8 + g;
       const int col = blockIdx.y * MCT + warp * 8 + 2 * t + e;
       if (m < n && col < a.p) {
-        a.seg[((size_t)blockIdx.x * a.p + col) * n + m] = acc[mt][e];
-        if constexpr (VPROJ) a.seg2[((size_t)blockIdx.x * a.p + col) * n + m] = accv[mt][e];
+        a.seg[((size_t)blockIdx.x * a.p + col) * n + m] = acc[mt][e] + acc1[mt][e];
+        if constexpr (VPROJ) a.seg2[((size_t)blockIdx.x * a.p + col) * n + m] = accv[mt][e] + accv1[mt][e];
       }
     }
 }
@@ -1658,10 +1681,6 @@ int rom_grid_mma(long long N, int p, int per_sm) {
   long long g = std::max(1LL, (long long)picrom_num_sms() * per_sm / tiles);
   return (int)std::min<long long>(g, std::max<long long>(1, N / 64));
 }
-#ifndef PICROM_GATHER_PER_SM
-#define PICROM_GATHER_PER_SM 3
-#endif
-constexpr int kGatherMmaPerSm = PICROM_GATHER_PER_SM;   // CTAs per SM of the gather wave (3 measured best)
 
 // kernel-path switches are compile time only (tools/build_variant.py -D...),
 // never environment-dependent: the DMMA F-evaluation kernels are the default
