@@ -10,7 +10,7 @@ export_rep() {   # $1 = report stem under gpurun_out/
 }
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_full.log
+SECONDS=0; timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$? wall=${SECONDS}s" >> gpurun_out/bench_full.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
 timeout 600 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --no-rom > gpurun_out/bench_c5.log 2>&1
 timeout 600 python bench.py --config C1 --steps 20 --warmup 3 --no-cpu-baseline --no-rom > gpurun_out/bench_c1.log 2>&1
@@ -22,10 +22,6 @@ timeout 900 $NCU --set full --import-source on --clock-control none -k regex:tal
 export_rep tall_atb_c4
 timeout 900 $NCU --set full --import-source on --clock-control none -k regex:wide_combine_kernel -s 3 -c 1 -o gpurun_out/wide_combine6_c4 -f python tools/prof_window_svd.py > gpurun_out/ncu_wide_combine.log 2>&1
 export_rep wide_combine6_c4
-for v in default g4; do
-  if [ "$v" = default ]; then lib=""; else lib="PICROM_LIB=paper_2201_05555_b200/variants/libpicrom_$v.so"; fi
-  echo "== $v micro_rom" >> gpurun_out/micro_variants.log
-  env $lib timeout 300 python tools/micro_rom.py >> gpurun_out/micro_variants.log 2>&1
-done
+timeout 300 python tools/micro_rom.py > gpurun_out/micro_rom.log 2>&1
 timeout 600 python tools/prof_window_svd.py > gpurun_out/prof_window_svd.log 2>&1
 echo done
