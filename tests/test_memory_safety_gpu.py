@@ -186,3 +186,40 @@ def test_rom_kernels_and_greedy_guards(m):
     from oracle import dmd_deim as odd
     np.testing.assert_array_equal(got, odd.greedy_indices(psi.cpu().numpy(), keep={3: 11}))
     np.testing.assert_array_equal(rows.t.cpu().numpy().reshape(d, d), psi.cpu().numpy()[got])
+
+
+@pytest.mark.parametrize("ca,k", [(420, 48), (46, 46), (22, 6)])
+def test_tall_atb_and_wide_combine_guards(m, ca, k):
+    """picrom_tall_atb (both kernel variants) and the 40/48-column wide combine
+    write only inside their outputs / workspace, also with a ragged last tile,
+    and repeat bit for bit."""
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(ca + k)
+    rows = 4099
+    a = torch.from_numpy(rng.standard_normal((rows, ca))).cuda()
+    b = torch.from_numpy(rng.standard_normal((rows, k))).cuda()
+    need = int(m.lib.query("picrom_tall_atb_workspace_bytes", rows, ca, k))
+    res = []
+    for rep in range(2):
+        ws = Guarded((need + 7) // 8)
+        out = Guarded(ca * k)
+        m.lib.call("picrom_tall_atb", a.data_ptr(), ca, ca, b.data_ptr(), k, k, rows, out.ptr, ws.ptr,
+                   m.dev.stream_handle())
+        torch.cuda.synchronize()
+        assert ws.intact() and out.intact()
+        res.append(out.t.cpu().numpy().reshape(ca, k))
+    np.testing.assert_array_equal(res[0], res[1])
+    ref = a.cpu().numpy().T @ b.cpu().numpy()
+    assert np.abs(res[0] - ref).max() <= 1e-12 * np.abs(ref).max()
+    # combine into a guarded (rows x k) block with a wider row stride
+    mat = rng.standard_normal((ca, k))
+    ldo = k + 6
+    outc = Guarded(rows * ldo, fill=7.0)
+    view = outc.t.view(rows, ldo)[:, :k]
+    _tall.combine([(a, mat, False)], out=view)
+    torch.cuda.synchronize()
+    assert outc.intact()
+    full = outc.t.view(rows, ldo).cpu().numpy()
+    assert (full[:, k:] == 7.0).all()                      # pad columns untouched
+    refc = a.cpu().numpy() @ mat
+    assert np.abs(full[:, :k] - refc).max() <= 1e-12 * np.abs(refc).max()
