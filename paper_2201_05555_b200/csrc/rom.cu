@@ -357,12 +357,32 @@ __global__ void __launch_bounds__(384) rom_gather_kernel(RomArgs a) {
 }
 
 // out[c][k] (and optional transpose layout) = sum_b seg[b][c][k]
-__global__ void seg_sum_kernel(const double* seg, int G, int rows, double* out, int out_ld,
-                               int transpose, int width, const long long* skip = nullptr) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= rows || (skip && *skip)) return;
-  double s = 0.0;
-  for (int b = 0; b < G; ++b) s += seg[(size_t)b * rows + q];
+// 256 threads = 64 entries x 4 slices of the G partials; a thread sums its
+// slice (b = slice, slice + 4, ...) with 8 loads in flight, the 4 slices are
+// combined through smem -- a fixed order (deterministic), and ~G/32 dependent
+// L2 round trips instead of ~G/4: this kernel sits behind every F-evaluation
+// and Gram and is pure latency
+constexpr int SEGQ = 64;
+__global__ void __launch_bounds__(256)
+seg_sum_kernel(const double* seg, int G, int rows, double* out, int out_ld,
+               int transpose, int width, const long long* skip = nullptr) {
+  if (skip && *skip) return;
+  __shared__ double part[4][SEGQ];
+  const int ql = threadIdx.x & (SEGQ - 1), slice = threadIdx.x / SEGQ;
+  const int q = blockIdx.x * SEGQ + ql;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (q < rows) {
+    int b = slice;
+    for (; b + 28 < G; b += 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += __ldcg(seg + (size_t)(b + 4 * u) * rows + q);
+    }
+    for (int u = 0; b < G; b += 4, ++u) acc[u] += __ldcg(seg + (size_t)b * rows + q);
+  }
+  part[slice][ql] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  __syncthreads();
+  if (slice != 0 || q >= rows) return;
+  const double s = (part[0][ql] + part[1][ql]) + (part[2][ql] + part[3][ql]);
   if (transpose) {  // q = c*width + k  ->  out[k][c]
     const int c = q / width, k = q % width;
     out[(size_t)k * out_ld + c] = s;
@@ -2015,12 +2035,12 @@ static int rom_gather_impl(const double* ux, long long N, int n, const double* z
   if (rc) return rc;
   const int rows = p * n;
   if (g_out) {
-    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg, G, rows, g_out, ldg, 1, n, a.skip);
+    seg_sum_kernel<<<(rows + SEGQ - 1) / SEGQ, 256, 0, s>>>(a.seg, G, rows, g_out, ldg, 1, n, a.skip);
     rc = picrom_check_launch("seg_sum");
     if (rc) return rc;
   }
   if (gv_out) {
-    seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a.seg2, G, rows, gv_out, ldg, 1, n, a.skip);
+    seg_sum_kernel<<<(rows + SEGQ - 1) / SEGQ, 256, 0, s>>>(a.seg2, G, rows, gv_out, ldg, 1, n, a.skip);
     rc = picrom_check_launch("seg_sum");
   }
   return rc;
@@ -2105,7 +2125,7 @@ static int gram_mma_try(const Blocks& b, int na, long long N, void* ws, cudaStre
   const int W = b.off[b.nb];
   const int wa = na > 0 ? b.off[na] : W, wb = na > 0 ? W - b.off[na] : W;
   const int rows = wa * wb;
-  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>((const double*)ws, gy, rows, out, 0, 0, 1);
+  seg_sum_kernel<<<(rows + SEGQ - 1) / SEGQ, 256, 0, s>>>((const double*)ws, gy, rows, out, 0, 0, 1);
   return picrom_check_launch("seg_sum");
 }
 
@@ -2167,7 +2187,7 @@ static int gram_impl(int nblocks, int na, const double* const* ptrs, const int* 
   if (rc) return rc;
   const int rows = wa * wb;
   const int Gp = G * RG;
-  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>((const double*)ws, Gp, rows, out, 0, 0, 1);
+  seg_sum_kernel<<<(rows + SEGQ - 1) / SEGQ, 256, 0, s>>>((const double*)ws, Gp, rows, out, 0, 0, 1);
   return picrom_check_launch("seg_sum");
 }
 
@@ -2260,7 +2280,7 @@ extern "C" int picrom_tall_atb(const double* a, int lda, int ca, const double* b
                  : launch_tall_atb<7, 3, false>(a, lda, ca, b, ldb, k, N, seg, G, s);
   if (rc) return rc;
   const int rows = ca * k;
-  seg_sum_kernel<<<(rows + 255) / 256, 256, 0, s>>>(seg, G, rows, out, 0, 0, 1);
+  seg_sum_kernel<<<(rows + SEGQ - 1) / SEGQ, 256, 0, s>>>(seg, G, rows, out, 0, 0, 1);
   return picrom_check_launch("seg_sum");
 }
 
@@ -2779,15 +2799,26 @@ __global__ void __launch_bounds__(256) fp_update_kernel(const double* gout, cons
                                                        const double* z, double* k, double* zeval,
                                                        int n, int p, double half_dt, double tol,
                                                        int it, long long* state, double* trace) {
-  extern __shared__ double g[];
+  extern __shared__ double g[];        // [n p] g | [n p] z_eval | [n n] C
   __shared__ double red[64];
   if (state[0]) return;
   const int tid = threadIdx.x, np = n * p;
+  // stage z_eval and C first (every load in flight at once: one L2 round trip
+  // instead of one per FMA batch -- the kernel sits between the F-evaluation
+  // launches of every fixed-point iteration and is pure latency)
+  double* zs = g + np;
+  double* cs = zs + np;
   for (int q = tid; q < np; q += blockDim.x) {
-    const int r = q / p, col = q % p;
-    double acc = gout[q];
-    for (int j = 0; j < n; ++j) acc = fma(c[r * n + j], zeval[(size_t)j * p + col], acc);
-    g[q] = acc;
+    zs[q] = zeval[q];
+    g[q] = gout[q];
+  }
+  for (int q = tid; q < n * n; q += blockDim.x) cs[q] = c[q];
+  __syncthreads();
+  for (int q = tid; q < np; q += blockDim.x) {
+    const int r = q / p, col = q - r * p;
+    double acc = g[q];
+    for (int j = 0; j < n; ++j) acc = fma(cs[r * n + j], zs[j * p + col], acc);
+    g[q] = acc;                        // each thread rewrites only its own entries
   }
   __syncthreads();
   const int h = n / 2;
@@ -2835,7 +2866,7 @@ extern "C" int picrom_fp_update(const double* gout, const double* c, const doubl
                                 double* zeval, int n, int p, double half_dt, double tol, int it,
                                 long long* state, double* trace, void* stream) {
   if (n < 2 || (n & 1) || p < 1) return picrom_set_error(PICROM_ERR_CONFIG, "fp_update: bad n / p");
-  const size_t sm = (size_t)n * p * sizeof(double);
+  const size_t sm = ((size_t)2 * n * p + (size_t)n * n) * sizeof(double);
   if (sm > 200 * 1024) return picrom_set_error(PICROM_ERR_CONFIG, "fp_update: n p too large");
   static bool attr = false;
   if (!attr) {
