@@ -294,7 +294,7 @@ def fom_measure(args, w, world, local_rank, e2e_steps=None, steps=None, warmup=N
         # soak (untimed) so the 200 ms nvidia-smi sampler sees the clocks under
         # this exact load; the timed K steps follow immediately
         t_soak = time.perf_counter()
-        while time.perf_counter() - t_soak < 1.0:
+        while time.perf_counter() - t_soak < args.soak_seconds:
             e.launch_block(16)
             torch.cuda.synchronize()
     l2_flush()
@@ -438,6 +438,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--soak-seconds", type=float, default=1.0,
+                    help="untimed steps right before the timed block so nvidia-smi samples the clocks under load")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rom", action="store_true",
                     help="skip the other-config sections (C1/C5 FOM, C3/C4 reduced)")
