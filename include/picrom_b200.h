@@ -272,6 +272,17 @@ size_t picrom_tall_atb_workspace_bytes(long long N, int ca, int k);
 int picrom_tall_atb(const double* a, int lda, int ca, const double* b, int ldb, int k,
                     long long N, double* out, void* workspace, void* stream);
 
+/* Small dense steps of the windowed SVD's Cholesky-QR chain (hyper.py:262), so
+ * that the chain Y -> Y^T Y -> R^-1 -> (W^T Y) R^-1 -> W M stays on the device:
+ * picrom_small_cholinv: g (k x k SPD, k <= 48) -> rinv = R^-1 with g = R^T R (R
+ *   upper triangular); info[0], info[1] = min / max diag(R), min = 0 when g is
+ *   not positive definite;
+ * picrom_small_rmul: out (r x k) = a (r x k) b (k x k), column j times
+ *   colscale[j] (nullable). */
+int picrom_small_cholinv(const double* g, int k, double* rinv, double* info, void* stream);
+int picrom_small_rmul(const double* a, int r, int k, const double* b, const double* colscale,
+                      double* out, void* stream);
+
 /* DEIM greedy selection step (hyper.py:241-244): out_index = the first index
  * of max |v[i*stride]| over i < n with the `banned` indices scored -1;
  * out_value (nullable) = that maximum. */

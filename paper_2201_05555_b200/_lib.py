@@ -55,6 +55,8 @@ SIGNATURES = {
     "picrom_cross_gram": (_i, [_i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp]),
     "picrom_tall_atb_workspace_bytes": (_sz, [_ll, _i, _i]),
     "picrom_tall_atb": (_i, [_vp, _i, _i, _vp, _i, _i, _ll, _vp, _vp, _vp]),
+    "picrom_small_cholinv": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "picrom_small_rmul": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
     "picrom_argmax_abs": (_i, [_vp, _ll, _ll, _vp, _i, _vp, _vp, _vp, _vp]),
     "picrom_deim_workspace_bytes": (_sz, [_ll, _i]),
     "picrom_diff_sumsq": (_i, [_vp, _vp, _ll, _vp, _vp, _vp]),

@@ -88,11 +88,12 @@ def cross_gram(a_blocks, b_blocks):
 _ATB_WS = {}
 
 
-def atb(a, b):
-    """a^T b (host numpy, ca x k) for a WIDE tall device block a (N x ca, even
-    ca <= 448: the DEIM sample window) and a block b (N x k, even k <= 48),
-    picrom_tall_atb.  a and b may be column slices of wider row-major matrices
-    (row strides even, 16-byte aligned rows)."""
+def atb(a, b, to_host=True):
+    """a^T b (host numpy, ca x k; the device tensor with to_host=False) for a
+    WIDE tall device block a (N x ca, even ca <= 448: the DEIM sample window)
+    and a block b (N x k, even k <= 48), picrom_tall_atb.  a and b may be
+    column slices of wider row-major matrices (row strides even, 16-byte
+    aligned rows)."""
     rows = a.shape[0]
     ca, k = int(a.shape[1]), int(b.shape[1])
     if a.stride(1) != 1:
@@ -107,7 +108,46 @@ def atb(a, b):
     out = torch.empty((ca, k), dtype=torch.float64, device="cuda")
     _lib.call("picrom_tall_atb", a.data_ptr(), int(a.stride(0)), ca, b.data_ptr(), int(b.stride(0)), k,
               int(rows), out.data_ptr(), ws.data_ptr(), dev.stream_handle())
-    return _reduced(out).cpu().numpy()
+    out = _reduced(out)
+    return out.cpu().numpy() if to_host else out
+
+
+def combine_dev(block, mat_dev, out=None):
+    """block (N x a, device) @ mat_dev (a x c, DEVICE, contiguous) -> (N x c):
+    picrom_combine with the small matrix already on the device (no upload, no
+    host round trip in a chain of tall products)."""
+    rows, a = block.shape
+    c = int(mat_dev.shape[1])
+    if tuple(mat_dev.shape) != (a, c) or not mat_dev.is_contiguous():
+        raise ConfigurationError("combine_dev: matrix must be a contiguous (width x c) device tensor")
+    if out is None:
+        out = torch.empty((rows, c), dtype=torch.float64, device="cuda")
+    t = block if block.stride(1) == 1 else block.contiguous()
+    _lib.call("picrom_combine", 1, _arr(C.c_void_p, [t.data_ptr()]), _arr(C.c_int, [int(t.stride(0))]),
+              _arr(C.c_int, [int(a)]), _arr(C.c_int, [0]), _arr(C.c_int, [0]), mat_dev.data_ptr(),
+              int(a * c), rows, out.data_ptr(), int(out.stride(0)), c, 0, dev.stream_handle())
+    return out
+
+
+def cholinv_dev(g_dev):
+    """(R^-1, info) on the device for g = R^T R (k x k SPD device tensor, k <= 48);
+    info = [min diag R, max diag R] (picrom_small_cholinv)."""
+    k = int(g_dev.shape[0])
+    rinv = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    info = torch.empty(2, dtype=torch.float64, device="cuda")
+    _lib.call("picrom_small_cholinv", g_dev.data_ptr(), k, rinv.data_ptr(), info.data_ptr(),
+              dev.stream_handle())
+    return rinv, info
+
+
+def rmul_dev(a_dev, b_dev, colscale=None):
+    """a (r x k) @ b (k x k), column j scaled by colscale[j], all on the device
+    (picrom_small_rmul)."""
+    r, k = int(a_dev.shape[0]), int(a_dev.shape[1])
+    out = torch.empty((r, k), dtype=torch.float64, device="cuda")
+    _lib.call("picrom_small_rmul", a_dev.data_ptr(), r, k, b_dev.data_ptr(),
+              None if colscale is None else colscale.data_ptr(), out.data_ptr(), dev.stream_handle())
+    return out
 
 
 def gram_tasks(blocks, tasks):

@@ -972,6 +972,79 @@ tall_atb_kernel(const double* __restrict__ A, int lda, int ca, const double* __r
   }
 }
 
+// ---- small dense algebra of the window SVD's Cholesky-QR chain (hyper.py:262) ----
+//
+// One CTA: G (k x k, SPD, k <= 48) -> R^-1 with G = R^T R (R upper triangular),
+// so Q = Y R^-1 is orthonormal when G = Y^T Y.  info[0], info[1] = min / max of
+// diag(R) (min <= 0: G was not positive definite; the ratio is the caller's
+// conditioning check).  Keeps the chain Y -> Y^T Y -> R^-1 -> (W^T Y) R^-1 -> W M
+// on the device: no host round trip between its tall products.
+constexpr int SMK = 48;
+__global__ void __launch_bounds__(256) small_cholinv_kernel(const double* g, int k, double* rinv,
+                                                            double* info) {
+  __shared__ double a[SMK][SMK + 1];     // lower factor L (G = L L^T), then L^-1
+  __shared__ double li[SMK][SMK + 1];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int q = tid; q < k * k; q += blockDim.x) a[q / k][q % k] = g[q];
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      const double d = a[j][j];
+      if (!(d > 0.0)) bad = 1;
+      a[j][j] = sqrt(d > 0.0 ? d : 1.0);
+    }
+    __syncthreads();
+    const double djj = a[j][j];
+    for (int i = j + 1 + tid; i < k; i += blockDim.x) a[i][j] /= djj;
+    __syncthreads();
+    const int m = k - j - 1;             // trailing lower triangle update
+    for (int q = tid; q < m * m; q += blockDim.x) {
+      const int i = j + 1 + q / m, c = j + 1 + q % m;
+      if (c <= i) a[i][c] = fma(-a[i][j], a[c][j], a[i][c]);
+    }
+    __syncthreads();
+  }
+  // L^-1 by forward substitution, one column per thread
+  for (int c = tid; c < k; c += blockDim.x) {
+    for (int i = 0; i < k; ++i) {
+      double x = i == c ? 1.0 : 0.0;
+      for (int m = c; m < i; ++m) x = fma(-a[i][m], li[m][c], x);
+      li[i][c] = i < c ? 0.0 : x / a[i][i];
+    }
+  }
+  __syncthreads();
+  // R^-1 = (L^T)^-1 = (L^-1)^T
+  for (int q = tid; q < k * k; q += blockDim.x) rinv[q] = li[q % k][q / k];
+  if (tid == 0) {
+    double lo = a[0][0], hi = a[0][0];
+    for (int j = 1; j < k; ++j) { lo = fmin(lo, a[j][j]); hi = fmax(hi, a[j][j]); }
+    info[0] = bad ? 0.0 : lo;
+    info[1] = hi;
+  }
+}
+
+// out (r x k) = A (r x k) B (k x k), column j scaled by colscale[j] (nullable)
+__global__ void __launch_bounds__(SMK) small_rmul_kernel(const double* a, int r, int k,
+                                                         const double* b, const double* colscale,
+                                                         double* out) {
+  __shared__ double bs[SMK][SMK + 1];
+  __shared__ double row[SMK];
+  const int j = threadIdx.x;
+  for (int q = j; q < k * k; q += blockDim.x) bs[q / k][q % k] = b[q];
+  for (int i = blockIdx.x; i < r; i += gridDim.x) {
+    __syncthreads();
+    if (j < k) row[j] = a[(size_t)i * k + j];
+    __syncthreads();
+    if (j < k) {
+      double acc = 0.0;
+      for (int m = 0; m < k; ++m) acc = fma(row[m], bs[m][j], acc);
+      out[(size_t)i * k + j] = colscale ? acc * colscale[j] : acc;
+    }
+  }
+}
+
 // first index of max |v[i*stride]| over i < n, skipping `banned` (numpy
 // argmax tie rule: the smallest index among equal maxima); banned entries
 // score -1 as in hyper.py:241-243.  Two passes: per-CTA (value, index), then
@@ -2282,6 +2355,20 @@ extern "C" int picrom_tall_atb(const double* a, int lda, int ca, const double* b
   const int rows = ca * k;
   seg_sum_kernel<<<(rows + SEGQ - 1) / SEGQ, 256, 0, s>>>(seg, G, rows, out, 0, 0, 1);
   return picrom_check_launch("seg_sum");
+}
+
+extern "C" int picrom_small_cholinv(const double* g, int k, double* rinv, double* info,
+                                    void* stream) {
+  if (k < 1 || k > SMK) return picrom_set_error(PICROM_ERR_CONFIG, "small_cholinv: 1 <= k <= 48");
+  small_cholinv_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(g, k, rinv, info);
+  return picrom_check_launch("small_cholinv");
+}
+
+extern "C" int picrom_small_rmul(const double* a, int r, int k, const double* b,
+                                 const double* colscale, double* out, void* stream) {
+  if (r < 1 || k < 1 || k > SMK) return picrom_set_error(PICROM_ERR_CONFIG, "small_rmul: r >= 1, 1 <= k <= 48");
+  small_rmul_kernel<<<std::min(r, 4 * picrom_num_sms()), SMK, 0, (cudaStream_t)stream>>>(a, r, k, b, colscale, out);
+  return picrom_check_launch("small_rmul");
 }
 
 extern "C" int picrom_argmax_abs(const double* v, long long n, long long stride,

@@ -423,6 +423,35 @@ def _orthonormalize(y, kappa_one=16.0):
     return _mul(y, rinv)
 
 
+def _refine_on_device(W, m0, lam_k, d_eff, iterations, kappa_one=16.0):
+    """Steps 2-3 of _window_svd with the whole Cholesky-QR chain on the device:
+    Y^T Y -> R^-1 (picrom_small_cholinv) -> (W^T Y) R^-1 Sigma^-2
+    (picrom_small_rmul) -> W M (picrom_combine with a device matrix); one host
+    sync, at the Rayleigh-Ritz SVD.  Returns None when a Cholesky factor was
+    not positive definite or not balanced (diag ratio > kappa_one): the caller
+    then runs the host chain with its explicit second round."""
+    inv_lam = torch.from_numpy(np.ascontiguousarray(1.0 / lam_k)).to("cuda")
+    y = _tall.combine_dev(W, torch.from_numpy(np.ascontiguousarray(m0)).to("cuda"))
+    infos = []
+    for _ in range(iterations):
+        rinv, info = _tall.cholinv_dev(_tall.atb(y, y, to_host=False))
+        infos.append(info)
+        y = _tall.combine_dev(W, _tall.rmul_dev(_tall.atb(W, y, to_host=False), rinv, inv_lam))
+    rinv, info = _tall.cholinv_dev(_tall.atb(y, y, to_host=False))
+    infos.append(info)
+    wq = _tall.rmul_dev(_tall.atb(W, y, to_host=False), rinv)           # (c x k) = (Q^T W)^T
+    k = rinv.shape[0]
+    packed = torch.cat([wq.reshape(-1), rinv.reshape(-1)] + infos).cpu().numpy()    # the one sync
+    c = wq.shape[0]
+    diag = packed[c * k + k * k:].reshape(-1, 2)
+    if not (np.all(diag[:, 0] > 0.0) and np.all(diag[:, 1] <= kappa_one * diag[:, 0])):
+        return None
+    qtw = packed[:c * k].reshape(c, k).T
+    rinv_h = packed[c * k:c * k + k * k].reshape(k, k)
+    ub, _, _ = svd(qtw, full_matrices=False)
+    return _mul(y, rinv_h @ ub[:, :d_eff])
+
+
 def _window_svd(window, dim, oversample=8, iterations=1):
     """Leading left singular vectors of the window W (N x c) without forming
     more than an N x (d+q) block; every tall product runs on the library's own
@@ -450,6 +479,11 @@ def _window_svd(window, dim, oversample=8, iterations=1):
     if d_eff < dim:
         warnings.warn(f"DEIM samples have numerical rank {rank} < {dim}; basis reduced to {d_eff}")
     k = min(c, rank, d_eff + oversample, 64)
+    if (k <= 48 and k % 2 == 0 and c % 2 == 0 and c <= 448 and W.stride(1) == 1
+            and W.stride(0) % 2 == 0 and W.data_ptr() % 16 == 0 and W.shape[0] >= 1024):
+        psi = _refine_on_device(W, vec[:, :k] / sing[:k], lam[:k], d_eff, iterations)
+        if psi is not None:
+            return psi, d_eff
     y = _mul(W, vec[:, :k] / sing[:k])
     for _ in range(iterations):
         # W W^T Q ~ Q Sigma^2: dividing column j by sigma_j^2 keeps the block

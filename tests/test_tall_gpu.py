@@ -189,3 +189,59 @@ def test_window_svd_tall_products_helpers(lib_built):
     m = rng.standard_normal((451, 51))
     got = hyper._mul(ad, m).cpu().numpy()
     assert np.abs(got - a @ m).max() <= 1e-12 * np.abs(a @ m).max()
+
+
+@pytest.mark.parametrize("k", [2, 20, 48])
+def test_small_cholinv_and_rmul(lib_built, k):
+    """picrom_small_cholinv / picrom_small_rmul (the device Cholesky-QR chain of
+    the window SVD) against numpy."""
+    import torch
+    from paper_2201_05555_b200 import _tall
+    rng = np.random.default_rng(k)
+    y = rng.standard_normal((500, k)) * np.logspace(0, -1, k)
+    g = y.T @ y
+    rinv, info = _tall.cholinv_dev(torch.from_numpy(g).cuda())
+    r = np.linalg.cholesky(g).T
+    got = rinv.cpu().numpy()
+    assert np.abs(got - np.linalg.inv(r)).max() <= 1e-12 * np.abs(np.linalg.inv(r)).max()
+    q = y @ got
+    assert np.abs(q.T @ q - np.eye(k)).max() <= 1e-12
+    d = np.abs(np.diag(r))
+    np.testing.assert_allclose(info.cpu().numpy(), [d.min(), d.max()], rtol=1e-13)
+    a = rng.standard_normal((421, k))
+    scale = rng.uniform(0.5, 2.0, k)
+    out = _tall.rmul_dev(torch.from_numpy(a).cuda(), rinv, torch.from_numpy(scale).cuda()).cpu().numpy()
+    ref = (a @ got) * scale
+    assert np.abs(out - ref).max() <= 1e-13 * np.abs(ref).max()
+    # not positive definite -> info[0] == 0
+    bad = g.copy()
+    bad[0, 0] = -1.0
+    _, info2 = _tall.cholinv_dev(torch.from_numpy(bad).cuda())
+    assert float(info2[0]) == 0.0
+
+
+def test_window_svd_device_chain_matches_host_chain(lib_built, monkeypatch):
+    """The device-resident Cholesky-QR chain of hyper._window_svd spans the same
+    basis as the host chain (same algorithm, small algebra in LAPACK)."""
+    import torch
+    from paper_2201_05555_b200 import hyper
+    rng = np.random.default_rng(9)
+    rows, cols, dim = 5003, 80, 16
+    left = np.linalg.qr(rng.standard_normal((rows, cols)))[0]
+    right = np.linalg.qr(rng.standard_normal((cols, cols)))[0]
+    samples = torch.from_numpy((left * np.logspace(0, -7, cols)) @ right.T).cuda()
+    win = hyper.DeimWindow(1)
+    win.append(samples)
+    used = []
+    real = hyper._refine_on_device
+    monkeypatch.setattr(hyper, "_refine_on_device", lambda *a, **k: used.append(1) or real(*a, **k))
+    psi_dev, d1 = hyper._window_svd(win, dim)
+    assert used, "the device chain did not run"
+    monkeypatch.setattr(hyper, "_refine_on_device", lambda *a, **k: None)
+    psi_host, d2 = hyper._window_svd(win, dim)
+    assert d1 == d2 == dim
+    a, b = psi_dev.cpu().numpy(), psi_host.cpu().numpy()
+    assert np.abs(a.T @ a - np.eye(dim)).max() <= 1e-12
+    s = np.linalg.svd(a.T @ b, compute_uv=False)
+    assert s.min() > 1 - 1e-13
+    assert np.abs(np.abs(np.diag(a.T @ b)) - 1.0).max() <= 1e-9     # same vectors up to sign
