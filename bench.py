@@ -284,6 +284,15 @@ def fom_measure(args, w, world, local_rank, e2e_steps=None, steps=None, warmup=N
     l2_flush()
     e.launch_block(warmup)
     torch.cuda.synchronize()
+    # the K timed steps are one CUDA-graph replay -- the production schedule of
+    # run_full_order (graph blocks of steps) -- so the timed region holds the K
+    # steps' kernels and no Python launch latency (from Python the first kernel
+    # reaches the GPU ~40 us after the start event: +2-3 us per step at K = 20)
+    timed_graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(timed_graph):
+        e.launch_block(steps)
+    timed_graph.replay()                # untimed: part of the warm-up
+    torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     if world > 1:
         import torch.distributed as tdist
@@ -303,7 +312,7 @@ def fom_measure(args, w, world, local_rank, e2e_steps=None, steps=None, warmup=N
         tdist.barrier()
     torch.cuda.synchronize()
     ev0.record()
-    e.launch_block(steps)               # K steps, every instance group
+    timed_graph.replay()                # exactly K steps, every instance group
     ev1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()

@@ -338,13 +338,17 @@ class PicEngine:
             for k in range(steps):
                 self._launch_group(0, first and k == 0, dev.stream_handle())
             return
+        # group 0 runs on the current stream itself: one fork and one join per
+        # extra group instead of two
         main = torch.cuda.current_stream()
-        for st in self.streams:
+        side = self.streams[1:]
+        for st in side:
             st.wait_stream(main)
         for k in range(steps):
-            for g, st in enumerate(self.streams):
-                self._launch_group(g, first and k == 0, st.cuda_stream)
-        for st in self.streams:
+            for g in range(self.groups):
+                stream = main.cuda_stream if g == 0 else self.streams[g].cuda_stream
+                self._launch_group(g, first and k == 0, stream)
+        for st in side:
             main.wait_stream(st)
 
     def launch(self, first):
