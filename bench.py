@@ -333,10 +333,16 @@ def fom_measure(args, w, world, local_rank, e2e_steps=None, steps=None, warmup=N
     # run_full_order (graph blocks of steps) -- so the timed region holds the K
     # steps' kernels and no Python launch latency (from Python the first kernel
     # reaches the GPU ~40 us after the start event: +2-3 us per step at K = 20)
-    timed_graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(timed_graph):
-        e.launch_block(steps)
-    timed_graph.replay()                # untimed: part of the warm-up
+    timed_block = None
+    try:
+        timed_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(timed_graph):
+            e.launch_block(steps)
+        timed_graph.replay()            # untimed: part of the warm-up
+        timed_block = timed_graph.replay
+    except RuntimeError:                # capture refused (e.g. another stream busy): plain launches
+        torch.cuda.synchronize()
+        timed_block = lambda: e.launch_block(steps)
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     if world > 1:
@@ -357,7 +363,7 @@ def fom_measure(args, w, world, local_rank, e2e_steps=None, steps=None, warmup=N
         tdist.barrier()
     torch.cuda.synchronize()
     ev0.record()
-    timed_graph.replay()                # exactly K steps, every instance group
+    timed_block()                       # exactly K steps, every instance group
     ev1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
